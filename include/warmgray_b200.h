@@ -1,0 +1,175 @@
+/*
+ * warmgray_b200.h -- C ABI of the B200-native warm/cool decolorization path.
+ *
+ * This is the drop-in boundary that replaces the reference's kernel-module
+ * plugin API (`backend.get_kernels(name)` -> module with `NAME` and
+ * `decolor_rows(rgb, out, beta_r, beta_k, row0, row1)`,
+ * /root/reference/pkg/src/warmgray/backend.py:44-52, _kernels.pyx:47-56) and
+ * the NumPy-only stages the reference runs after it (apply_sigmoid,
+ * reinstate_color, quantize_u8 / dequantize_u8; tonemap.py:72-83,172-192,
+ * codec.py:22-29).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch / Python types.
+ *  - Return value: 0 = OK; negative = argument error (the Python layer raises
+ *    ValueError, like the reference's memoryview / validation errors);
+ *    positive = a cudaError_t (raised as RuntimeError). wg_last_error()
+ *    returns a thread-local message for the last failing call.
+ *  - `wg_*` device entry points take DEVICE pointers and a cudaStream_t
+ *    (passed as void*; NULL = legacy default stream). They are asynchronous,
+ *    stream-ordered, allocate nothing and are safe to call concurrently on
+ *    disjoint outputs (the analogue of decolor_rows being re-entrant over
+ *    disjoint row ranges with the GIL released, _kernels.pyx:52).
+ *  - `wg_host_*` entry points take HOST pointers (pinned or pageable) plus a
+ *    device ordinal; they stream chunks host->device->host through
+ *    per-device staging buffers on several CUDA streams and return when the
+ *    output is complete (synchronous, like the reference call).
+ *  - RGB is interleaved (H, W, 3) row-major (C-contiguous), exactly the
+ *    reference's PlanarImage layout (core.py:57-99); a batch of N images is
+ *    (N, H, W, 3). Gray is (H, W) / (N, H, W).
+ *  - beta_r / beta_k must satisfy 0.5 < beta < 1 (core.py:33-51),
+ *    midpoint in [0, 1] and slope > 0 finite (tonemap.py:22-33); violations
+ *    return WG_EINVAL.
+ *  - There is no CPU fallback: every entry point runs on the GPU or fails.
+ */
+#ifndef WARMGRAY_B200_H
+#define WARMGRAY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define WG_API __attribute__((visibility("default")))
+#else
+#define WG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WG_OK 0
+#define WG_EINVAL (-1)      /* bad argument (size, parameter range, null pointer) */
+#define WG_EALIGN (-2)      /* reserved: misaligned buffer where alignment is mandatory */
+#define WG_ESCRATCH (-3)    /* scratch buffer too small */
+#define WG_ENODEV (-4)      /* no CUDA device / bad ordinal */
+
+/* ---- library / device info ------------------------------------------------ */
+WG_API int wg_version(void);                              /* 100 * major + minor */
+WG_API const char* wg_last_error(void);                   /* thread-local; "" when none */
+WG_API int wg_device_count(void);
+WG_API int wg_sm_count(int device);
+
+/* ---- device-pointer, stream-ordered hot path ------------------------------ */
+
+/* uint8 RGB -> uint8 gray, i.e. quantize_u8(decolor_image(dequantize_u8(rgb)))
+ * (codec.py:22-29 around core.py:147-169 / _kernels.pyx:31-56), fused in one
+ * pass over a flat batch of npix pixels: 3 B in, 1 B out per pixel. */
+WG_API int wg_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r, float beta_k,
+                  void* stream);
+
+/* fp32 RGB in [0,1] -> fp32 gray (decolor_image on float data; core.py:147-169). */
+WG_API int wg_decolor_f32(const float* rgb, float* gray, int64_t npix, float beta_r, float beta_k,
+                   void* stream);
+
+/* fp64 RGB -> fp64 gray: replaces _kernels.decolor_rows (_kernels.pyx:47-56)
+ * operation for operation in IEEE fp64 without contraction, so the result is
+ * bit-identical to the reference's compiled backend. */
+WG_API int wg_decolor_f64(const double* rgb, double* gray, int64_t npix, double beta_r, double beta_k,
+                   void* stream);
+
+/* apply_sigmoid (tonemap.py:72-83) on fp64 / fp32 luminance. */
+WG_API int wg_sigmoid_f64(const double* lum, double* out, int64_t n, double midpoint, double slope,
+                   void* stream);
+WG_API int wg_sigmoid_f32(const float* lum, float* out, int64_t n, float midpoint, float slope,
+                   void* stream);
+
+/* reinstate_color (tonemap.py:172-192) on fp64 data. */
+WG_API int wg_reinstate_f64(const double* rgb, const double* l_in, const double* l_out, double* rgb_out,
+                     int64_t npix, void* stream);
+
+/* tonemap_image(mode="global") (tonemap.py:195-216) fused in one fp64 pass:
+ * decolor -> sigmoid -> reinstate; writes l_out (toned luminance) and rgb_out. */
+WG_API int wg_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_out, int64_t npix,
+                          double beta_r, double beta_k, double midpoint, double slope,
+                          void* stream);
+
+/* Fused decolor + global tone map on uint8 RGB:
+ * toned = quantize_u8(apply_sigmoid(decolor(rgb/255))); gray_or_null receives
+ * quantize_u8(decolor(rgb/255)) when non-NULL. */
+WG_API int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null, int64_t npix,
+                       float beta_r, float beta_k, float midpoint, float slope, void* stream);
+
+/* Fused decolor + global tone map on fp32 RGB; gray_or_null gets the
+ * untoned gray, rgb_out_or_null the reinstated colour (tonemap.py:172-192). */
+WG_API int wg_decolor_tone_f32(const float* rgb, float* toned, float* gray_or_null,
+                        float* rgb_out_or_null, int64_t npix, float beta_r, float beta_k,
+                        float midpoint, float slope, void* stream);
+
+/* codec.py:22-29 on device buffers. */
+WG_API int wg_quantize_u8_f64(const double* in, uint8_t* out, int64_t n, void* stream);
+WG_API int wg_dequantize_u8_f64(const uint8_t* in, double* out, int64_t n, void* stream);
+
+/* HDR adapter (no reference counterpart):
+ * nimg fp32 linear-radiance images of pix_per_img pixels -> uint8 via
+ * per-image log-range normalisation of the gray channel, then the global
+ * sigmoid. Two passes with an atomics-free per-block min/max statistic. */
+WG_API size_t wg_hdr_scratch_bytes(int64_t nimg, int64_t pix_per_img);
+WG_API int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
+                      float beta_r, float beta_k, float midpoint, float slope, void* scratch,
+                      size_t scratch_bytes, void* stream);
+
+/* ---- host-buffer entry points (synchronous; pipelined H2D/compute/D2H) ---- */
+
+/* The plugin call itself: fills out[row0:row1] of an (height, width) fp64
+ * gray image from rgb (height, width, 3) fp64, like
+ * _kernels.decolor_rows(rgb, out, beta_r, beta_k, row0, row1). */
+WG_API int wg_host_decolor_rows_f64(const double* rgb, double* out, int64_t height, int64_t width,
+                             double beta_r, double beta_k, int64_t row0, int64_t row1,
+                             int device);
+WG_API int wg_host_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r,
+                       float beta_k, int device);
+WG_API int wg_host_decolor_f32(const float* rgb, float* gray, int64_t npix, float beta_r, float beta_k,
+                        int device);
+WG_API int wg_host_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null,
+                            int64_t npix, float beta_r, float beta_k, float midpoint,
+                            float slope, int device);
+WG_API int wg_host_sigmoid_f64(const double* lum, double* out, int64_t n, double midpoint, double slope,
+                        int device);
+WG_API int wg_host_reinstate_f64(const double* rgb, const double* l_in, const double* l_out,
+                          double* rgb_out, int64_t npix, int device);
+WG_API int wg_host_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_out, int64_t npix,
+                               double beta_r, double beta_k, double midpoint, double slope,
+                               int device);
+WG_API int wg_host_quantize_u8_f64(const double* in, uint8_t* out, int64_t n, int device);
+WG_API int wg_host_dequantize_u8_f64(const uint8_t* in, double* out, int64_t n, int device);
+WG_API int wg_host_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
+                           float beta_r, float beta_k, float midpoint, float slope, int device);
+
+/* ---- synthetic workload generators (bench / test inputs, on device) ------- */
+
+/* C5: i.i.d. uniform bytes from a counter hash of (seed, image, 32-bit word). */
+WG_API int wg_synth_uniform_u8(uint8_t* out, int64_t nimg, int64_t bytes_per_img, uint32_t seed,
+                        int64_t first_image, void* stream);
+/* C3: Voronoi partition (exact int distances, ties -> lowest index) coloured
+ * from a per-image table, plus integer noise -4..4, clipped. seeds_xy
+ * (nimg, nseeds, 2) int32 and colors (nimg, nseeds, 3) u8 are DEVICE arrays. */
+WG_API int wg_synth_voronoi_u8(uint8_t* out, int64_t nimg, int32_t width, int32_t height,
+                        const int32_t* seeds_xy, const uint8_t* colors, int32_t nseeds,
+                        uint32_t seed, int64_t first_image, void* stream);
+/* C2: Gaussian colour blobs over a mid-gray base plus uniform noise, clipped
+ * to [0,1]. blobs: (nimg, nblobs, 8) fp32 device table
+ * {cx, cy, inv_two_sigma2, amp, r, g, b, 0}; base: (nimg,) fp32. */
+WG_API int wg_synth_blobs_f32(float* out, int64_t nimg, int32_t width, int32_t height,
+                       const float* blobs, int32_t nblobs, const float* base, float noise,
+                       uint32_t seed, int64_t first_image, void* stream);
+/* C4: i.i.d. HDR radiance: luminance log-uniform in [lum_lo, lum_hi],
+ * saturated hue mixed with white, scaled so BT.709 Y equals the luminance. */
+WG_API int wg_synth_hdr_f32(float* out, int64_t nimg, int64_t pix_per_img, float lum_lo, float lum_hi,
+                     uint32_t seed, int64_t first_image, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WARMGRAY_B200_H */

@@ -1,0 +1,323 @@
+/*
+ * warmgray_oracle.c -- CPU ORACLE. TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain-C, fp64, scalar restatement of the reference's per-pixel hot path
+ * (package `warmgray`, /root/reference/pkg/src/warmgray). Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * may load this library, and only as the CHECKER or as the timed CPU
+ * baseline -- never as the product path (the product is the CUDA library in
+ * paper_2108_13656_b200/, which has no CPU fallback).
+ *
+ * Pinning: tests/test_oracle_golden.py checks this restatement against the
+ * golden vectors produced by the reference itself (tests/golden/, generated
+ * by tests/golden/make_golden.py from both reference backends), including
+ * the sha256 of the reference's fp64 output over all 2^24 uint8 colours.
+ *
+ * Arithmetic provenance: the reference kernel is Cython compiled with
+ * `gcc -O3` and no -march (setup.py:9), i.e. SSE2 fp64 without FMA
+ * contraction; libm sqrt is correctly rounded. This file is compiled with
+ * -O3 -ffp-contract=off and evaluates every expression in the same order,
+ * so it is bit-identical to `_kernels.decolor_rows`.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_API __attribute__((visibility("default")))
+
+/* _kernels.pyx:23-28 (_clamp01); core.py:144 */
+static inline double clamp01(double v) {
+    if (v < 0.0) return 0.0;
+    if (v > 1.0) return 1.0;
+    return v;
+}
+
+/* Eqs. 1-6, following _kernels.pyx:31-44 (_decolor_px) operation for
+ * operation; scalar oracle in core.py:102-144 states the same model. */
+static inline double decolor_px(double r, double g, double b, double beta_r, double beta_k) {
+    double white = sqrt((r * r + g * g + b * b) / 3.0);        /* Eq. 1 */
+    double s = r + g + b;
+    double wr = 0.0, wb = 0.0;
+    if (s > 0.0) {                                              /* black: shares 0 */
+        wr = r / s;
+        wb = b / s;
+    }
+    double redgreen = sqrt(beta_r * r * r + (1.0 - beta_r) * g * g);   /* Eq. 3 */
+    double warm = wr * redgreen + (1.0 - wr) * white;                 /* Eq. 4 */
+    double cool = (1.0 - wb) * b + wb * white;                        /* Eq. 5 (L_B = b, Eq. 2) */
+    return clamp01(sqrt(beta_k * warm * warm + (1.0 - beta_k) * cool * cool)); /* Eq. 6 */
+}
+
+/* codec.py:22-25: floor(clip(v, 0, 1) * 255 + 0.5) */
+static inline uint8_t quantize(double v) {
+    double c = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    return (uint8_t)floor(c * 255.0 + 0.5);
+}
+
+/* codec.py:28-29: k / 255.0 */
+static inline double dequantize(uint8_t k) { return (double)k / 255.0; }
+
+/* tonemap.py:72-83 (apply_sigmoid): logistic curve renormalised so 0->0, 1->1. */
+typedef struct { double m, k, lo, hi; } sig_t;
+static inline sig_t sig_make(double m, double k) {
+    sig_t s;
+    s.m = m;
+    s.k = k;
+    s.lo = 1.0 / (1.0 + exp(k * m));
+    s.hi = 1.0 / (1.0 + exp(-k * (1.0 - m)));
+    return s;
+}
+static inline double sig_apply(const sig_t* s, double x) {
+    double y = 1.0 / (1.0 + exp(-s->k * (x - s->m)));
+    double out = (y - s->lo) / (s->hi - s->lo);
+    return clamp01(out);
+}
+
+/* ------------------------------------------------------------------ */
+/* row-span thread pool, the analogue of backend.run_rows (backend.py:65-81) */
+
+typedef void (*span_fn)(void* ctx, int64_t p0, int64_t p1);
+typedef struct { span_fn fn; void* ctx; int64_t p0, p1; } span_job;
+
+static void* span_thread(void* arg) {
+    span_job* j = (span_job*)arg;
+    j->fn(j->ctx, j->p0, j->p1);
+    return NULL;
+}
+
+static void run_spans(int64_t n, int threads, span_fn fn, void* ctx) {
+    if (n <= 0) return;
+    if (threads < 1) threads = 1;
+    if (threads > n) threads = (int)n;
+    if (threads == 1) {
+        fn(ctx, 0, n);
+        return;
+    }
+    int64_t chunk = (n + threads - 1) / threads;
+    pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    span_job* jobs = (span_job*)calloc((size_t)threads, sizeof(span_job));
+    int started = 0;
+    for (int t = 0; t < threads; ++t) {
+        int64_t p0 = (int64_t)t * chunk, p1 = p0 + chunk > n ? n : p0 + chunk;
+        if (p0 >= p1) break;
+        jobs[t].fn = fn; jobs[t].ctx = ctx; jobs[t].p0 = p0; jobs[t].p1 = p1;
+        if (pthread_create(&tid[t], NULL, span_thread, &jobs[t]) != 0) {
+            span_thread(&jobs[t]);  /* degrade to inline on failure */
+            tid[t] = 0;
+        }
+        ++started;
+    }
+    for (int t = 0; t < started; ++t)
+        if (tid[t]) pthread_join(tid[t], NULL);
+    free(tid);
+    free(jobs);
+}
+
+/* ------------------------------------------------------------------ */
+/* decolor, fp64 in -> fp64 out (the reference kernel's own representation) */
+
+typedef struct { const double* rgb; double* out; double br, bk; } dec64_ctx;
+static void dec64_span(void* c, int64_t p0, int64_t p1) {
+    dec64_ctx* x = (dec64_ctx*)c;
+    for (int64_t i = p0; i < p1; ++i)
+        x->out[i] = decolor_px(x->rgb[3 * i], x->rgb[3 * i + 1], x->rgb[3 * i + 2], x->br, x->bk);
+}
+OR_API void or_decolor_f64(const double* rgb, double* out, int64_t npix, double beta_r,
+                           double beta_k, int threads) {
+    dec64_ctx c = {rgb, out, beta_r, beta_k};
+    run_spans(npix, threads, dec64_span, &c);
+}
+
+/* fp32 samples promoted exactly to fp64 (PlanarImage stores float64; core.py:68) */
+typedef struct { const float* rgb; double* out; double br, bk; } dec32_ctx;
+static void dec32_span(void* c, int64_t p0, int64_t p1) {
+    dec32_ctx* x = (dec32_ctx*)c;
+    for (int64_t i = p0; i < p1; ++i)
+        x->out[i] = decolor_px((double)x->rgb[3 * i], (double)x->rgb[3 * i + 1],
+                               (double)x->rgb[3 * i + 2], x->br, x->bk);
+}
+OR_API void or_decolor_f32in(const float* rgb, double* out, int64_t npix, double beta_r,
+                             double beta_k, int threads) {
+    dec32_ctx c = {rgb, out, beta_r, beta_k};
+    run_spans(npix, threads, dec32_span, &c);
+}
+
+/* uint8 -> uint8: quantize_u8(decolor_image(PlanarImage(dequantize_u8(u8))).data) */
+typedef struct { const uint8_t* rgb; uint8_t* out; double br, bk; } dec8_ctx;
+static void dec8_span(void* c, int64_t p0, int64_t p1) {
+    dec8_ctx* x = (dec8_ctx*)c;
+    for (int64_t i = p0; i < p1; ++i)
+        x->out[i] = quantize(decolor_px(dequantize(x->rgb[3 * i]), dequantize(x->rgb[3 * i + 1]),
+                                        dequantize(x->rgb[3 * i + 2]), x->br, x->bk));
+}
+OR_API void or_decolor_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, double beta_r,
+                          double beta_k, int threads) {
+    dec8_ctx c = {rgb, out, beta_r, beta_k};
+    run_spans(npix, threads, dec8_span, &c);
+}
+
+/* apply_sigmoid on fp64 luminance (tonemap.py:72-83) */
+OR_API void or_sigmoid_f64(const double* in, double* out, int64_t n, double midpoint,
+                           double slope) {
+    sig_t s = sig_make(midpoint, slope);
+    for (int64_t i = 0; i < n; ++i) out[i] = sig_apply(&s, in[i]);
+}
+
+/* reinstate_color (tonemap.py:172-192): clip(c * l_out / max(l_in, 1e-6)), l_in == 0 -> 0 */
+OR_API void or_reinstate_f64(const double* rgb, const double* l_in, const double* l_out,
+                             double* out, int64_t npix) {
+    for (int64_t i = 0; i < npix; ++i) {
+        double li = l_in[i];
+        double ratio = l_out[i] / (li > 1e-6 ? li : 1e-6);
+        for (int c = 0; c < 3; ++c) {
+            double v = clamp01(rgb[3 * i + c] * ratio);
+            out[3 * i + c] = li == 0.0 ? 0.0 : v;
+        }
+    }
+}
+
+/* u8 -> toned u8 via the global tone map:
+ * quantize_u8(apply_sigmoid(decolor_image(dequantize_u8(u8))).data); optional
+ * gray u8 = quantize_u8(decolor_image(...)). */
+typedef struct { const uint8_t* rgb; uint8_t* toned; uint8_t* gray; double br, bk; sig_t s; } tone8_ctx;
+static void tone8_span(void* c, int64_t p0, int64_t p1) {
+    tone8_ctx* x = (tone8_ctx*)c;
+    for (int64_t i = p0; i < p1; ++i) {
+        double g = decolor_px(dequantize(x->rgb[3 * i]), dequantize(x->rgb[3 * i + 1]),
+                              dequantize(x->rgb[3 * i + 2]), x->br, x->bk);
+        x->toned[i] = quantize(sig_apply(&x->s, g));
+        if (x->gray) x->gray[i] = quantize(g);
+    }
+}
+OR_API void or_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray, int64_t npix,
+                       double beta_r, double beta_k, double midpoint, double slope, int threads) {
+    tone8_ctx c = {rgb, toned, gray, beta_r, beta_k, sig_make(midpoint, slope)};
+    run_spans(npix, threads, tone8_span, &c);
+}
+
+/* fp64 rgb -> (toned luminance, reinstated rgb): tonemap_image(mode="global")
+ * (tonemap.py:195-216) = decolor -> apply_sigmoid -> reinstate_color. */
+OR_API void or_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_out, int64_t npix,
+                                  double beta_r, double beta_k, double midpoint, double slope) {
+    sig_t s = sig_make(midpoint, slope);
+    for (int64_t i = 0; i < npix; ++i) {
+        double li = decolor_px(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], beta_r, beta_k);
+        double lo = sig_apply(&s, li);
+        l_out[i] = lo;
+        double ratio = lo / (li > 1e-6 ? li : 1e-6);
+        for (int c = 0; c < 3; ++c) {
+            double v = clamp01(rgb[3 * i + c] * ratio);
+            rgb_out[3 * i + c] = li == 0.0 ? 0.0 : v;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------ */
+/* HDR adapter. No reference counterpart: the
+ * reference rejects samples > 1 (core.py:78-79) and lists HDR ingestion as a
+ * non-goal. Builder-defined, restated here on top of the
+ * reference's own operators:
+ *   M  = max over the image's samples;  gn = decolor_image(x / M)  (clamp inactive)
+ *   t  = log(gn / gmin) / log(gmax / gmin) over gn > 0, gmin/gmax over gn > 0
+ *   t  = 0 where gn == 0;  t = 1 for gn > 0 when gmax == gmin
+ *   out = quantize_u8(apply_sigmoid(t, curve))
+ * Scale cancels in t, so the device may decolorize the raw radiance. */
+typedef struct {
+    const float* rgb; uint8_t* out; int64_t ppi; double br, bk; sig_t s;
+} hdr_ctx;
+static void hdr_span(void* c, int64_t i0, int64_t i1) {
+    hdr_ctx* x = (hdr_ctx*)c;
+    double* g = (double*)malloc((size_t)x->ppi * sizeof(double));
+    for (int64_t im = i0; im < i1; ++im) {
+        const float* px = x->rgb + im * x->ppi * 3;
+        uint8_t* o = x->out + im * x->ppi;
+        double M = 0.0;
+        for (int64_t j = 0; j < x->ppi * 3; ++j)
+            if ((double)px[j] > M) M = (double)px[j];
+        double gmin = INFINITY, gmax = 0.0;
+        for (int64_t j = 0; j < x->ppi; ++j) {
+            double gv = 0.0;
+            if (M > 0.0)
+                gv = decolor_px((double)px[3 * j] / M, (double)px[3 * j + 1] / M,
+                                (double)px[3 * j + 2] / M, x->br, x->bk);
+            g[j] = gv;
+            if (gv > 0.0) {
+                if (gv < gmin) gmin = gv;
+                if (gv > gmax) gmax = gv;
+            }
+        }
+        double lrange = gmax > gmin ? log(gmax / gmin) : 0.0;
+        for (int64_t j = 0; j < x->ppi; ++j) {
+            double t;
+            if (!(g[j] > 0.0)) t = 0.0;
+            else if (lrange > 0.0) t = clamp01(log(g[j] / gmin) / lrange);
+            else t = 1.0;
+            o[j] = quantize(sig_apply(&x->s, t));
+        }
+    }
+    free(g);
+}
+OR_API void or_hdr_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
+                      double beta_r, double beta_k, double midpoint, double slope, int threads) {
+    hdr_ctx c = {rgb, out, pix_per_img, beta_r, beta_k, sig_make(midpoint, slope)};
+    run_spans(nimg, threads, hdr_span, &c);
+}
+
+/* ------------------------------------------------------------------ */
+/* Synthetic-workload restatements (integer-exact, so the device generators
+ * in paper_2108_13656_b200/csrc/wg_synth.cu can be checked bit for bit). */
+
+/* lowbias32 integer hash (public-domain mixer by C. Wellons) */
+static inline uint32_t mix32(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352dU;
+    x ^= x >> 15; x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+static inline uint32_t hash3(uint32_t seed, uint32_t image, uint32_t ctr) {
+    return mix32(ctr ^ mix32(image ^ mix32(seed ^ 0x9e3779b9U)));
+}
+
+/* C5: i.i.d. uniform bytes; 32-bit word w of image i holds bytes 4w..4w+3 */
+OR_API void or_synth_uniform_u8(uint8_t* out, int64_t nimg, int64_t bytes_per_img,
+                                uint32_t seed, int64_t first_image) {
+    for (int64_t im = 0; im < nimg; ++im) {
+        uint8_t* o = out + im * bytes_per_img;
+        for (int64_t j = 0; j < bytes_per_img; ++j) {
+            uint32_t h = hash3(seed, (uint32_t)(first_image + im), (uint32_t)(j >> 2));
+            o[j] = (uint8_t)(h >> (8 * (j & 3)));
+        }
+    }
+}
+
+/* C3: Voronoi cells, exact integer squared distance, ties -> lowest index;
+ * cell colour + per-channel integer noise in -4..4, clipped to 0..255.
+ * seeds_xy: (nimg, nseeds, 2) int32; colors: (nimg, nseeds, 3) uint8. */
+OR_API void or_synth_voronoi_u8(uint8_t* out, int64_t nimg, int32_t width, int32_t height,
+                                const int32_t* seeds_xy, const uint8_t* colors, int32_t nseeds,
+                                uint32_t seed, int64_t first_image) {
+    for (int64_t im = 0; im < nimg; ++im) {
+        const int32_t* sxy = seeds_xy + im * nseeds * 2;
+        const uint8_t* col = colors + im * nseeds * 3;
+        uint8_t* o = out + im * (int64_t)width * height * 3;
+        for (int32_t y = 0; y < height; ++y)
+            for (int32_t x = 0; x < width; ++x) {
+                int32_t best = 0;
+                int64_t bd = INT64_MAX;
+                for (int32_t k = 0; k < nseeds; ++k) {
+                    int64_t dx = x - sxy[2 * k], dy = y - sxy[2 * k + 1];
+                    int64_t d = dx * dx + dy * dy;
+                    if (d < bd) { bd = d; best = k; }
+                }
+                int64_t p = (int64_t)y * width + x;
+                uint32_t h = hash3(seed ^ 0x5bd1e995U, (uint32_t)(first_image + im), (uint32_t)p);
+                for (int c = 0; c < 3; ++c) {
+                    int n = (int)((h >> (10 * c)) & 1023U) % 9 - 4;
+                    int v = (int)col[3 * best + c] + n;
+                    o[3 * p + c] = (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+                }
+            }
+    }
+}

@@ -1,0 +1,219 @@
+"""Flat-batch API: the throughput path.
+
+Two flavours over the same C ABI (include/warmgray_b200.h):
+
+* ``decolor`` / ``decolor_tone`` / ``hdr_tonemap`` / ``sigmoid`` take CUDA
+  ``torch.Tensor`` batches that are already resident in HBM (N, H, W, 3)
+  (or any (..., 3) shape) and launch on the caller's current stream. One
+  launch covers the whole batch: images are independent and the kernels
+  are per-pixel maps (HDR adds a per-image statistic), so there is no
+  per-image launch overhead.
+* ``decolor_host`` / ``decolor_tone_host`` / ``hdr_tonemap_host`` take host
+  NumPy arrays and run the pipelined host->device->host path
+  (wg_host_*), the batch analogue of the reference's ``decolor_rows``
+  plugin call on host memory.
+
+uint8 inputs produce uint8 outputs bit-for-bit equal to
+``quantize_u8(decolor_image(dequantize_u8(x)))`` except for at most +-1 on
+rounding ties; fp32 inputs produce fp32 gray within 1e-6 of the fp64
+reference; fp64 inputs reproduce the reference's compiled backend exactly.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .backend import get_device
+from .core import DEFAULT_PARAMS, DecolorParams
+from .tonemap import SigmoidCurve
+
+_DECOLOR_FN = {"uint8": "wg_decolor_u8", "float32": "wg_decolor_f32", "float64": "wg_decolor_f64"}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _check_rgb_tensor(rgb, dtypes):
+    torch = _torch()
+    if not isinstance(rgb, torch.Tensor):
+        raise TypeError(f"expected a torch.Tensor, got {type(rgb).__name__}")
+    if not rgb.is_cuda:
+        raise ValueError("expected a CUDA tensor (use the *_host functions for host arrays)")
+    if rgb.dim() < 1 or rgb.shape[-1] != 3:
+        raise ValueError(f"rgb needs a trailing channel axis of 3, got shape {tuple(rgb.shape)}")
+    if not rgb.is_contiguous():
+        raise ValueError("rgb must be contiguous (interleaved HWC)")
+    name = str(rgb.dtype).replace("torch.", "")
+    if name not in dtypes:
+        raise ValueError(f"unsupported dtype {rgb.dtype} (have: {', '.join(dtypes)})")
+    return name
+
+
+def _stream(stream, device):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return s.cuda_stream
+
+
+def decolor(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, stream=None):
+    """Gray of a device-resident (..., 3) uint8 / float32 / float64 batch."""
+    torch = _torch()
+    name = _check_rgb_tensor(rgb, _DECOLOR_FN)
+    if out is None:
+        out = torch.empty(rgb.shape[:-1], dtype=rgb.dtype, device=rgb.device)
+    elif out.shape != rgb.shape[:-1] or out.dtype != rgb.dtype or not out.is_contiguous() \
+            or out.device != rgb.device:
+        raise ValueError("out must be a contiguous tensor of shape rgb.shape[:-1], same dtype/device")
+    n = out.numel()
+    with torch.cuda.device(rgb.device):
+        _lib.call(_DECOLOR_FN[name], rgb.data_ptr(), out.data_ptr(), n, params.beta_r,
+                  params.beta_k, _stream(stream, rgb.device))
+    return out
+
+
+def decolor_tone(rgb, curve: SigmoidCurve = SigmoidCurve(), params: DecolorParams = DEFAULT_PARAMS,
+                 return_gray: bool = False, return_rgb: bool = False, stream=None):
+    """Fused decolor + global sigmoid on a device batch.
+
+    uint8 -> toned uint8 (and gray uint8 if ``return_gray``);
+    float32 -> toned float32 (+ gray, + reinstated rgb if requested).
+    Returns the toned tensor, or a tuple ``(toned, gray, rgb_out)`` with
+    ``None`` for outputs not requested when either flag is set.
+    """
+    torch = _torch()
+    name = _check_rgb_tensor(rgb, ("uint8", "float32"))
+    shape = rgb.shape[:-1]
+    toned = torch.empty(shape, dtype=rgb.dtype, device=rgb.device)
+    gray = torch.empty(shape, dtype=rgb.dtype, device=rgb.device) if return_gray else None
+    rgb_out = None
+    with torch.cuda.device(rgb.device):
+        st = _stream(stream, rgb.device)
+        if name == "uint8":
+            if return_rgb:
+                raise ValueError("return_rgb is supported for float32 input only")
+            _lib.call("wg_decolor_tone_u8", rgb.data_ptr(), toned.data_ptr(),
+                      gray.data_ptr() if gray is not None else None, toned.numel(),
+                      params.beta_r, params.beta_k, curve.midpoint, curve.slope, st)
+        else:
+            rgb_out = torch.empty_like(rgb) if return_rgb else None
+            _lib.call("wg_decolor_tone_f32", rgb.data_ptr(), toned.data_ptr(),
+                      gray.data_ptr() if gray is not None else None,
+                      rgb_out.data_ptr() if rgb_out is not None else None, toned.numel(),
+                      params.beta_r, params.beta_k, curve.midpoint, curve.slope, st)
+    if return_gray or return_rgb:
+        return toned, gray, rgb_out
+    return toned
+
+
+def sigmoid(lum, curve: SigmoidCurve = SigmoidCurve(), stream=None):
+    """apply_sigmoid on a device float32 / float64 tensor."""
+    torch = _torch()
+    if not isinstance(lum, torch.Tensor) or not lum.is_cuda or not lum.is_contiguous():
+        raise ValueError("expected a contiguous CUDA tensor")
+    fn = {torch.float32: "wg_sigmoid_f32", torch.float64: "wg_sigmoid_f64"}.get(lum.dtype)
+    if fn is None:
+        raise ValueError(f"unsupported dtype {lum.dtype}")
+    out = torch.empty_like(lum)
+    with torch.cuda.device(lum.device):
+        _lib.call(fn, lum.data_ptr(), out.data_ptr(), lum.numel(), curve.midpoint, curve.slope,
+                  _stream(stream, lum.device))
+    return out
+
+
+class HdrScratch:
+    """Reusable device scratch for :func:`hdr_tonemap` (gray plane + per-block partials)."""
+
+    def __init__(self, nimg: int, pix_per_img: int, device=None):
+        torch = _torch()
+        self.nbytes = int(_lib.load().wg_hdr_scratch_bytes(nimg, pix_per_img))
+        self.buf = torch.empty(max(self.nbytes, 1), dtype=torch.uint8,
+                               device=device if device is not None else "cuda")
+
+
+def hdr_tonemap(rgb, params: DecolorParams = DEFAULT_PARAMS, curve: SigmoidCurve = SigmoidCurve(),
+                scratch: HdrScratch | None = None, out=None, stream=None):
+    """HDR adapter on a device (N, H, W, 3) float32 radiance batch -> uint8."""
+    torch = _torch()
+    _check_rgb_tensor(rgb, ("float32",))
+    if rgb.dim() < 2:
+        raise ValueError("hdr_tonemap expects a batch (N, ..., 3)")
+    n = rgb.shape[0]
+    ppi = rgb[0].numel() // 3 if n else 0
+    if out is None:
+        out = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=rgb.device)
+    need = int(_lib.load().wg_hdr_scratch_bytes(n, ppi))
+    if scratch is None or scratch.nbytes < need:
+        scratch = HdrScratch(n, ppi, device=rgb.device)
+    with torch.cuda.device(rgb.device):
+        _lib.call("wg_hdr_tonemap_u8", rgb.data_ptr(), out.data_ptr(), n, ppi, params.beta_r,
+                  params.beta_k, curve.midpoint, curve.slope, scratch.buf.data_ptr(),
+                  scratch.nbytes, _stream(stream, rgb.device))
+    return out
+
+
+# ---------------------------------------------------------------- host-array flavour
+
+def _host_rgb(rgb, dtypes):
+    arr = np.asarray(rgb)
+    if arr.ndim < 1 or arr.shape[-1] != 3:
+        raise ValueError(f"rgb needs a trailing channel axis of 3, got shape {arr.shape}")
+    if arr.dtype.name not in dtypes:
+        raise ValueError(f"unsupported dtype {arr.dtype} (have: {', '.join(dtypes)})")
+    return np.ascontiguousarray(arr)
+
+
+def decolor_host(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, device: int | None = None):
+    """Gray of a host (..., 3) uint8 / float32 / float64 array via the pipelined host path."""
+    arr = _host_rgb(rgb, ("uint8", "float32", "float64"))
+    if out is None:
+        out = np.empty(arr.shape[:-1], dtype=arr.dtype)
+    elif out.shape != arr.shape[:-1] or out.dtype != arr.dtype or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError("out must be C-contiguous with shape rgb.shape[:-1] and rgb's dtype")
+    dev = get_device() if device is None else device
+    n = out.size
+    if n:
+        if arr.dtype == np.uint8:
+            _lib.call("wg_host_decolor_u8", arr.ctypes.data, out.ctypes.data, n, params.beta_r,
+                      params.beta_k, dev)
+        elif arr.dtype == np.float32:
+            _lib.call("wg_host_decolor_f32", arr.ctypes.data, out.ctypes.data, n, params.beta_r,
+                      params.beta_k, dev)
+        else:
+            _lib.call("wg_host_decolor_rows_f64", arr.ctypes.data, out.ctypes.data, 1, n,
+                      params.beta_r, params.beta_k, 0, 1, dev)
+    return out
+
+
+def decolor_tone_host(rgb, curve: SigmoidCurve = SigmoidCurve(),
+                      params: DecolorParams = DEFAULT_PARAMS, return_gray: bool = False,
+                      device: int | None = None):
+    """Fused decolor + global sigmoid of a host uint8 (..., 3) array -> toned uint8 (+ gray)."""
+    arr = _host_rgb(rgb, ("uint8",))
+    toned = np.empty(arr.shape[:-1], dtype=np.uint8)
+    gray = np.empty_like(toned) if return_gray else None
+    if toned.size:
+        _lib.call("wg_host_decolor_tone_u8", arr.ctypes.data, toned.ctypes.data,
+                  gray.ctypes.data if gray is not None else None, toned.size, params.beta_r,
+                  params.beta_k, curve.midpoint, curve.slope,
+                  get_device() if device is None else device)
+    return (toned, gray) if return_gray else toned
+
+
+def hdr_tonemap_host(rgb, params: DecolorParams = DEFAULT_PARAMS,
+                     curve: SigmoidCurve = SigmoidCurve(), device: int | None = None):
+    """HDR adapter on a host (N, H, W, 3) float32 batch -> (N, H, W) uint8."""
+    arr = _host_rgb(rgb, ("float32",))
+    if arr.ndim < 2:
+        raise ValueError("hdr_tonemap_host expects a batch (N, ..., 3)")
+    out = np.empty(arr.shape[:-1], dtype=np.uint8)
+    n = arr.shape[0]
+    ppi = out.size // n if n else 0
+    if out.size:
+        _lib.call("wg_host_hdr_tonemap_u8", arr.ctypes.data, out.ctypes.data, n, ppi,
+                  params.beta_r, params.beta_k, curve.midpoint, curve.slope,
+                  get_device() if device is None else device)
+    return out

@@ -1,0 +1,334 @@
+// wg_device.cuh -- device-side building blocks for the sm_100a decolorization
+// kernels: PTX wrappers (mbarrier, cp.async.bulk, packed f32x2 math, MUFU)
+// and the three per-pixel formulations of the warm/cool model (Eqs. 1-6,
+// reference _kernels.pyx:31-44 / core.py:102-144):
+//
+//   decolor255_x2   uint8 path: two pixels per packed f32x2 lane pair, in the
+//                   0..255 domain (homogeneity), 3 MUFU / px, no divide.
+//   decolor_acc     fp32 path: IEEE sqrt / reciprocal, <= ~2e-7 abs error.
+//   decolor_f64     fp64 path: the reference's operation order with explicit
+//                   round-to-nearest intrinsics (no FMA contraction), hence
+//                   bit-identical to the reference's compiled backend.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace wg {
+
+// ---------------------------------------------------------------- PTX: smem / mbarrier / bulk copy
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// One-thread bulk copy global -> shared (TMA engine, no tensor map needed for a
+// contiguous byte range); completion is signalled on `bar` as tx bytes.
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void st_global_cs_v4(void* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// ---------------------------------------------------------------- packed f32x2 (FFMA2 / FMUL2 / FADD2)
+__device__ __forceinline__ unsigned long long pk(float2 a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 upk(unsigned long long r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)), "l"(pk(c)));
+    return upk(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)));
+    return upk(d);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)));
+    return upk(d);
+}
+__device__ __forceinline__ float2 add2_rz(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)));
+    return upk(d);
+}
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+
+// ---------------------------------------------------------------- MUFU
+__device__ __forceinline__ float sqrt_mufu(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rsqrt_mufu(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// ---------------------------------------------------------------- byte <-> float
+// 0x4B0000bb as float is 2^23 + bb: one PRMT inserts the byte, one packed
+// FADD removes the 2^23 bias (exact), instead of a quarter-rate I2F.
+constexpr float kMagic = 8388608.0f;  // 2^23
+__device__ __forceinline__ float byte_biased(uint32_t w, int k) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | static_cast<uint32_t>(k)));
+}
+// low bytes of a and b -> bytes 0,1 of the result
+__device__ __forceinline__ uint32_t pack_lo2(float a, float b) {
+    return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x0040u);
+}
+
+// ---------------------------------------------------------------- uint8 path (0..255 domain)
+// With r, g, b the raw byte values and S = r + g + b (homogeneity lets the
+// whole model run in the 0..255 domain, so gray*255 comes out directly):
+//   W   = sqrt(r^2 + g^2 + b^2)                  (= sqrt(3) * white, Eq. 1)
+//   RGq = sqrt(cr r^2 + g^2), cr = br/(1-br)     (= RG / sqrt(1-br), Eq. 3)
+//   A   = c1 r RGq + (g+b) W                     (= sqrt(3) * S * warm, Eq. 4)
+//   B   = b (sqrt(3)(r+g) + W)                   (= sqrt(3) * S * cool, Eqs. 2, 5)
+//   T   = A^2 + c3 B^2, c3 = (1-bk)/bk
+//   gray255 = c4 * sqrt(T) / S = c4 * T * rsqrt(T S^2 + tiny),  c4 = sqrt(bk/3)   (Eq. 6)
+// 3 MUFU (2 sqrt, 1 rsqrt) and no divide per pixel; the tiny bias makes black
+// (T = S = 0) come out 0 instead of 0*inf. gray <= max(r,g,b) <= 255, so no
+// clamp is needed before round-half-up (codec.py:22-25), done as
+// floor(v + 0.5) via a round-toward-zero add of 2^23 whose low byte is the
+// result.
+struct U8Consts {
+    float cr, c1, sqrt3, c3, c4;
+};
+
+inline U8Consts make_u8_consts(float beta_r, float beta_k) {
+    // derive in double, round once to fp32
+    double br = beta_r, bk = beta_k;
+    U8Consts k;
+    k.cr = static_cast<float>(br / (1.0 - br));
+    k.c1 = static_cast<float>(1.7320508075688772 * std::sqrt(1.0 - br));
+    k.sqrt3 = 1.7320508075688772f;
+    k.c3 = static_cast<float>((1.0 - bk) / bk);
+    k.c4 = static_cast<float>(std::sqrt(bk / 3.0));
+    return k;
+}
+
+// Returns 2^23 + floor(gray255 + 0.5) per lane (low byte = the uint8 gray).
+__device__ __forceinline__ float2 decolor255_x2(float2 R, float2 G, float2 B, const U8Consts& k) {
+    float2 G2 = mul2(G, G);
+    float2 q = fma2(B, B, G2);
+    q = fma2(R, R, q);
+    float2 Rc = mul2(R, bc2(k.cr));
+    float2 rgq = fma2(Rc, R, G2);
+    float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
+    float2 RGq = make_float2(sqrt_mufu(rgq.x), sqrt_mufu(rgq.y));
+    float2 RG = add2(R, G);
+    float2 S = add2(RG, B);
+    float2 GB = add2(G, B);
+    float2 Rc1 = mul2(R, bc2(k.c1));
+    float2 t1 = mul2(GB, W);
+    float2 A = fma2(Rc1, RGq, t1);
+    float2 u = fma2(RG, bc2(k.sqrt3), W);
+    float2 Bp = mul2(B, u);
+    float2 Bc = mul2(Bp, bc2(k.c3));
+    float2 T1 = mul2(Bc, Bp);
+    float2 T = fma2(A, A, T1);
+    float2 S2 = mul2(S, S);
+    float2 X = fma2(T, S2, bc2(1e-30f));
+    float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
+    float2 z = mul2(T, y);
+    float2 v = fma2(z, bc2(k.c4), bc2(0.5f));
+    return add2_rz(v, bc2(kMagic));
+}
+
+// Scalar twin of decolor255_x2 with the identical per-lane operation
+// sequence (IEEE rn ops are lane-exact), so tails / unaligned buffers give
+// bit-identical bytes to the vector path.
+__device__ __forceinline__ uint8_t decolor255_x1(float r, float g, float b, const U8Consts& k) {
+    float G2 = __fmul_rn(g, g);
+    float q = __fmaf_rn(b, b, G2);
+    q = __fmaf_rn(r, r, q);
+    float Rc = __fmul_rn(r, k.cr);
+    float rgq = __fmaf_rn(Rc, r, G2);
+    float W = sqrt_mufu(q);
+    float RGq = sqrt_mufu(rgq);
+    float RG = __fadd_rn(r, g);
+    float S = __fadd_rn(RG, b);
+    float GB = __fadd_rn(g, b);
+    float Rc1 = __fmul_rn(r, k.c1);
+    float t1 = __fmul_rn(GB, W);
+    float A = __fmaf_rn(Rc1, RGq, t1);
+    float u = __fmaf_rn(RG, k.sqrt3, W);
+    float Bp = __fmul_rn(b, u);
+    float Bc = __fmul_rn(Bp, k.c3);
+    float T1 = __fmul_rn(Bc, Bp);
+    float T = __fmaf_rn(A, A, T1);
+    float S2 = __fmul_rn(S, S);
+    float X = __fmaf_rn(T, S2, 1e-30f);
+    float y = rsqrt_mufu(X);
+    float z = __fmul_rn(T, y);
+    float v = __fmaf_rn(z, k.c4, 0.5f);
+    return static_cast<uint8_t>(__float_as_uint(__fadd_rz(v, kMagic)) & 0xFFu);
+}
+
+// ---------------------------------------------------------------- fp32 path (accurate)
+struct AccConsts {
+    float br, omr, bk, omk;
+};
+inline AccConsts make_acc_consts(float beta_r, float beta_k) {
+    AccConsts k;
+    k.br = beta_r;
+    k.omr = static_cast<float>(1.0 - static_cast<double>(beta_r));
+    k.bk = beta_k;
+    k.omk = static_cast<float>(1.0 - static_cast<double>(beta_k));
+    return k;
+}
+
+// Unclamped gray of an fp32 pixel (any non-negative scale: used on raw HDR
+// radiance too, where homogeneity makes the clamp meaningless).
+__device__ __forceinline__ float decolor_acc_raw(float r, float g, float b, const AccConsts& k) {
+    float q = __fmaf_rn(r, r, __fmaf_rn(g, g, __fmul_rn(b, b)));
+    float white = __fsqrt_rn(__fmul_rn(q, 0.333333343f));               // Eq. 1
+    float s = __fadd_rn(__fadd_rn(r, g), b);
+    float inv = s > 0.0f ? __frcp_rn(s) : 0.0f;                        // black: shares 0
+    float rg = __fsqrt_rn(__fmaf_rn(k.br, __fmul_rn(r, r), __fmul_rn(k.omr, __fmul_rn(g, g))));
+    float warm = __fmaf_rn(__fmul_rn(r, inv), __fsub_rn(rg, white), white);   // Eq. 4
+    float cool = __fmaf_rn(__fmul_rn(b, inv), __fsub_rn(white, b), b);       // Eq. 5
+    return __fsqrt_rn(
+        __fmaf_rn(__fmul_rn(k.bk, warm), warm, __fmul_rn(k.omk, __fmul_rn(cool, cool))));  // Eq. 6
+}
+__device__ __forceinline__ float decolor_acc(float r, float g, float b, const AccConsts& k) {
+    return fminf(fmaxf(decolor_acc_raw(r, g, b, k), 0.0f), 1.0f);
+}
+
+// quantize_u8 (codec.py:22-25) of a [0,1] fp32 value: floor(clip(v)*255 + 0.5)
+__device__ __forceinline__ uint8_t quantize_f32(float v) {
+    v = fminf(fmaxf(v, 0.0f), 1.0f);
+    return static_cast<uint8_t>(__float2uint_rd(__fmaf_rn(v, 255.0f, 0.5f)));
+}
+
+// ---------------------------------------------------------------- global sigmoid, fp32 (tanh form)
+// apply_sigmoid (tonemap.py:72-83) computes (y - lo)/(hi - lo) with
+// y = logistic(k(x - m)); that difference cancels catastrophically in fp32
+// for small slopes. The algebraically equal tanh form
+//   (tanh(k(x-m)/2) + tanh(km/2)) / (tanh(k(1-m)/2) + tanh(km/2))
+// keeps full relative precision; t0/den are evaluated on the device with the
+// same operations as the numerator so x = 0 -> 0 and x = 1 -> 1 exactly.
+struct SigF {
+    float m, hk, t0, den;
+};
+__device__ __forceinline__ SigF make_sig_f(float midpoint, float slope) {
+    SigF s;
+    s.m = midpoint;
+    s.hk = 0.5f * slope;
+    s.t0 = tanhf(__fmul_rn(s.hk, midpoint));
+    s.den = __fadd_rn(tanhf(__fmul_rn(s.hk, __fsub_rn(1.0f, midpoint))), s.t0);
+    return s;
+}
+__device__ __forceinline__ float sigmoid_f(float x, const SigF& s) {
+    float num = __fadd_rn(tanhf(__fmul_rn(s.hk, __fsub_rn(x, s.m))), s.t0);
+    return fminf(fmaxf(__fdiv_rn(num, s.den), 0.0f), 1.0f);
+}
+
+// ---------------------------------------------------------------- fp64 path (reference-exact)
+__device__ __forceinline__ double clamp01_d(double v) {
+    if (v < 0.0) return 0.0;   // _kernels.pyx:23-28
+    if (v > 1.0) return 1.0;
+    return v;
+}
+__device__ __forceinline__ double decolor_f64(double r, double g, double b, double br, double bk) {
+    double white = __dsqrt_rn(__ddiv_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(r, r), __dmul_rn(g, g)), __dmul_rn(b, b)), 3.0));
+    double s = __dadd_rn(__dadd_rn(r, g), b);
+    double wr = 0.0, wb = 0.0;
+    if (s > 0.0) {
+        wr = __ddiv_rn(r, s);
+        wb = __ddiv_rn(b, s);
+    }
+    double redgreen = __dsqrt_rn(__dadd_rn(__dmul_rn(__dmul_rn(br, r), r),
+                                           __dmul_rn(__dmul_rn(__dsub_rn(1.0, br), g), g)));
+    double warm = __dadd_rn(__dmul_rn(wr, redgreen), __dmul_rn(__dsub_rn(1.0, wr), white));
+    double cool = __dadd_rn(__dmul_rn(__dsub_rn(1.0, wb), b), __dmul_rn(wb, white));
+    return clamp01_d(__dsqrt_rn(__dadd_rn(__dmul_rn(__dmul_rn(bk, warm), warm),
+                                          __dmul_rn(__dmul_rn(__dsub_rn(1.0, bk), cool), cool))));
+}
+
+// apply_sigmoid in fp64, logistic form exactly as tonemap.py:76-83.
+struct SigD {
+    double m, k, lo, hi;
+};
+__device__ __forceinline__ SigD make_sig_d(double midpoint, double slope) {
+    SigD s;
+    s.m = midpoint;
+    s.k = slope;
+    s.lo = 1.0 / (1.0 + exp(slope * midpoint));
+    s.hi = 1.0 / (1.0 + exp(-slope * (1.0 - midpoint)));
+    return s;
+}
+__device__ __forceinline__ double sigmoid_d(double x, const SigD& s) {
+    double y = 1.0 / (1.0 + exp(-s.k * (x - s.m)));
+    return clamp01_d((y - s.lo) / (s.hi - s.lo));
+}
+
+// ---------------------------------------------------------------- counter hash (synthetic inputs)
+__host__ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+__host__ __device__ __forceinline__ uint32_t hash3(uint32_t seed, uint32_t image, uint32_t ctr) {
+    return mix32(ctr ^ mix32(image ^ mix32(seed ^ 0x9e3779b9U)));
+}
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ float u01(uint32_t h) { return (h >> 8) * (1.0f / 16777216.0f); }
+
+}  // namespace wg

@@ -1,0 +1,379 @@
+// wg_host.cu -- host runtime of libwarmgray_b200.so: error reporting, device
+// info, and the host-buffer entry points (wg_host_*).
+//
+// The reference's plugin call `_kernels.decolor_rows(rgb, out, ...)`
+// (_kernels.pyx:47-56) consumes host buffers. The wg_host_* entry points keep
+// that contract: they stream the caller's host arrays through per-device
+// staging buffers in chunks, rotating over kSlots CUDA streams so the
+// host->device copy of chunk i+1, the kernel on chunk i and the device->host
+// copy of chunk i-1 overlap (PCIe is full duplex), then return when the
+// output is complete. Staging buffers are allocated once per device and
+// grown on demand (the device-buffer manager), guarded by a per-device mutex.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/warmgray_b200.h"
+#include "wg_internal.h"
+
+namespace wg {
+
+static thread_local std::string t_err;
+
+int set_error(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return code;
+}
+
+int check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_error(static_cast<int>(e), "%s: %s (%s)", what, cudaGetErrorString(e),
+                         cudaGetErrorName(e));
+    return WG_OK;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+    return set_error(static_cast<int>(e), "%s: %s (%s)", what, cudaGetErrorString(e),
+                     cudaGetErrorName(e));
+}
+
+int sm_count(int device) {
+    static int cache[kMaxDevices] = {0};
+    if (device < 0 || device >= kMaxDevices) return 148;
+    if (!cache[device]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 148;
+        }
+        cache[device] = n;
+    }
+    return cache[device];
+}
+
+int check_npix(int64_t n) {
+    return n < 0 ? set_error(WG_EINVAL, "size must be >= 0, got %lld", static_cast<long long>(n)) : 0;
+}
+
+int check_ptrs(int64_t n, const void* a, const void* b) {
+    return (n > 0 && (a == nullptr || b == nullptr)) ? set_error(WG_EINVAL, "null buffer pointer") : 0;
+}
+
+int check_params(double beta_r, double beta_k) {
+    if (!(beta_r > 0.5 && beta_r < 1.0))
+        return set_error(WG_EINVAL, "beta_r must lie strictly between 0.5 and 1, got %.17g", beta_r);
+    if (!(beta_k > 0.5 && beta_k < 1.0))
+        return set_error(WG_EINVAL, "beta_k must lie strictly between 0.5 and 1, got %.17g", beta_k);
+    return 0;
+}
+
+int check_curve(double midpoint, double slope) {
+    if (!(midpoint >= 0.0 && midpoint <= 1.0))
+        return set_error(WG_EINVAL, "midpoint must lie in [0, 1], got %.17g", midpoint);
+    if (!(slope > 0.0) || std::isinf(slope))
+        return set_error(WG_EINVAL, "slope must be a positive finite value, got %.17g", slope);
+    return 0;
+}
+
+// ---------------------------------------------------------------- device-buffer manager
+constexpr int kSlots = 3;
+constexpr size_t kChunkBytes = size_t(64) << 20;  // staging bytes per slot (in + out + scratch)
+
+struct Slot {
+    cudaStream_t stream = nullptr;
+    void* dbuf = nullptr;
+    size_t cap = 0;
+};
+struct DevCtx {
+    std::mutex mu;
+    bool init = false;
+    Slot slots[kSlots];
+};
+static DevCtx g_ctx[kMaxDevices];
+
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev_);
+        ok_ = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() { cudaSetDevice(prev_); }
+    cudaError_t status() const { return ok_; }
+
+  private:
+    int prev_ = 0;
+    cudaError_t ok_ = cudaSuccess;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct HostIn {
+    const void* p;
+    size_t bpu;  // bytes per unit
+};
+struct HostOut {
+    void* p;  // may be null (optional output)
+    size_t bpu;
+};
+
+// Streams `nunits` units (pixels or images) through the device in chunks.
+// launch(dev_in[], dev_out[], dev_scratch, n_units, stream) -> WG status.
+template <class Launch, class ScratchFn>
+static int host_pipeline(int device, int64_t nunits, const HostIn* ins, int nin, const HostOut* outs,
+                         int nout, int64_t quantum, ScratchFn scratch_bytes, Launch launch) {
+    if (nunits == 0) return WG_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_error(WG_ENODEV, "no CUDA device available (this library has no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev || device >= kMaxDevices)
+        return set_error(WG_ENODEV, "device ordinal %d out of range (have %d)", device, ndev);
+    DeviceGuard guard(device);
+    if (guard.status() != cudaSuccess) return cuda_fail(guard.status(), "cudaSetDevice");
+
+    size_t bpu = 0;
+    for (int i = 0; i < nin; ++i) bpu += ins[i].bpu;
+    for (int i = 0; i < nout; ++i) bpu += outs[i].bpu;
+    int64_t chunk = static_cast<int64_t>(kChunkBytes / std::max<size_t>(bpu, 1));
+    chunk = std::max<int64_t>(quantum, chunk / quantum * quantum);
+    chunk = std::min<int64_t>(chunk, (nunits + quantum - 1) / quantum * quantum);
+
+    size_t need = 0;
+    for (int i = 0; i < nin; ++i) need += align256(chunk * ins[i].bpu);
+    for (int i = 0; i < nout; ++i) need += align256(chunk * outs[i].bpu);
+    const size_t scratch = align256(scratch_bytes(chunk));
+    need += scratch;
+
+    DevCtx& ctx = g_ctx[device];
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    if (!ctx.init) {
+        for (Slot& s : ctx.slots) {
+            cudaError_t e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        }
+        ctx.init = true;
+    }
+    for (Slot& s : ctx.slots) {
+        if (s.cap < need) {
+            if (s.dbuf) cudaFree(s.dbuf);
+            s.dbuf = nullptr;
+            s.cap = 0;
+            cudaError_t e = cudaMalloc(&s.dbuf, need);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+            s.cap = need;
+        }
+    }
+
+    int rc = WG_OK;
+    const int64_t nchunks = (nunits + chunk - 1) / chunk;
+    for (int64_t c = 0; c < nchunks && rc == WG_OK; ++c) {
+        Slot& s = ctx.slots[c % kSlots];
+        const int64_t u0 = c * chunk;
+        const int64_t n = std::min<int64_t>(chunk, nunits - u0);
+        uint8_t* cur = static_cast<uint8_t*>(s.dbuf);
+        const void* din[4] = {nullptr, nullptr, nullptr, nullptr};
+        void* dout[4] = {nullptr, nullptr, nullptr, nullptr};
+        for (int i = 0; i < nin; ++i) {
+            din[i] = cur;
+            cudaError_t e = cudaMemcpyAsync(cur, static_cast<const uint8_t*>(ins[i].p) + u0 * ins[i].bpu,
+                                            n * ins[i].bpu, cudaMemcpyHostToDevice, s.stream);
+            if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemcpyAsync H2D"); break; }
+            cur += align256(chunk * ins[i].bpu);
+        }
+        if (rc != WG_OK) break;
+        for (int i = 0; i < nout; ++i) {
+            dout[i] = outs[i].p ? cur : nullptr;
+            cur += align256(chunk * outs[i].bpu);
+        }
+        rc = launch(din, dout, scratch ? static_cast<void*>(cur) : nullptr, n, s.stream);
+        if (rc != WG_OK) break;
+        for (int i = 0; i < nout; ++i) {
+            if (!outs[i].p) continue;
+            cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(outs[i].p) + u0 * outs[i].bpu, dout[i],
+                                            n * outs[i].bpu, cudaMemcpyDeviceToHost, s.stream);
+            if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemcpyAsync D2H"); break; }
+        }
+    }
+    for (Slot& s : ctx.slots) {
+        cudaError_t e = cudaStreamSynchronize(s.stream);
+        if (e != cudaSuccess && rc == WG_OK) rc = cuda_fail(e, "cudaStreamSynchronize");
+    }
+    return rc;
+}
+
+static size_t no_scratch(int64_t) { return 0; }
+
+}  // namespace wg
+
+using namespace wg;
+
+// ====================================================================== info
+extern "C" int wg_version(void) { return 100; }
+
+extern "C" const char* wg_last_error(void) { return t_err.c_str(); }
+
+extern "C" int wg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+extern "C" int wg_sm_count(int device) { return sm_count(device); }
+
+// ====================================================================== host-buffer entry points
+extern "C" int wg_host_decolor_rows_f64(const double* rgb, double* out, int64_t height, int64_t width,
+                                        double beta_r, double beta_k, int64_t row0, int64_t row1,
+                                        int device) {
+    WG_CHECK_ARGS(check_npix(height) || check_npix(width) || check_params(beta_r, beta_k));
+    if (row0 < 0 || row1 > height || row0 > row1)
+        return set_error(WG_EINVAL, "row range [%lld, %lld) outside [0, %lld]", (long long)row0,
+                         (long long)row1, (long long)height);
+    const int64_t npix = (row1 - row0) * width;
+    WG_CHECK_ARGS(check_ptrs(npix, rgb, out));
+    HostIn in[1] = {{rgb + row0 * width * 3, 24}};
+    HostOut o[1] = {{out + row0 * width, 8}};
+    return host_pipeline(device, npix, in, 1, o, 1, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_decolor_f64(static_cast<const double*>(di[0]),
+                                                   static_cast<double*>(dout[0]), n, beta_r, beta_k, st);
+                         });
+}
+
+extern "C" int wg_host_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r,
+                                  float beta_k, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
+    HostIn in[1] = {{rgb, 3}};
+    HostOut o[1] = {{gray, 1}};
+    return host_pipeline(device, npix, in, 1, o, 1, 4096, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_decolor_u8(static_cast<const uint8_t*>(di[0]),
+                                                  static_cast<uint8_t*>(dout[0]), n, beta_r, beta_k, st);
+                         });
+}
+
+extern "C" int wg_host_decolor_f32(const float* rgb, float* gray, int64_t npix, float beta_r,
+                                   float beta_k, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
+    HostIn in[1] = {{rgb, 12}};
+    HostOut o[1] = {{gray, 4}};
+    return host_pipeline(device, npix, in, 1, o, 1, 1024, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_decolor_f32(static_cast<const float*>(di[0]),
+                                                   static_cast<float*>(dout[0]), n, beta_r, beta_k, st);
+                         });
+}
+
+extern "C" int wg_host_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null,
+                                       int64_t npix, float beta_r, float beta_k, float midpoint,
+                                       float slope, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, toned) || check_params(beta_r, beta_k) ||
+                  check_curve(midpoint, slope));
+    HostIn in[1] = {{rgb, 3}};
+    HostOut o[2] = {{toned, 1}, {gray_or_null, 1}};
+    return host_pipeline(device, npix, in, 1, o, 2, 4096, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_decolor_tone_u8(static_cast<const uint8_t*>(di[0]),
+                                                       static_cast<uint8_t*>(dout[0]),
+                                                       static_cast<uint8_t*>(dout[1]), n, beta_r,
+                                                       beta_k, midpoint, slope, st);
+                         });
+}
+
+extern "C" int wg_host_sigmoid_f64(const double* lum, double* out, int64_t n, double midpoint,
+                                   double slope, int device) {
+    WG_CHECK_ARGS(check_npix(n) || check_ptrs(n, lum, out) || check_curve(midpoint, slope));
+    HostIn in[1] = {{lum, 8}};
+    HostOut o[1] = {{out, 8}};
+    return host_pipeline(device, n, in, 1, o, 1, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t k, cudaStream_t st) {
+                             return wg_sigmoid_f64(static_cast<const double*>(di[0]),
+                                                   static_cast<double*>(dout[0]), k, midpoint, slope, st);
+                         });
+}
+
+extern "C" int wg_host_reinstate_f64(const double* rgb, const double* l_in, const double* l_out,
+                                     double* rgb_out, int64_t npix, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, rgb_out) || check_ptrs(npix, l_in, l_out));
+    HostIn in[3] = {{rgb, 24}, {l_in, 8}, {l_out, 8}};
+    HostOut o[1] = {{rgb_out, 24}};
+    return host_pipeline(device, npix, in, 3, o, 1, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_reinstate_f64(static_cast<const double*>(di[0]),
+                                                     static_cast<const double*>(di[1]),
+                                                     static_cast<const double*>(di[2]),
+                                                     static_cast<double*>(dout[0]), n, st);
+                         });
+}
+
+extern "C" int wg_host_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_out,
+                                          int64_t npix, double beta_r, double beta_k, double midpoint,
+                                          double slope, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, l_out) || check_ptrs(npix, rgb_out, rgb) ||
+                  check_params(beta_r, beta_k) || check_curve(midpoint, slope));
+    HostIn in[1] = {{rgb, 24}};
+    HostOut o[2] = {{l_out, 8}, {rgb_out, 24}};
+    return host_pipeline(device, npix, in, 1, o, 2, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_tonemap_global_f64(static_cast<const double*>(di[0]),
+                                                          static_cast<double*>(dout[0]),
+                                                          static_cast<double*>(dout[1]), n, beta_r,
+                                                          beta_k, midpoint, slope, st);
+                         });
+}
+
+extern "C" int wg_host_quantize_u8_f64(const double* in_, uint8_t* out, int64_t n, int device) {
+    WG_CHECK_ARGS(check_npix(n) || check_ptrs(n, in_, out));
+    HostIn in[1] = {{in_, 8}};
+    HostOut o[1] = {{out, 1}};
+    return host_pipeline(device, n, in, 1, o, 1, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t k, cudaStream_t st) {
+                             return wg_quantize_u8_f64(static_cast<const double*>(di[0]),
+                                                       static_cast<uint8_t*>(dout[0]), k, st);
+                         });
+}
+
+extern "C" int wg_host_dequantize_u8_f64(const uint8_t* in_, double* out, int64_t n, int device) {
+    WG_CHECK_ARGS(check_npix(n) || check_ptrs(n, in_, out));
+    HostIn in[1] = {{in_, 1}};
+    HostOut o[1] = {{out, 8}};
+    return host_pipeline(device, n, in, 1, o, 1, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t k, cudaStream_t st) {
+                             return wg_dequantize_u8_f64(static_cast<const uint8_t*>(di[0]),
+                                                         static_cast<double*>(dout[0]), k, st);
+                         });
+}
+
+extern "C" int wg_host_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
+                                      float beta_r, float beta_k, float midpoint, float slope,
+                                      int device) {
+    WG_CHECK_ARGS(check_npix(nimg) || check_npix(pix_per_img) || check_params(beta_r, beta_k) ||
+                  check_curve(midpoint, slope));
+    if (nimg == 0 || pix_per_img == 0) return WG_OK;
+    WG_CHECK_ARGS(check_ptrs(1, rgb, out));
+    HostIn in[1] = {{rgb, static_cast<size_t>(pix_per_img) * 12}};
+    HostOut o[1] = {{out, static_cast<size_t>(pix_per_img)}};
+    return host_pipeline(device, nimg, in, 1, o, 1, 1,
+                         [&](int64_t chunk) { return wg_hdr_scratch_bytes(chunk, pix_per_img); },
+                         [&](const void** di, void** dout, void* scratch, int64_t n, cudaStream_t st) {
+                             return wg_hdr_tonemap_u8(static_cast<const float*>(di[0]),
+                                                      static_cast<uint8_t*>(dout[0]), n, pix_per_img,
+                                                      beta_r, beta_k, midpoint, slope, scratch,
+                                                      wg_hdr_scratch_bytes(n, pix_per_img), st);
+                         });
+}

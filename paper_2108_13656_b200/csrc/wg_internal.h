@@ -1,0 +1,29 @@
+// wg_internal.h -- host-side helpers shared by the translation units of
+// libwarmgray_b200.so (error reporting, argument checks, device info).
+#pragma once
+
+#include <cstdint>
+
+namespace wg {
+
+constexpr int kMaxDevices = 64;
+
+// Records a thread-local message for wg_last_error() and returns `code`.
+int set_error(int code, const char* fmt, ...);
+// cudaGetLastError() after a launch: 0, or the (positive) cudaError_t with a message.
+int check_launch(const char* what);
+// Cached multiprocessor count of `device` (148 on B200).
+int sm_count(int device);
+
+// Argument checks: return nonzero (after recording a message) on failure.
+int check_npix(int64_t n);
+int check_ptrs(int64_t n, const void* a, const void* b);
+int check_params(double beta_r, double beta_k);   // core.py:33-51: 0.5 < beta < 1
+int check_curve(double midpoint, double slope);   // tonemap.py:22-33
+
+}  // namespace wg
+
+#define WG_CHECK_ARGS(failed) \
+    do {                      \
+        if (failed) return WG_EINVAL; \
+    } while (0)

@@ -1,0 +1,614 @@
+// wg_kernels.cu -- sm_100a kernels and their stream-ordered C-ABI launchers.
+//
+// Hot path: a persistent streaming kernel. Each CTA (256 threads) owns a
+// ring of kStages shared-memory tiles of 12 KiB that one elected thread fills
+// with cp.async.bulk (TMA engine, mbarrier complete_tx); every thread then
+// pulls its 48 contiguous input bytes out of shared memory with three
+// conflict-free 128-bit loads (the warp-cooperative de-interleave of packed
+// RGB), computes in registers and writes its gray bytes with one 128-bit
+// coalesced store. 12 KiB = 4096 uint8 pixels or 1024 fp32 pixels per tile.
+//
+// Reference correspondence: _kernels.pyx:47-56 (decolor_rows),
+// tonemap.py:72-83 (apply_sigmoid), :172-192 (reinstate_color),
+// :195-216 (tonemap_image global), codec.py:22-29 (quantize / dequantize).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/warmgray_b200.h"
+#include "wg_device.cuh"
+#include "wg_internal.h"
+
+namespace wg {
+
+constexpr int kThreads = 256;
+constexpr int kStages = 4;
+constexpr int kTileBytes = kThreads * 48;  // 12288 B: 48 input bytes per thread
+constexpr int kSmemBytes = kStages * kTileBytes + kStages * 8;
+
+// ------------------------------------------------------------------ ops
+// An Op consumes the 48 input bytes of one thread (3 x uint4, already in
+// registers) for pixels [px0, px0 + kPx) and stores its outputs; scalar()
+// handles one pixel straight from global memory (tails, unaligned buffers)
+// with bit-identical arithmetic.
+
+struct OpDecolorU8 {
+    static constexpr int kInBpp = 3;
+    static constexpr int kPx = 16;
+    const uint8_t* in;
+    uint8_t* gray;
+    U8Consts k;
+
+    __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
+        const uint32_t w[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y,
+                                v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
+        float2 f[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            // pixels 2j and 2j+1 share one packed lane pair
+            float2 ch[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int b0 = 3 * (2 * j) + c, b1 = 3 * (2 * j + 1) + c;
+                ch[c] = make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3));
+                ch[c] = add2(ch[c], bc2(-kMagic));
+            }
+            f[j] = decolor255_x2(ch[0], ch[1], ch[2], k);
+        }
+        uint4 o;
+        o.x = __byte_perm(pack_lo2(f[0].x, f[0].y), pack_lo2(f[1].x, f[1].y), 0x5410u);
+        o.y = __byte_perm(pack_lo2(f[2].x, f[2].y), pack_lo2(f[3].x, f[3].y), 0x5410u);
+        o.z = __byte_perm(pack_lo2(f[4].x, f[4].y), pack_lo2(f[5].x, f[5].y), 0x5410u);
+        o.w = __byte_perm(pack_lo2(f[6].x, f[6].y), pack_lo2(f[7].x, f[7].y), 0x5410u);
+        st_global_cs_v4(gray + px0, o);
+    }
+    __device__ __forceinline__ void scalar(int64_t p) const {
+        gray[p] = decolor255_x1(static_cast<float>(in[3 * p]), static_cast<float>(in[3 * p + 1]),
+                                static_cast<float>(in[3 * p + 2]), k);
+    }
+};
+
+struct OpDecolorF32 {
+    static constexpr int kInBpp = 12;
+    static constexpr int kPx = 4;
+    const float* in;
+    float* gray;
+    AccConsts k;
+
+    __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
+        const float* f = reinterpret_cast<const float*>(&v[0]);
+        float4 o;
+        o.x = decolor_acc(f[0], f[1], f[2], k);
+        o.y = decolor_acc(f[3], f[4], f[5], k);
+        o.z = decolor_acc(f[6], f[7], f[8], k);
+        o.w = decolor_acc(f[9], f[10], f[11], k);
+        st_global_cs_v4(gray + px0, make_uint4(__float_as_uint(o.x), __float_as_uint(o.y),
+                                              __float_as_uint(o.z), __float_as_uint(o.w)));
+    }
+    __device__ __forceinline__ void scalar(int64_t p) const {
+        gray[p] = decolor_acc(in[3 * p], in[3 * p + 1], in[3 * p + 2], k);
+    }
+};
+
+// decolor + global sigmoid on uint8 input: toned u8 (+ optional gray u8)
+struct OpToneU8 {
+    static constexpr int kInBpp = 3;
+    static constexpr int kPx = 16;
+    const uint8_t* in;
+    uint8_t* toned;
+    uint8_t* gray;  // may be null
+    AccConsts k;
+    float m, slope;
+
+    __device__ __forceinline__ void one(float r, float g, float b, const SigF& s, uint8_t& t,
+                                        uint8_t& q) const {
+        const float inv255 = 1.0f / 255.0f;
+        float l = decolor_acc(__fmul_rn(r, inv255), __fmul_rn(g, inv255), __fmul_rn(b, inv255), k);
+        t = quantize_f32(sigmoid_f(l, s));
+        q = quantize_f32(l);
+    }
+    __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
+        const SigF s = make_sig_f(m, slope);
+        const uint8_t* bytes = reinterpret_cast<const uint8_t*>(&v[0]);
+        uint32_t tw[4] = {0u, 0u, 0u, 0u}, qw[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+            uint8_t t, q;
+            one(bytes[3 * p], bytes[3 * p + 1], bytes[3 * p + 2], s, t, q);
+            tw[p >> 2] |= static_cast<uint32_t>(t) << (8 * (p & 3));
+            qw[p >> 2] |= static_cast<uint32_t>(q) << (8 * (p & 3));
+        }
+        st_global_cs_v4(toned + px0, make_uint4(tw[0], tw[1], tw[2], tw[3]));
+        if (gray) st_global_cs_v4(gray + px0, make_uint4(qw[0], qw[1], qw[2], qw[3]));
+    }
+    __device__ __forceinline__ void scalar(int64_t p) const {
+        const SigF s = make_sig_f(m, slope);
+        uint8_t t, q;
+        one(in[3 * p], in[3 * p + 1], in[3 * p + 2], s, t, q);
+        toned[p] = t;
+        if (gray) gray[p] = q;
+    }
+};
+
+// decolor + global sigmoid (+ reinstate) on fp32 input
+struct OpToneF32 {
+    static constexpr int kInBpp = 12;
+    static constexpr int kPx = 4;
+    const float* in;
+    float* toned;
+    float* gray;     // may be null
+    float* rgb_out;  // may be null
+    AccConsts k;
+    float m, slope;
+
+    __device__ __forceinline__ void one(const float* px, const SigF& s, int64_t p) const {
+        float l = decolor_acc(px[0], px[1], px[2], k);
+        float lo = sigmoid_f(l, s);
+        toned[p] = lo;
+        if (gray) gray[p] = l;
+        if (rgb_out) {
+            // reinstate_color (tonemap.py:187-191)
+            float ratio = __fdiv_rn(lo, fmaxf(l, 1e-6f));
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                rgb_out[3 * p + c] = l == 0.0f ? 0.0f : fminf(fmaxf(__fmul_rn(px[c], ratio), 0.0f), 1.0f);
+        }
+    }
+    __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
+        const SigF s = make_sig_f(m, slope);
+        const float* f = reinterpret_cast<const float*>(&v[0]);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) one(f + 3 * p, s, px0 + p);
+    }
+    __device__ __forceinline__ void scalar(int64_t p) const {
+        const SigF s = make_sig_f(m, slope);
+        one(in + 3 * p, s, p);
+    }
+};
+
+// ------------------------------------------------------------------ streaming kernels
+template <class Op>
+__global__ void __launch_bounds__(kThreads) stream_kernel(Op op, const uint8_t* __restrict__ in,
+                                                          int64_t ntiles, int64_t npix) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
+    constexpr int kTilePx = kThreads * Op::kPx;
+    const int tid = threadIdx.x;
+    const int64_t stride = gridDim.x;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    uint64_t policy = 0;
+    if (tid == 0) {
+        policy = l2_policy_evict_first();
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) {
+            const int64_t t = blockIdx.x + s * stride;
+            if (t < ntiles) {
+                mbar_arrive_expect_tx(&bars[s], kTileBytes);
+                bulk_g2s(smem + s * kTileBytes, in + t * kTileBytes, kTileBytes, &bars[s], policy);
+            }
+        }
+    }
+
+    int s = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
+        mbar_wait(&bars[s], phase);
+        uint4 v[3];
+        const uint4* src = reinterpret_cast<const uint4*>(smem + s * kTileBytes) + tid * 3;
+        v[0] = src[0];
+        v[1] = src[1];
+        v[2] = src[2];
+        __syncthreads();  // every thread has drained slot s
+        if (tid == 0) {
+            const int64_t tn = t + kStages * stride;
+            if (tn < ntiles) {
+                mbar_arrive_expect_tx(&bars[s], kTileBytes);
+                bulk_g2s(smem + s * kTileBytes, in + tn * kTileBytes, kTileBytes, &bars[s], policy);
+            }
+        }
+        op.vec(v, t * kTilePx + static_cast<int64_t>(tid) * Op::kPx);
+        if (++s == kStages) {
+            s = 0;
+            phase ^= 1u;
+        }
+    }
+
+    // tail (< one tile) by the last CTA
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t p = ntiles * kTilePx + tid; p < npix; p += kThreads) op.scalar(p);
+    }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kThreads) scalar_kernel(Op op, int64_t npix) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; p < npix;
+         p += static_cast<int64_t>(gridDim.x) * kThreads)
+        op.scalar(p);
+}
+
+// ------------------------------------------------------------------ launch helpers
+template <class Op>
+static int stream_grid(int device) {
+    static int occ_cache[kMaxDevices] = {0};
+    static int attr_set[kMaxDevices] = {0};
+    if (!attr_set[device]) {
+        cudaFuncSetAttribute(stream_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmemBytes);
+        attr_set[device] = 1;
+    }
+    if (!occ_cache[device]) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<Op>, kThreads,
+                                                      kSmemBytes);
+        occ_cache[device] = std::max(occ, 1);
+    }
+    return occ_cache[device] * sm_count(device);
+}
+
+template <class Op>
+static int launch_stream(const Op& op, const void* in, const void* const* outs, int nouts,
+                         int64_t npix, cudaStream_t stream) {
+    if (npix == 0) return WG_OK;
+    int device = 0;
+    cudaGetDevice(&device);
+    if (device < 0 || device >= kMaxDevices) return set_error(WG_ENODEV, "device ordinal out of range");
+    bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    for (int i = 0; i < nouts; ++i)
+        if (outs[i] && (reinterpret_cast<uintptr_t>(outs[i]) & 15) != 0) aligned = false;
+    constexpr int64_t kTilePx = kThreads * Op::kPx;
+    const int64_t ntiles = npix / kTilePx;
+    if (aligned) {
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, stream_grid<Op>(device)));
+        stream_kernel<Op><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, stream>>>(
+            op, static_cast<const uint8_t*>(in), ntiles, npix);
+    } else {
+        const int64_t blocks = std::min<int64_t>((npix + kThreads - 1) / kThreads, 148LL * 32);
+        scalar_kernel<Op><<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(op, npix);
+    }
+    return check_launch("stream kernel");
+}
+
+// ------------------------------------------------------------------ elementwise fp64 kernels
+__global__ void decolor_f64_kernel(const double* __restrict__ rgb, double* __restrict__ out,
+                                   int64_t npix, double br, double bk) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npix;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[p] = decolor_f64(rgb[3 * p], rgb[3 * p + 1], rgb[3 * p + 2], br, bk);
+}
+
+__global__ void sigmoid_f64_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                   int64_t n, double m, double k) {
+    const SigD s = make_sig_d(m, k);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = sigmoid_d(in[i], s);
+}
+
+__global__ void sigmoid_f32_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                   int64_t n, float m, float k) {
+    const SigF s = make_sig_f(m, k);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = sigmoid_f(in[i], s);
+}
+
+// reinstate_color, tonemap.py:187-191
+__device__ __forceinline__ void reinstate_px_d(const double* c, double li, double lo, double* o) {
+    const double ratio = lo / (li > 1e-6 ? li : 1e-6);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) o[ch] = li == 0.0 ? 0.0 : clamp01_d(c[ch] * ratio);
+}
+
+__global__ void reinstate_f64_kernel(const double* __restrict__ rgb, const double* __restrict__ l_in,
+                                     const double* __restrict__ l_out, double* __restrict__ out,
+                                     int64_t npix) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npix;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        reinstate_px_d(rgb + 3 * p, l_in[p], l_out[p], out + 3 * p);
+}
+
+__global__ void tonemap_global_f64_kernel(const double* __restrict__ rgb, double* __restrict__ l_out,
+                                          double* __restrict__ rgb_out, int64_t npix, double br,
+                                          double bk, double m, double k) {
+    const SigD s = make_sig_d(m, k);
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npix;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double* c = rgb + 3 * p;
+        const double li = decolor_f64(c[0], c[1], c[2], br, bk);
+        const double lo = sigmoid_d(li, s);
+        l_out[p] = lo;
+        reinstate_px_d(c, li, lo, rgb_out + 3 * p);
+    }
+}
+
+__global__ void quantize_u8_f64_kernel(const double* __restrict__ in, uint8_t* __restrict__ out,
+                                       int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double v = clamp01_d(in[i]);
+        if (v != v) v = 0.0;  // np.clip keeps NaN; astype(uint8) of NaN is 0 on x86
+        out[i] = static_cast<uint8_t>(floor(__dadd_rn(__dmul_rn(v, 255.0), 0.5)));
+    }
+}
+
+__global__ void dequantize_u8_f64_kernel(const uint8_t* __restrict__ in, double* __restrict__ out,
+                                         int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = __ddiv_rn(static_cast<double>(in[i]), 255.0);
+}
+
+static unsigned ew_blocks(int64_t n) {
+    int device = 0;
+    cudaGetDevice(&device);
+    const int64_t want = (n + 255) / 256;
+    return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 8LL * sm_count(device))));
+}
+
+// ------------------------------------------------------------------ HDR two-pass
+// Pass 1: per (image, block) chunk, gray = unclamped decolor of the raw
+// radiance (homogeneous, so the per-image scale cancels in t), stored fp32
+// to scratch; block min over gray > 0 and max via warp shuffles + shared
+// memory into partials[img][blk]. No atomics: the statistic is exact and
+// independent of reduction order / GPU count.
+// Pass 2: each block folds its image's partials, then t = log(g/gmin) /
+// log(gmax/gmin) (0 for g == 0, 1 if gmax == gmin), sigmoid, round to u8.
+constexpr int kHdrBlocksPerImage = 128;
+
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__global__ void __launch_bounds__(256) hdr_pass1_kernel(const float* __restrict__ rgb,
+                                                         float* __restrict__ gray,
+                                                         float2* __restrict__ partials,
+                                                         int64_t ppi, AccConsts k) {
+    const int64_t img = blockIdx.y;
+    const int64_t chunk = ((ppi + gridDim.x - 1) / gridDim.x + 3) & ~int64_t(3);
+    const int64_t p0 = imin64(ppi, blockIdx.x * chunk);
+    const int64_t p1 = imin64(ppi, p0 + chunk);
+    const float* in = rgb + img * ppi * 3;
+    float* g = gray + img * ppi;
+    float lo = INFINITY, hi = 0.0f;
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(in + 3 * p0) & 15) == 0) &&
+                        ((reinterpret_cast<uintptr_t>(g + p0) & 15) == 0);
+    int64_t p = p0;
+    if (vec_ok) {
+        for (int64_t q = p0 + 4 * static_cast<int64_t>(threadIdx.x); q + 4 <= p1; q += 4 * blockDim.x) {
+            const float4* src = reinterpret_cast<const float4*>(in + 3 * q);
+            const float4 a = __ldcs(src), b = __ldcs(src + 1), c = __ldcs(src + 2);
+            const float f[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+            float o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                o[j] = decolor_acc_raw(f[3 * j], f[3 * j + 1], f[3 * j + 2], k);
+                if (o[j] > 0.0f) lo = fminf(lo, o[j]);
+                hi = fmaxf(hi, o[j]);
+            }
+            *reinterpret_cast<float4*>(g + q) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        p = p0 + ((p1 - p0) & ~int64_t(3));
+    }
+    for (int64_t q = p + threadIdx.x; q < p1; q += blockDim.x) {
+        const float v = decolor_acc_raw(in[3 * q], in[3 * q + 1], in[3 * q + 2], k);
+        g[q] = v;
+        if (v > 0.0f) lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+    }
+    __shared__ float s_lo[8], s_hi[8];
+    lo = warp_min(lo);
+    hi = warp_max(hi);
+    if ((threadIdx.x & 31) == 0) {
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        lo = threadIdx.x < (blockDim.x >> 5) ? s_lo[threadIdx.x] : INFINITY;
+        hi = threadIdx.x < (blockDim.x >> 5) ? s_hi[threadIdx.x] : 0.0f;
+        lo = warp_min(lo);
+        hi = warp_max(hi);
+        if (threadIdx.x == 0) partials[img * gridDim.x + blockIdx.x] = make_float2(lo, hi);
+    }
+}
+
+__global__ void __launch_bounds__(256) hdr_pass2_kernel(const float* __restrict__ gray,
+                                                         const float2* __restrict__ partials,
+                                                         int nparts, uint8_t* __restrict__ out,
+                                                         int64_t ppi, float m, float slope) {
+    const int64_t img = blockIdx.y;
+    __shared__ float s_lo[8], s_hi[8];
+    __shared__ float s_stat[3];
+    float lo = INFINITY, hi = 0.0f;
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
+        const float2 pr = partials[img * nparts + i];
+        lo = fminf(lo, pr.x);
+        hi = fmaxf(hi, pr.y);
+    }
+    lo = warp_min(lo);
+    hi = warp_max(hi);
+    if ((threadIdx.x & 31) == 0) {
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            lo = fminf(lo, s_lo[w]);
+            hi = fmaxf(hi, s_hi[w]);
+        }
+        // per-image constants in fp64, rounded once
+        const bool has_pos = lo <= hi && hi > 0.0f;
+        const bool range = has_pos && hi > lo;
+        s_stat[0] = has_pos ? static_cast<float>(1.0 / static_cast<double>(lo)) : 0.0f;
+        s_stat[1] = range ? static_cast<float>(1.0 / log2(static_cast<double>(hi) / lo)) : 0.0f;
+        s_stat[2] = range ? 1.0f : 0.0f;
+    }
+    __syncthreads();
+    const float inv_gmin = s_stat[0], inv_lrange = s_stat[1];
+    const bool range = s_stat[2] != 0.0f;
+    const SigF s = make_sig_f(m, slope);
+    const int64_t chunk = ((ppi + gridDim.x - 1) / gridDim.x + 3) & ~int64_t(3);
+    const int64_t p0 = imin64(ppi, blockIdx.x * chunk);
+    const int64_t p1 = imin64(ppi, p0 + chunk);
+    const float* g = gray + img * ppi;
+    uint8_t* o = out + img * ppi;
+    for (int64_t q = p0 + threadIdx.x; q < p1; q += blockDim.x) {
+        const float v = g[q];
+        float t;
+        if (!(v > 0.0f)) t = 0.0f;
+        else if (range) t = fminf(fmaxf(__fmul_rn(log2f(__fmul_rn(v, inv_gmin)), inv_lrange), 0.0f), 1.0f);
+        else t = 1.0f;
+        o[q] = quantize_f32(sigmoid_f(t, s));
+    }
+}
+
+}  // namespace wg
+
+using namespace wg;
+
+// ====================================================================== C ABI (device pointers)
+
+extern "C" int wg_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r,
+                             float beta_k, void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
+    OpDecolorU8 op{rgb, gray, make_u8_consts(beta_r, beta_k)};
+    const void* outs[1] = {gray};
+    return launch_stream(op, rgb, outs, 1, npix, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int wg_decolor_f32(const float* rgb, float* gray, int64_t npix, float beta_r,
+                              float beta_k, void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
+    OpDecolorF32 op{rgb, gray, make_acc_consts(beta_r, beta_k)};
+    const void* outs[1] = {gray};
+    return launch_stream(op, rgb, outs, 1, npix, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int wg_decolor_f64(const double* rgb, double* gray, int64_t npix, double beta_r,
+                              double beta_k, void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
+    if (npix == 0) return WG_OK;
+    decolor_f64_kernel<<<ew_blocks(npix), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        rgb, gray, npix, beta_r, beta_k);
+    return check_launch("decolor_f64");
+}
+
+extern "C" int wg_sigmoid_f64(const double* lum, double* out, int64_t n, double midpoint,
+                              double slope, void* stream) {
+    WG_CHECK_ARGS(check_npix(n) || check_ptrs(n, lum, out) || check_curve(midpoint, slope));
+    if (n == 0) return WG_OK;
+    sigmoid_f64_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(lum, out, n,
+                                                                                    midpoint, slope);
+    return check_launch("sigmoid_f64");
+}
+
+extern "C" int wg_sigmoid_f32(const float* lum, float* out, int64_t n, float midpoint, float slope,
+                              void* stream) {
+    WG_CHECK_ARGS(check_npix(n) || check_ptrs(n, lum, out) || check_curve(midpoint, slope));
+    if (n == 0) return WG_OK;
+    sigmoid_f32_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(lum, out, n,
+                                                                                    midpoint, slope);
+    return check_launch("sigmoid_f32");
+}
+
+extern "C" int wg_reinstate_f64(const double* rgb, const double* l_in, const double* l_out,
+                                double* rgb_out, int64_t npix, void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, rgb_out) || check_ptrs(npix, l_in, l_out));
+    if (npix == 0) return WG_OK;
+    reinstate_f64_kernel<<<ew_blocks(npix), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        rgb, l_in, l_out, rgb_out, npix);
+    return check_launch("reinstate_f64");
+}
+
+extern "C" int wg_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_out,
+                                     int64_t npix, double beta_r, double beta_k, double midpoint,
+                                     double slope, void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, l_out) || check_ptrs(npix, rgb_out, rgb) ||
+                  check_params(beta_r, beta_k) || check_curve(midpoint, slope));
+    if (npix == 0) return WG_OK;
+    tonemap_global_f64_kernel<<<ew_blocks(npix), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        rgb, l_out, rgb_out, npix, beta_r, beta_k, midpoint, slope);
+    return check_launch("tonemap_global_f64");
+}
+
+extern "C" int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null,
+                                  int64_t npix, float beta_r, float beta_k, float midpoint,
+                                  float slope, void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, toned) || check_params(beta_r, beta_k) ||
+                  check_curve(midpoint, slope));
+    OpToneU8 op{rgb, toned, gray_or_null, make_acc_consts(beta_r, beta_k), midpoint, slope};
+    const void* outs[2] = {toned, gray_or_null};
+    return launch_stream(op, rgb, outs, 2, npix, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int wg_decolor_tone_f32(const float* rgb, float* toned, float* gray_or_null,
+                                   float* rgb_out_or_null, int64_t npix, float beta_r, float beta_k,
+                                   float midpoint, float slope, void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, toned) || check_params(beta_r, beta_k) ||
+                  check_curve(midpoint, slope));
+    OpToneF32 op{rgb, toned, gray_or_null, rgb_out_or_null, make_acc_consts(beta_r, beta_k),
+                 midpoint, slope};
+    const void* outs[3] = {toned, gray_or_null, rgb_out_or_null};
+    return launch_stream(op, rgb, outs, 3, npix, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int wg_quantize_u8_f64(const double* in, uint8_t* out, int64_t n, void* stream) {
+    WG_CHECK_ARGS(check_npix(n) || check_ptrs(n, in, out));
+    if (n == 0) return WG_OK;
+    quantize_u8_f64_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(in, out, n);
+    return check_launch("quantize_u8_f64");
+}
+
+extern "C" int wg_dequantize_u8_f64(const uint8_t* in, double* out, int64_t n, void* stream) {
+    WG_CHECK_ARGS(check_npix(n) || check_ptrs(n, in, out));
+    if (n == 0) return WG_OK;
+    dequantize_u8_f64_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(in, out, n);
+    return check_launch("dequantize_u8_f64");
+}
+
+extern "C" size_t wg_hdr_scratch_bytes(int64_t nimg, int64_t pix_per_img) {
+    if (nimg < 0 || pix_per_img < 0) return 0;
+    const size_t gray = static_cast<size_t>(nimg) * static_cast<size_t>(pix_per_img) * sizeof(float);
+    const size_t parts = static_cast<size_t>(nimg) * kHdrBlocksPerImage * sizeof(float2);
+    return ((gray + 255) & ~size_t(255)) + parts;
+}
+
+extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
+                                 float beta_r, float beta_k, float midpoint, float slope,
+                                 void* scratch, size_t scratch_bytes, void* stream) {
+    WG_CHECK_ARGS(check_npix(nimg) || check_npix(pix_per_img) || check_params(beta_r, beta_k) ||
+                  check_curve(midpoint, slope));
+    if (nimg > 65535) return set_error(WG_EINVAL, "hdr: at most 65535 images per call");
+    if (nimg == 0 || pix_per_img == 0) return WG_OK;
+    if (!rgb || !out || !scratch) return set_error(WG_EINVAL, "hdr: null pointer");
+    if (scratch_bytes < wg_hdr_scratch_bytes(nimg, pix_per_img))
+        return set_error(WG_ESCRATCH, "hdr: scratch buffer smaller than wg_hdr_scratch_bytes()");
+    const size_t gray_bytes = (static_cast<size_t>(nimg) * pix_per_img * sizeof(float) + 255) & ~size_t(255);
+    float* gray = static_cast<float*>(scratch);
+    float2* parts = reinterpret_cast<float2*>(static_cast<uint8_t*>(scratch) + gray_bytes);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const dim3 grid(kHdrBlocksPerImage, static_cast<unsigned>(nimg));
+    hdr_pass1_kernel<<<grid, 256, 0, st>>>(rgb, gray, parts, pix_per_img,
+                                           make_acc_consts(beta_r, beta_k));
+    hdr_pass2_kernel<<<grid, 256, 0, st>>>(gray, parts, kHdrBlocksPerImage, out, pix_per_img,
+                                           midpoint, slope);
+    return check_launch("hdr_tonemap_u8");
+}

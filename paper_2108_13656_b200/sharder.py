@@ -1,0 +1,87 @@
+"""Per-GPU batch sharder (SURVEY.md 8 e).
+
+Images are independent, so a batch shards by image with NO data-path
+collective: GPU g owns images [start_g, stop_g) (contiguous, balanced), runs
+one flat-batch launch on its own stream, and the per-pixel maps plus the
+exact per-image min/max make outputs bit-identical for any GPU count (the
+multi-GPU analogue of the reference's thread-count invariance,
+test_core.py:201-206). Two drivers:
+
+* one process per GPU (``torch.distributed``, the bench / torchrun layout):
+  :func:`shard_range` picks the rank's images; :func:`gather_to_root` is the
+  optional final gather (an all-gather of equal-size padded shards, timed
+  separately from the device metric);
+* one process driving several GPUs: :func:`run_on_devices` fans the shards
+  of a host batch out to ``wg_host_*`` calls, one host thread per device.
+"""
+
+from __future__ import annotations
+
+from concurrent.futures import ThreadPoolExecutor
+from typing import Callable, Sequence
+
+import numpy as np
+
+
+def shard_range(n_items: int, world_size: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced split: the first ``n % world`` ranks get one extra item."""
+    if world_size < 1 or not 0 <= rank < world_size:
+        raise ValueError(f"bad rank {rank} for world size {world_size}")
+    if n_items < 0:
+        raise ValueError(f"n_items must be >= 0, got {n_items}")
+    base, extra = divmod(n_items, world_size)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def shard_sizes(n_items: int, world_size: int) -> list[int]:
+    return [b - a for a, b in (shard_range(n_items, world_size, r) for r in range(world_size))]
+
+
+def gather_to_root(local, n_items: int, group=None, root: int = 0):
+    """Assemble every rank's shard (leading axis = items) on ``root``.
+
+    Shards are padded to the largest shard size and exchanged with one
+    ``all_gather_into_tensor`` (NCCL over NVLink on GPUs, gloo on CPU); the
+    root trims the padding and concatenates in rank order. Returns the full
+    batch on ``root`` and ``None`` elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    sizes = shard_sizes(n_items, world)
+    if local.shape[0] != sizes[rank]:
+        raise ValueError(f"rank {rank} holds {local.shape[0]} items, expected {sizes[rank]}")
+    cap = max(sizes) if sizes else 0
+    padded = torch.zeros((cap, *local.shape[1:]), dtype=local.dtype, device=local.device)
+    if local.shape[0]:
+        padded[: local.shape[0]] = local
+    full = torch.empty((world * cap, *local.shape[1:]), dtype=local.dtype, device=local.device)
+    if dist.get_backend(group) == "gloo" or not hasattr(dist, "all_gather_into_tensor"):
+        parts = list(full.chunk(world)) if world else []
+        dist.all_gather(parts, padded, group=group)
+    else:
+        dist.all_gather_into_tensor(full, padded, group=group)
+    if rank != root:
+        return None
+    pieces = [full[r * cap: r * cap + sizes[r]] for r in range(world)]
+    return torch.cat(pieces, dim=0) if pieces else full[:0]
+
+
+def run_on_devices(fn: Callable[[np.ndarray, int], np.ndarray], batch: np.ndarray,
+                   devices: Sequence[int]) -> np.ndarray:
+    """Shard a host batch by image over ``devices``; ``fn(shard, device)`` -> per-shard result.
+
+    One host thread per device (each ``wg_host_*`` call is synchronous on
+    its own device's streams); results are concatenated in image order.
+    """
+    if not devices:
+        raise ValueError("need at least one device")
+    n = batch.shape[0]
+    spans = [shard_range(n, len(devices), r) for r in range(len(devices))]
+    with ThreadPoolExecutor(max_workers=len(devices)) as pool:
+        futs = [pool.submit(fn, batch[a:b], d) for (a, b), d in zip(spans, devices) if b > a]
+        parts = [f.result() for f in futs]
+    return np.concatenate(parts, axis=0) if parts else fn(batch[:0], devices[0])

@@ -1,0 +1,201 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It copies /root/reference/pkg to a scratch directory, builds the reference's
+own Cython extension there (`python setup.py build_ext --inplace`, the
+reference's documented build), imports `warmgray` from that scratch copy and
+records the outputs of the reference's public functions on seeded inputs.
+Nothing under /root/reference is modified and no reference source is copied
+into this repository; only the outputs below are committed:
+
+  kat.json            scalar / image known answers (test_core, test_codec,
+                      test_tonemap fixtures) evaluated by the reference
+  cube.json           sha256 of the reference's outputs over all 2^24 u8
+                      colours (fp64 gray, u8 gray, u8 toned) for both backends
+  c1.json             C1 (512x512 u8, default_rng(0)) input/output sha256
+  rand_f64.npz        seeded fp64 images and the reference's decolor output
+  sigmoid.npz         apply_sigmoid over a grid of inputs and curves
+  reinstate.npz       reinstate_color on seeded inputs
+  tonemap_global.npz  tonemap_image(mode="global") on a seeded image
+  hdr.npz             HDR adapter evaluated with the
+                      reference's decolor_image/apply_sigmoid/quantize_u8
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_PKG = "/root/reference/pkg"
+
+
+def build_reference() -> str:
+    scratch = os.path.join(tempfile.gettempdir(), "wg_ref_golden")
+    if not os.path.exists(os.path.join(scratch, "src", "warmgray")):
+        shutil.rmtree(scratch, ignore_errors=True)
+        shutil.copytree(REF_PKG, scratch)
+    subprocess.run([sys.executable, "setup.py", "build_ext", "--inplace"], cwd=scratch,
+                   check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    return os.path.join(scratch, "src")
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def color_cube_u8() -> np.ndarray:
+    i = np.arange(1 << 24, dtype=np.uint32)
+    cube = np.empty((1 << 24, 3), dtype=np.uint8)
+    cube[:, 0] = i >> 16
+    cube[:, 1] = (i >> 8) & 255
+    cube[:, 2] = i & 255
+    return cube.reshape(4096, 4096, 3)
+
+
+def main() -> None:
+    sys.path.insert(0, build_reference())
+    import warmgray as wg
+    from warmgray.backend import get_kernels
+
+    assert wg.compiled_available(), "reference extension did not build"
+
+    # ---------------- known answers ----------------
+    fixture_pixels = [(1, 1, 1), (0, 0, 0), (0, 0, 1), (1, 0, 0), (0, 1, 0), (0.3, 0.9, 0.4),
+                      (0.5, 0.25, 0.1), (1, 1, 0), (0, 1, 1), (1, 0, 1), (0.2, 0.2, 0.2)]
+    kat = {
+        "decolor_pixel": [[list(map(float, p)), wg.decolor_pixel(p)] for p in fixture_pixels],
+        "white_luminance": [[list(map(float, p)), wg.white_luminance(p)] for p in fixture_pixels],
+        "red_green_luminance": [[list(map(float, p)), wg.red_green_luminance(p)]
+                                for p in fixture_pixels],
+        "warm_luminance": [[list(map(float, p)), wg.warm_luminance(p)] for p in fixture_pixels],
+        "cool_luminance": [[list(map(float, p)), wg.cool_luminance(p)] for p in fixture_pixels],
+        "custom_params": [[list(map(float, p)), wg.decolor_pixel(p, wg.DecolorParams(0.9, 0.6))]
+                          for p in fixture_pixels],
+        "two_pixel_image": wg.decolor_image(
+            wg.PlanarImage(np.array([[[1, 0, 0], [0, 1, 0]]], dtype=np.float64))).data.tolist(),
+        "quantize_in": [0.0, 0.5, 1.0, 0.66332, 0.2989, 127.5 / 255.0, -0.5, 1.5],
+    }
+    kat["quantize_out"] = wg.quantize_u8(np.array(kat["quantize_in"])).tolist()
+    with open(os.path.join(HERE, "kat.json"), "w") as f:
+        json.dump(kat, f, indent=1)
+
+    # ---------------- exhaustive u8 cube ----------------
+    cube = color_cube_u8()
+    x = wg.dequantize_u8(cube)
+    cube_info = {}
+    for backend in ("compiled", "python"):
+        out = np.empty((4096, 4096), dtype=np.float64)
+        get_kernels(backend).decolor_rows(x, out, 0.55, 0.8, 0, 4096)
+        gray_u8 = wg.quantize_u8(out)
+        toned = wg.quantize_u8(wg.apply_sigmoid(wg.PlanarImage(out)).data)
+        toned2 = wg.quantize_u8(
+            wg.apply_sigmoid(wg.PlanarImage(out), wg.SigmoidCurve(0.3, 12.0)).data)
+        cube_info[backend] = {
+            "gray_f64_sha256": sha(out),
+            "gray_u8_sha256": sha(gray_u8),
+            "toned_u8_default_sha256": sha(toned),
+            "toned_u8_m0.3_k12_sha256": sha(toned2),
+            "gray_u8_histogram": np.bincount(gray_u8.ravel(), minlength=256).tolist(),
+        }
+        if backend == "compiled":
+            ref_compiled = out
+    cube_info["python_vs_compiled_f64_max_abs"] = float(np.abs(out - ref_compiled).max())
+    cube_info["layout"] = "index i -> (i>>16, (i>>8)&255, i&255), 4096x4096 row-major"
+    # custom parameters over the cube (u8 only)
+    out = np.empty((4096, 4096), dtype=np.float64)
+    get_kernels("compiled").decolor_rows(x, out, 0.9, 0.6, 0, 4096)
+    cube_info["compiled_b0.9_0.6_gray_u8_sha256"] = sha(wg.quantize_u8(out))
+    with open(os.path.join(HERE, "cube.json"), "w") as f:
+        json.dump(cube_info, f, indent=1)
+
+    # ---------------- C1 ----------------
+    c1 = np.random.default_rng(0).integers(0, 256, (512, 512, 3), dtype=np.uint8)
+    c1_gray = wg.quantize_u8(wg.decolor_image(wg.PlanarImage(wg.dequantize_u8(c1))).data)
+    with open(os.path.join(HERE, "c1.json"), "w") as f:
+        json.dump({"input_sha256": sha(c1), "gray_u8_sha256": sha(c1_gray),
+                   "gray_u8_mean": float(c1_gray.mean()),
+                   "generator": "np.random.default_rng(0).integers(0,256,(512,512,3),dtype=np.uint8)"},
+                  f, indent=1)
+
+    # ---------------- seeded fp64 images ----------------
+    rng = np.random.default_rng(1234)
+    rgb_a = rng.random((23, 31, 3))
+    rgb_b = rng.random((8, 11, 3))
+    edge = np.array([[[0, 0, 0], [1, 1, 1], [1, 0, 0], [0, 1, 0], [0, 0, 1]]], dtype=np.float64)
+    np.savez_compressed(
+        os.path.join(HERE, "rand_f64.npz"),
+        rgb_a=rgb_a, gray_a=wg.decolor_image(wg.PlanarImage(rgb_a)).data,
+        gray_a_custom=wg.decolor_image(wg.PlanarImage(rgb_a), wg.DecolorParams(0.9, 0.6)).data,
+        rgb_b=rgb_b, gray_b=wg.decolor_image(wg.PlanarImage(rgb_b)).data,
+        edge=edge, gray_edge=wg.decolor_image(wg.PlanarImage(edge)).data,
+    )
+
+    # ---------------- sigmoid ----------------
+    xs = np.concatenate([np.linspace(0.0, 1.0, 1001), [0.5, 0.0, 1.0, 1e-9, 1 - 1e-9, 0.3]])
+    curves = [(0.5, 8.0), (0.5, 7.0), (0.3, 5.0), (0.5, 1e-6), (0.8, 50.0), (0.0, 3.0),
+              (1.0, 3.0), (0.5, 1e-3), (0.25, 0.1)]
+    outs = np.stack([wg.apply_sigmoid(wg.PlanarImage(xs[None, :]), wg.SigmoidCurve(m, k)).data[0]
+                     for m, k in curves])
+    np.savez_compressed(os.path.join(HERE, "sigmoid.npz"), x=xs, curves=np.array(curves), out=outs)
+
+    # ---------------- reinstate ----------------
+    rng = np.random.default_rng(77)
+    rgb = rng.random((8, 9, 3))
+    l_in = wg.decolor_image(wg.PlanarImage(rgb)).data.copy()
+    l_in[0, :3] = 0.0
+    l_in[1, :2] = 5e-7
+    l_out = rng.random((8, 9))
+    np.savez_compressed(os.path.join(HERE, "reinstate.npz"), rgb=rgb, l_in=l_in, l_out=l_out,
+                        out=wg.reinstate_color(wg.PlanarImage(rgb), wg.PlanarImage(l_in),
+                                               wg.PlanarImage(l_out)).data)
+
+    # ---------------- tonemap global ----------------
+    rng = np.random.default_rng(78)
+    rgb = rng.random((12, 10, 3))
+    rgb[0, 0] = 0.0
+    rgb_out, l_out = wg.tonemap_image(wg.PlanarImage(rgb), mode="global")
+    rgb_out2, l_out2 = wg.tonemap_image(wg.PlanarImage(rgb), mode="global",
+                                        params=wg.DecolorParams(0.7, 0.9),
+                                        curve=wg.SigmoidCurve(0.4, 3.0))
+    np.savez_compressed(os.path.join(HERE, "tonemap_global.npz"), rgb=rgb, rgb_out=rgb_out.data,
+                        l_out=l_out.data, rgb_out2=rgb_out2.data, l_out2=l_out2.data)
+
+    # ---------------- HDR adapter via the reference's own operators ----------------
+    rng = np.random.default_rng(79)
+    n, h, w = 3, 24, 32
+    lum = 10.0 ** rng.uniform(-3, 4, (n, h, w))
+    chroma = rng.random((n, h, w, 3))
+    chroma[..., rng.integers(0, 3, (n, h, w))[..., None] == np.arange(3)] = 0.0
+    y = chroma @ np.array([0.2126, 0.7152, 0.0722])
+    hdr = (chroma * (lum / np.maximum(y, 1e-6))[..., None]).astype(np.float32)
+    hdr[0, 0, 0] = 0.0                       # a black pixel
+    hdr[2] = hdr[2, 0, 0]                    # a constant image (gmax == gmin)
+    outs = []
+    for im in hdr.astype(np.float64):
+        m = im.max()
+        gn = wg.decolor_image(wg.PlanarImage(im / m)).data
+        pos = gn > 0
+        gmin, gmax = gn[pos].min(), gn[pos].max()
+        if gmax > gmin:
+            t = np.where(pos, np.clip(np.log(np.where(pos, gn, 1.0) / gmin) / np.log(gmax / gmin),
+                                      0, 1), 0.0)
+        else:
+            t = np.where(pos, 1.0, 0.0)
+        outs.append(wg.quantize_u8(wg.apply_sigmoid(wg.PlanarImage(t)).data))
+    np.savez_compressed(os.path.join(HERE, "hdr.npz"), rgb=hdr, out=np.stack(outs))
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
