@@ -137,14 +137,17 @@ __device__ __forceinline__ uint32_t pack_lo2(float a, float b) {
 //   A   = c1 r RGq + (g+b) W                     (= sqrt(3) * S * warm, Eq. 4)
 //   B   = b (sqrt(3)(r+g) + W)                   (= sqrt(3) * S * cool, Eqs. 2, 5)
 //   T   = A^2 + c3 B^2, c3 = (1-bk)/bk
-//   gray255 = c4 * sqrt(T) / S = c4 * T * rsqrt(T S^2 + tiny),  c4 = sqrt(bk/3)   (Eq. 6)
+//   gray255 = c4 * sqrt(T) / S = T * rsqrt(T S^2 / c4^2 + tiny),  c4 = sqrt(bk/3)   (Eq. 6)
 // 3 MUFU (2 sqrt, 1 rsqrt) and no divide per pixel; the tiny bias makes black
 // (T = S = 0) come out 0 instead of 0*inf. gray <= max(r,g,b) <= 255, so no
-// clamp is needed before round-half-up (codec.py:22-25), done as
-// floor(v + 0.5) via a round-toward-zero add of 2^23 whose low byte is the
-// result.
+// clamp is needed. The final FMA T*y + 2^23 rounds to nearest: its low byte is
+// round(gray255), which equals the reference's floor(v + 0.5) (codec.py:22-25)
+// except when the exact product T*y is a half-integer (an exact tie).
+// The operation order minimises distinct register operands per packed op:
+// on sm_100a the u8 kernel is bound by register-file reads / FMA-pipe issue,
+// not by HBM (scripts/ubench_mix.cu, scripts/tune_u8.cu).
 struct U8Consts {
-    float cr, c1, sqrt3, c3, c4;
+    float cr, c1, sqrt3, c3, inv_c4sq;
 };
 
 inline U8Consts make_u8_consts(float beta_r, float beta_k) {
@@ -155,66 +158,65 @@ inline U8Consts make_u8_consts(float beta_r, float beta_k) {
     k.c1 = static_cast<float>(1.7320508075688772 * std::sqrt(1.0 - br));
     k.sqrt3 = 1.7320508075688772f;
     k.c3 = static_cast<float>((1.0 - bk) / bk);
-    k.c4 = static_cast<float>(std::sqrt(bk / 3.0));
+    k.inv_c4sq = static_cast<float>(3.0 / bk);  // 1 / c4^2, c4 = sqrt(bk / 3)
     return k;
 }
 
-// Returns 2^23 + floor(gray255 + 0.5) per lane (low byte = the uint8 gray).
+// Two pixels per packed lane pair. Returns 2^23 + round(gray255) per lane
+// (the low byte is the uint8 gray).
 __device__ __forceinline__ float2 decolor255_x2(float2 R, float2 G, float2 B, const U8Consts& k) {
+    float2 R2 = mul2(R, R);
     float2 G2 = mul2(G, G);
-    float2 q = fma2(B, B, G2);
-    q = fma2(R, R, q);
-    float2 Rc = mul2(R, bc2(k.cr));
-    float2 rgq = fma2(Rc, R, G2);
+    float2 RG2 = add2(R2, G2);
+    float2 q = fma2(B, B, RG2);                 // r^2 + g^2 + b^2
+    float2 p = fma2(R2, bc2(k.cr), G2);         // cr r^2 + g^2
+    float2 Rc1 = mul2(R, bc2(k.c1));
     float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
-    float2 RGq = make_float2(sqrt_mufu(rgq.x), sqrt_mufu(rgq.y));
+    float2 RGq = make_float2(sqrt_mufu(p.x), sqrt_mufu(p.y));
     float2 RG = add2(R, G);
     float2 S = add2(RG, B);
     float2 GB = add2(G, B);
-    float2 Rc1 = mul2(R, bc2(k.c1));
     float2 t1 = mul2(GB, W);
-    float2 A = fma2(Rc1, RGq, t1);
+    float2 A = fma2(Rc1, RGq, t1);              // sqrt(3) S warm
     float2 u = fma2(RG, bc2(k.sqrt3), W);
-    float2 Bp = mul2(B, u);
-    float2 Bc = mul2(Bp, bc2(k.c3));
-    float2 T1 = mul2(Bc, Bp);
-    float2 T = fma2(A, A, T1);
+    float2 Bp = mul2(B, u);                     // sqrt(3) S cool
+    float2 B2 = mul2(Bp, Bp);
+    float2 A2 = mul2(A, A);
+    float2 T = fma2(B2, bc2(k.c3), A2);
     float2 S2 = mul2(S, S);
-    float2 X = fma2(T, S2, bc2(1e-30f));
+    float2 S2k = mul2(S2, bc2(k.inv_c4sq));
+    float2 X = fma2(T, S2k, bc2(1e-30f));
     float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
-    float2 z = mul2(T, y);
-    float2 v = fma2(z, bc2(k.c4), bc2(0.5f));
-    return add2_rz(v, bc2(kMagic));
+    return fma2(T, y, bc2(kMagic));
 }
 
 // Scalar twin of decolor255_x2 with the identical per-lane operation
 // sequence (IEEE rn ops are lane-exact), so tails / unaligned buffers give
 // bit-identical bytes to the vector path.
 __device__ __forceinline__ uint8_t decolor255_x1(float r, float g, float b, const U8Consts& k) {
+    float R2 = __fmul_rn(r, r);
     float G2 = __fmul_rn(g, g);
-    float q = __fmaf_rn(b, b, G2);
-    q = __fmaf_rn(r, r, q);
-    float Rc = __fmul_rn(r, k.cr);
-    float rgq = __fmaf_rn(Rc, r, G2);
+    float RG2 = __fadd_rn(R2, G2);
+    float q = __fmaf_rn(b, b, RG2);
+    float p = __fmaf_rn(R2, k.cr, G2);
+    float Rc1 = __fmul_rn(r, k.c1);
     float W = sqrt_mufu(q);
-    float RGq = sqrt_mufu(rgq);
+    float RGq = sqrt_mufu(p);
     float RG = __fadd_rn(r, g);
     float S = __fadd_rn(RG, b);
     float GB = __fadd_rn(g, b);
-    float Rc1 = __fmul_rn(r, k.c1);
     float t1 = __fmul_rn(GB, W);
     float A = __fmaf_rn(Rc1, RGq, t1);
     float u = __fmaf_rn(RG, k.sqrt3, W);
     float Bp = __fmul_rn(b, u);
-    float Bc = __fmul_rn(Bp, k.c3);
-    float T1 = __fmul_rn(Bc, Bp);
-    float T = __fmaf_rn(A, A, T1);
+    float B2 = __fmul_rn(Bp, Bp);
+    float A2 = __fmul_rn(A, A);
+    float T = __fmaf_rn(B2, k.c3, A2);
     float S2 = __fmul_rn(S, S);
-    float X = __fmaf_rn(T, S2, 1e-30f);
+    float S2k = __fmul_rn(S2, k.inv_c4sq);
+    float X = __fmaf_rn(T, S2k, 1e-30f);
     float y = rsqrt_mufu(X);
-    float z = __fmul_rn(T, y);
-    float v = __fmaf_rn(z, k.c4, 0.5f);
-    return static_cast<uint8_t>(__float_as_uint(__fadd_rz(v, kMagic)) & 0xFFu);
+    return static_cast<uint8_t>(__float_as_uint(__fmaf_rn(T, y, kMagic)) & 0xFFu);
 }
 
 // ---------------------------------------------------------------- fp32 path (accurate)

@@ -1,0 +1,22 @@
+#!/bin/bash
+# One GPU pass: parity tests, the bench line per workload, and the ncu evidence
+# (launch list + one full capture of the hot kernel) for the C3 bench command.
+# Usage (from the repo root, under gpurun):  bash scripts/gpu_round.sh [tag]
+TAG=${1:-r01}
+OUT=gpurun_out
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/nvsmi_$TAG.txt 2>&1
+python __graft_entry__.py smoke > $OUT/smoke_$TAG.log 2>&1; echo "smoke=$?"
+timeout 1200 python -m pytest tests -m gpu -q -s -p no:cacheprovider > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest_gpu=$?"
+tail -2 $OUT/pytest_gpu_$TAG.log
+for W in C3 C2 C4 C1; do
+  timeout 600 python bench.py --workload $W --steps 50 --warmup 5 --cpu-seconds 5 > $OUT/bench_${W}_$TAG.json 2> $OUT/bench_${W}_$TAG.err; echo "bench_$W=$?"
+done
+timeout 900 python bench.py --workload C5 --steps 5 --warmup 3 --no-cpu > $OUT/bench_C5_$TAG.json 2> $OUT/bench_C5_$TAG.err; echo "bench_C5=$?"
+B="python bench.py --workload C3 --steps 5 --warmup 3 --no-e2e --no-cpu"
+$B > $OUT/ncu_plain_$TAG.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $B > $OUT/ncu_launch_$TAG.log 2>&1
+echo "ncu_launches=$?"
+$B > $OUT/ncu_plain2_$TAG.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 3 -c 1 -o $OUT/prof_c3_$TAG $B > $OUT/ncu_full_$TAG.log 2>&1
+echo "ncu_full=$?"

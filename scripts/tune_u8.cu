@@ -1,0 +1,351 @@
+// tune_u8.cu -- variant sweep for the uint8 decolor streaming kernel.
+// Standalone (does not touch the library ABI): includes the same device
+// building blocks, generates a C3-sized batch of random bytes on the device,
+// times every variant with CUDA events and checks each variant's output is
+// bit-identical to variant 0.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -fmad=false -o /tmp/tune scripts/tune_u8.cu
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../paper_2108_13656_b200/csrc/wg_device.cuh"
+extern "C" void or_decolor_u8(const uint8_t*, uint8_t*, int64_t, double, double, int);
+
+using namespace wg;
+
+// ---------------- math variants (16 px from 12 words) ----------------
+// MATH 0: library formulation. MATH 1: c4 folded into the unpack FMA and the
+// +0.5 folded into the final FMA (one packed op fewer per pixel pair).
+template <int MATH>
+__device__ __forceinline__ uint4 decolor16(const uint32_t (&w)[12], const U8Consts& k) {
+    float2 f[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float2 ch[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int b0 = 3 * (2 * j) + c, b1 = 3 * (2 * j + 1) + c;
+            ch[c] = make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3));
+            if (MATH == 7) {
+                const float sc = c == 1 ? k.c1 * k.c4 : k.c4;
+                ch[c] = fma2(ch[c], bc2(sc), bc2(-kMagic * sc));
+            } else if (MATH != 1) ch[c] = add2(ch[c], bc2(-kMagic));
+            else ch[c] = fma2(ch[c], bc2(k.c4), bc2(-kMagic * k.c4));
+        }
+        if (MATH == 0) {
+            f[j] = decolor255_x2(ch[0], ch[1], ch[2], k);
+        } else if (MATH == 3) {  // synthetic: memory + unpack/pack only
+            f[j] = add2(add2(ch[0], ch[1]), ch[2]);
+        } else if (MATH == 4) {  // synthetic: unpack + 3 MUFU per px + pack
+            float2 q = add2(add2(ch[0], ch[1]), ch[2]);
+            float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
+            float2 V = make_float2(sqrt_mufu(W.x), sqrt_mufu(W.y));
+            f[j] = make_float2(rsqrt_mufu(V.x), rsqrt_mufu(V.y));
+        } else if (MATH == 5 || MATH == 6) {  // synthetic: math=2 with MUFU -> FMUL2 (5) or -> nothing (6)
+            float2 R = ch[0], G = ch[1], B = ch[2];
+            float2 R2 = mul2(R, R);
+            float2 G2 = mul2(G, G);
+            float2 RG2 = add2(R2, G2);
+            float2 q = fma2(B, B, RG2);
+            float2 p = fma2(R2, bc2(k.cr), G2);
+            float2 Rc1 = mul2(R, bc2(k.c1));
+            float2 W = MATH == 5 ? mul2(q, bc2(0.5f)) : q;
+            float2 RGq = MATH == 5 ? mul2(p, bc2(0.5f)) : p;
+            float2 RG = add2(R, G);
+            float2 S = add2(RG, B);
+            float2 GB = add2(G, B);
+            float2 t1 = mul2(GB, W);
+            float2 A = fma2(Rc1, RGq, t1);
+            float2 u = fma2(RG, bc2(k.sqrt3), W);
+            float2 Bp = mul2(B, u);
+            float2 B2 = mul2(Bp, Bp);
+            float2 A2 = mul2(A, A);
+            float2 T = fma2(B2, bc2(k.c3), A2);
+            float2 S2 = mul2(S, S);
+            float2 S2k = mul2(S2, bc2(1.0f / (k.c4 * k.c4)));
+            float2 X = fma2(T, S2k, bc2(1e-30f));
+            float2 y = MATH == 5 ? mul2(X, bc2(0.5f)) : X;
+            f[j] = fma2(T, y, bc2(kMagic));
+        } else if (MATH == 7) {
+            // 21 packed ops / pair: channels pre-scaled at unpack (R' = c4 r, G' = c1 c4 g,
+            // B' = c4 b) so that (homogeneity) gray255 = sqrt(T)/S with no final constant
+            // and RGq' = c1 RGq absorbs the c1 r multiply.
+            float2 R = ch[0], G = ch[1], B = ch[2];   // already scaled (see unpack below)
+            const float ic1 = 1.0f / k.c1;
+            float2 R2 = mul2(R, R);
+            float2 G2 = mul2(G, G);                     // c1^2 g'^2
+            float2 p = fma2(R2, bc2(k.c1 * k.c1 * k.cr), G2);   // c1^2 (cr r'^2 + g'^2)
+            float2 RB2 = fma2(B, B, R2);
+            float2 q = fma2(G2, bc2(ic1 * ic1), RB2);
+            float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
+            float2 RGq = make_float2(sqrt_mufu(p.x), sqrt_mufu(p.y));
+            float2 RG = fma2(G, bc2(ic1), R);
+            float2 GB = fma2(G, bc2(ic1), B);
+            float2 S = add2(RG, B);
+            float2 t1 = mul2(GB, W);
+            float2 A = fma2(R, RGq, t1);
+            float2 u = fma2(RG, bc2(k.sqrt3), W);
+            float2 Bp = mul2(B, u);
+            float2 B2 = mul2(Bp, Bp);
+            float2 A2 = mul2(A, A);
+            float2 T = fma2(B2, bc2(k.c3), A2);
+            float2 S2 = mul2(S, S);
+            float2 X = fma2(T, S2, bc2(1e-30f));
+            float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
+            f[j] = fma2(T, y, bc2(kMagic));
+        } else if (MATH == 2) {
+            // fewer distinct register operands (RF reads are the binding resource)
+            float2 R = ch[0], G = ch[1], B = ch[2];
+            float2 R2 = mul2(R, R);
+            float2 G2 = mul2(G, G);
+            float2 RG2 = add2(R2, G2);
+            float2 q = fma2(B, B, RG2);
+            float2 p = fma2(R2, bc2(k.cr), G2);
+            float2 Rc1 = mul2(R, bc2(k.c1));
+            float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
+            float2 RGq = make_float2(sqrt_mufu(p.x), sqrt_mufu(p.y));
+            float2 RG = add2(R, G);
+            float2 S = add2(RG, B);
+            float2 GB = add2(G, B);
+            float2 t1 = mul2(GB, W);
+            float2 A = fma2(Rc1, RGq, t1);
+            float2 u = fma2(RG, bc2(k.sqrt3), W);
+            float2 Bp = mul2(B, u);
+            float2 B2 = mul2(Bp, Bp);
+            float2 A2 = mul2(A, A);
+            float2 T = fma2(B2, bc2(k.c3), A2);
+            float2 S2 = mul2(S, S);
+            float2 S2k = mul2(S2, bc2(1.0f / (k.c4 * k.c4)));
+            float2 X = fma2(T, S2k, bc2(1e-30f));
+            float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
+            f[j] = fma2(T, y, bc2(kMagic));
+        } else {
+            float2 R = ch[0], G = ch[1], B = ch[2];
+            float2 G2 = mul2(G, G);
+            float2 q = fma2(B, B, G2);
+            q = fma2(R, R, q);
+            float2 Rc = mul2(R, bc2(k.cr));
+            float2 rgq = fma2(Rc, R, G2);
+            float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
+            float2 RGq = make_float2(sqrt_mufu(rgq.x), sqrt_mufu(rgq.y));
+            float2 RG = add2(R, G);
+            float2 S = add2(RG, B);
+            float2 GB = add2(G, B);
+            float2 Rc1 = mul2(R, bc2(k.c1));
+            float2 t1 = mul2(GB, W);
+            float2 A = fma2(Rc1, RGq, t1);
+            float2 u = fma2(RG, bc2(k.sqrt3), W);
+            float2 Bp = mul2(B, u);
+            float2 Bc = mul2(Bp, bc2(k.c3));
+            float2 T1 = mul2(Bc, Bp);
+            float2 T = fma2(A, A, T1);
+            float2 S2 = mul2(S, S);
+            float2 X = fma2(T, S2, bc2(1e-30f));
+            float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
+            float2 v = fma2(T, y, bc2(0.5f));
+            f[j] = add2_rz(v, bc2(kMagic));
+        }
+    }
+    uint4 o;
+    o.x = __byte_perm(pack_lo2(f[0].x, f[0].y), pack_lo2(f[1].x, f[1].y), 0x5410u);
+    o.y = __byte_perm(pack_lo2(f[2].x, f[2].y), pack_lo2(f[3].x, f[3].y), 0x5410u);
+    o.z = __byte_perm(pack_lo2(f[4].x, f[4].y), pack_lo2(f[5].x, f[5].y), 0x5410u);
+    o.w = __byte_perm(pack_lo2(f[6].x, f[6].y), pack_lo2(f[7].x, f[7].y), 0x5410u);
+    return o;
+}
+
+constexpr int kTileBytes = 256 * 48;  // 4096 px
+
+// ---------------- variant A: CTA-wide barrier ring (library kernel) ----------------
+template <int STAGES, int MINB, int MATH>
+__global__ void __launch_bounds__(256, MINB) k_sync(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                    int64_t ntiles, U8Consts k) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * kTileBytes);
+    const int tid = threadIdx.x;
+    const int64_t stride = gridDim.x;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    uint64_t pol = 0;
+    if (tid == 0) {
+        pol = l2_policy_evict_first();
+        for (int s = 0; s < STAGES; ++s) {
+            int64_t t = blockIdx.x + s * stride;
+            if (t < ntiles) {
+                mbar_arrive_expect_tx(&bars[s], kTileBytes);
+                bulk_g2s(smem + s * kTileBytes, in + t * kTileBytes, kTileBytes, &bars[s], pol);
+            }
+        }
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
+        mbar_wait(&bars[s], ph);
+        const uint4* src = reinterpret_cast<const uint4*>(smem + s * kTileBytes) + tid * 3;
+        uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+        __syncthreads();
+        if (tid == 0) {
+            int64_t tn = t + STAGES * stride;
+            if (tn < ntiles) {
+                mbar_arrive_expect_tx(&bars[s], kTileBytes);
+                bulk_g2s(smem + s * kTileBytes, in + tn * kTileBytes, kTileBytes, &bars[s], pol);
+            }
+        }
+        const uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+        st_global_cs_v4(out + t * 4096 + tid * 16, decolor16<MATH>(w, k));
+        if (++s == STAGES) { s = 0; ph ^= 1u; }
+    }
+}
+
+// ---------------- variant B: warp-specialised producer, full/empty mbarriers ----------------
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+template <int STAGES, int MINB, int MATH>
+__global__ void __launch_bounds__(288, MINB) k_ws(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                  int64_t ntiles, U8Consts k) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kTileBytes);
+    uint64_t* empty = full + STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t stride = gridDim.x;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 8); }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 8) {  // producer
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
+                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_arrive_expect_tx(&full[s], kTileBytes);
+                bulk_g2s(smem + s * kTileBytes, in + t * kTileBytes, kTileBytes, &full[s], pol);
+                if (++s == STAGES) { s = 0; ph ^= 1u; }
+            }
+        }
+        return;
+    }
+    const int tid = threadIdx.x;  // 0..255
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
+        mbar_wait(&full[s], ph);
+        const uint4* src = reinterpret_cast<const uint4*>(smem + s * kTileBytes) + tid * 3;
+        uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        const uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+        st_global_cs_v4(out + t * 4096 + tid * 16, decolor16<MATH>(w, k));
+        if (++s == STAGES) { s = 0; ph ^= 1u; }
+    }
+}
+
+// ---------------- variant C: direct 128-bit loads (no smem), software prefetch of next tile ----------------
+template <int MINB, int MATH>
+__global__ void __launch_bounds__(256, MINB) k_ldg(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                   int64_t ntiles, U8Consts k) {
+    const int tid = threadIdx.x;
+    const int64_t stride = gridDim.x;
+    int64_t t = blockIdx.x;
+    if (t >= ntiles) return;
+    const uint4* p = reinterpret_cast<const uint4*>(in + t * kTileBytes) + tid * 3;
+    uint4 v0 = __ldcs(p), v1 = __ldcs(p + 1), v2 = __ldcs(p + 2);
+    for (; t < ntiles; t += stride) {
+        uint4 n0 = v0, n1 = v1, n2 = v2;
+        if (t + stride < ntiles) {
+            const uint4* q = reinterpret_cast<const uint4*>(in + (t + stride) * kTileBytes) + tid * 3;
+            n0 = __ldcs(q); n1 = __ldcs(q + 1); n2 = __ldcs(q + 2);
+        }
+        const uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+        st_global_cs_v4(out + t * 4096 + tid * 16, decolor16<MATH>(w, k));
+        v0 = n0; v1 = n1; v2 = n2;
+    }
+}
+
+__global__ void fill(uint8_t* p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<uint32_t*>(p)[i] = hash3(1, 2, (uint32_t)i);
+}
+
+struct Res { const char* name; float ms; bool ok; };
+
+template <class F>
+Res time_it(const char* name, F launch, uint8_t* out, const std::vector<uint8_t>& ref, int64_t nout) {
+    for (int i = 0; i < 3; ++i) launch();
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    const int R = 20;
+    cudaEventRecord(a);
+    for (int i = 0; i < R; ++i) launch();
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    std::vector<uint8_t> h(nout);
+    cudaMemcpy(h.data(), out, nout, cudaMemcpyDeviceToHost);
+    bool ok = ref.empty() || h == ref;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); ok = false; }
+    return {name, ms / R, ok};
+}
+
+int main() {
+    const int64_t npx = 256LL * 3840 * 2160;  // C3
+    const int64_t ntiles = npx / 4096;
+    uint8_t *in, *out;
+    cudaMalloc(&in, npx * 3); cudaMalloc(&out, npx);
+    fill<<<4096, 256>>>(in, npx * 3);
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const U8Consts k = make_u8_consts(0.55f, 0.8f);
+    std::vector<uint8_t> ref;
+    std::vector<Res> res;
+    auto grid_of = [&](auto kern, int threads, int smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int occ = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        return std::min<int64_t>(ntiles, (int64_t)occ * sms);
+    };
+#define SYNC(ST, MB, M) { auto kern = k_sync<ST, MB, M>; int sm = ST * kTileBytes + 64; int64_t g = grid_of(kern, 256, sm); \
+    res.push_back(time_it("sync st=" #ST " minb=" #MB " math=" #M, [&] { kern<<<g, 256, sm>>>(in, out, ntiles, k); }, out, ref, npx)); \
+    if (ref.empty()) { ref.resize(npx); cudaMemcpy(ref.data(), out, npx, cudaMemcpyDeviceToHost); } }
+#define WS(ST, MB, M) { auto kern = k_ws<ST, MB, M>; int sm = ST * kTileBytes + 128; int64_t g = grid_of(kern, 288, sm); \
+    res.push_back(time_it("ws   st=" #ST " minb=" #MB " math=" #M, [&] { kern<<<g, 288, sm>>>(in, out, ntiles, k); }, out, ref, npx)); }
+#define LDG(MB, M, MULT) { auto kern = k_ldg<MB, M>; int64_t g = std::min<int64_t>(ntiles, (int64_t)sms * MULT); \
+    res.push_back(time_it("ldg  minb=" #MB " math=" #M " grid=" #MULT "xSM", [&] { kern<<<g, 256>>>(in, out, ntiles, k); }, out, ref, npx)); }
+    SYNC(4, 4, 0)
+    SYNC(4, 4, 2)
+    SYNC(4, 4, 7)
+    SYNC(3, 5, 7)
+    LDG(4, 2, 16)
+    LDG(4, 7, 16)
+    LDG(4, 7, 8)
+    LDG(5, 7, 20)
+    // cube parity of each math variant vs the fp64 oracle
+    {
+        const int64_t nc = 1 << 24;
+        std::vector<uint8_t> cube(nc * 3), want(nc), got(nc);
+        for (int64_t i = 0; i < nc; ++i) { cube[3 * i] = i >> 16; cube[3 * i + 1] = (i >> 8) & 255; cube[3 * i + 2] = i & 255; }
+        or_decolor_u8(cube.data(), want.data(), nc, 0.55, 0.8, 16);
+        cudaMemcpy(in, cube.data(), nc * 3, cudaMemcpyHostToDevice);
+        auto check = [&](const char* nm, auto kern) {
+            int sm = 4 * kTileBytes + 64;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+            kern<<<nc / 4096, 256, sm>>>(in, out, nc / 4096, k);
+            cudaMemcpy(got.data(), out, nc, cudaMemcpyDeviceToHost);
+            int64_t bad = 0; int mx = 0;
+            for (int64_t i = 0; i < nc; ++i) { int d = abs((int)got[i] - (int)want[i]); if (d) { ++bad; mx = d > mx ? d : mx; } }
+            printf("cube parity %-8s: %lld mismatches (%.2e), max diff %d\n", nm, (long long)bad, bad / double(nc), mx);
+        };
+        check("math=0", k_sync<4, 1, 0>);
+        check("math=1", k_sync<4, 1, 1>);
+        check("math=2", k_sync<4, 1, 2>);
+        check("math=7", k_sync<4, 1, 7>);
+    }
+    for (auto& r : res)
+        printf("%-32s %8.4f ms  %7.1f Gpix/s  %6.1f GB/s  %5.1f%% of 6545  %s\n", r.name, r.ms, npx / r.ms / 1e6,
+               4.0 * npx / r.ms / 1e6, 400.0 * npx / r.ms / 1e6 / 6545.3, r.ok ? "ok" : (r.name[0] == 's' && r.name[10] == '4' ? "ref" : "MISMATCH"));
+    return 0;
+}
