@@ -227,7 +227,12 @@ def main():
         else:
             wg.decolor(rgb, out=out)
 
-    launches_per_step = 2 if wl.output == "hdr_u8" else 1
+    if wl.output == "hdr_u8":
+        # wg_hdr.cu: gray + stats + tone per group of images whose gray plane fits 128 MiB
+        group = max(1, min(32, n_img, (128 << 20) // (wl.pix_per_image * 4)))
+        launches_per_step = 3 * (-(-n_img // group))
+    else:
+        launches_per_step = 1
     in_bytes = rgb.numel() * rgb.element_size()
     flush = None
     if in_bytes < 4 * L2_BYTES:  # small batches: flush L2 between timed steps

@@ -162,6 +162,61 @@ inline U8Consts make_u8_consts(float beta_r, float beta_k) {
     return k;
 }
 
+// Unclamped gray of two non-negative pixels of ANY scale (homogeneous of
+// degree 1), same operation sequence as decolor255_x2 minus the rounding:
+// used on raw HDR radiance, where only relative accuracy (~2e-7) matters.
+__device__ __forceinline__ float2 decolor_fast_x2(float2 R, float2 G, float2 B, const U8Consts& k) {
+    float2 R2 = mul2(R, R);
+    float2 G2 = mul2(G, G);
+    float2 RG2 = add2(R2, G2);
+    float2 q = fma2(B, B, RG2);
+    float2 p = fma2(R2, bc2(k.cr), G2);
+    float2 Rc1 = mul2(R, bc2(k.c1));
+    float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
+    float2 RGq = make_float2(sqrt_mufu(p.x), sqrt_mufu(p.y));
+    float2 RG = add2(R, G);
+    float2 S = add2(RG, B);
+    float2 GB = add2(G, B);
+    float2 t1 = mul2(GB, W);
+    float2 A = fma2(Rc1, RGq, t1);
+    float2 u = fma2(RG, bc2(k.sqrt3), W);
+    float2 Bp = mul2(B, u);
+    float2 B2 = mul2(Bp, Bp);
+    float2 A2 = mul2(A, A);
+    float2 T = fma2(B2, bc2(k.c3), A2);
+    float2 S2 = mul2(S, S);
+    float2 S2k = mul2(S2, bc2(k.inv_c4sq));
+    float2 X = fma2(T, S2k, bc2(1e-36f));
+    float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
+    return mul2(T, y);
+}
+
+// Scalar twin of decolor_fast_x2 (identical per-lane operation sequence).
+__device__ __forceinline__ float decolor_fast_x1(float r, float g, float b, const U8Consts& k) {
+    float R2 = __fmul_rn(r, r);
+    float G2 = __fmul_rn(g, g);
+    float RG2 = __fadd_rn(R2, G2);
+    float q = __fmaf_rn(b, b, RG2);
+    float p = __fmaf_rn(R2, k.cr, G2);
+    float Rc1 = __fmul_rn(r, k.c1);
+    float W = sqrt_mufu(q);
+    float RGq = sqrt_mufu(p);
+    float RG = __fadd_rn(r, g);
+    float S = __fadd_rn(RG, b);
+    float GB = __fadd_rn(g, b);
+    float t1 = __fmul_rn(GB, W);
+    float A = __fmaf_rn(Rc1, RGq, t1);
+    float u = __fmaf_rn(RG, k.sqrt3, W);
+    float Bp = __fmul_rn(b, u);
+    float B2 = __fmul_rn(Bp, Bp);
+    float A2 = __fmul_rn(A, A);
+    float T = __fmaf_rn(B2, k.c3, A2);
+    float S2 = __fmul_rn(S, S);
+    float S2k = __fmul_rn(S2, k.inv_c4sq);
+    float X = __fmaf_rn(T, S2k, 1e-36f);
+    return __fmul_rn(T, rsqrt_mufu(X));
+}
+
 // Two pixels per packed lane pair. Returns 2^23 + round(gray255) per lane
 // (the low byte is the uint8 gray).
 __device__ __forceinline__ float2 decolor255_x2(float2 R, float2 G, float2 B, const U8Consts& k) {

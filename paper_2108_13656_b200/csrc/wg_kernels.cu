@@ -398,131 +398,6 @@ static unsigned ew_blocks(int64_t n) {
     return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 8LL * sm_count(device))));
 }
 
-// ------------------------------------------------------------------ HDR two-pass
-// Pass 1: per (image, block) chunk, gray = unclamped decolor of the raw
-// radiance (homogeneous, so the per-image scale cancels in t), stored fp32
-// to scratch; block min over gray > 0 and max via warp shuffles + shared
-// memory into partials[img][blk]. No atomics: the statistic is exact and
-// independent of reduction order / GPU count.
-// Pass 2: each block folds its image's partials, then t = log(g/gmin) /
-// log(gmax/gmin) (0 for g == 0, 1 if gmax == gmin), sigmoid, round to u8.
-constexpr int kHdrBlocksPerImage = 128;
-
-__device__ __forceinline__ float warp_min(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
-__global__ void __launch_bounds__(256) hdr_pass1_kernel(const float* __restrict__ rgb,
-                                                         float* __restrict__ gray,
-                                                         float2* __restrict__ partials,
-                                                         int64_t ppi, AccConsts k) {
-    const int64_t img = blockIdx.y;
-    const int64_t chunk = ((ppi + gridDim.x - 1) / gridDim.x + 3) & ~int64_t(3);
-    const int64_t p0 = imin64(ppi, blockIdx.x * chunk);
-    const int64_t p1 = imin64(ppi, p0 + chunk);
-    const float* in = rgb + img * ppi * 3;
-    float* g = gray + img * ppi;
-    float lo = INFINITY, hi = 0.0f;
-    const bool vec_ok = ((reinterpret_cast<uintptr_t>(in + 3 * p0) & 15) == 0) &&
-                        ((reinterpret_cast<uintptr_t>(g + p0) & 15) == 0);
-    int64_t p = p0;
-    if (vec_ok) {
-        for (int64_t q = p0 + 4 * static_cast<int64_t>(threadIdx.x); q + 4 <= p1; q += 4 * blockDim.x) {
-            const float4* src = reinterpret_cast<const float4*>(in + 3 * q);
-            const float4 a = __ldcs(src), b = __ldcs(src + 1), c = __ldcs(src + 2);
-            const float f[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
-            float o[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                o[j] = decolor_acc_raw(f[3 * j], f[3 * j + 1], f[3 * j + 2], k);
-                if (o[j] > 0.0f) lo = fminf(lo, o[j]);
-                hi = fmaxf(hi, o[j]);
-            }
-            *reinterpret_cast<float4*>(g + q) = make_float4(o[0], o[1], o[2], o[3]);
-        }
-        p = p0 + ((p1 - p0) & ~int64_t(3));
-    }
-    for (int64_t q = p + threadIdx.x; q < p1; q += blockDim.x) {
-        const float v = decolor_acc_raw(in[3 * q], in[3 * q + 1], in[3 * q + 2], k);
-        g[q] = v;
-        if (v > 0.0f) lo = fminf(lo, v);
-        hi = fmaxf(hi, v);
-    }
-    __shared__ float s_lo[8], s_hi[8];
-    lo = warp_min(lo);
-    hi = warp_max(hi);
-    if ((threadIdx.x & 31) == 0) {
-        s_lo[threadIdx.x >> 5] = lo;
-        s_hi[threadIdx.x >> 5] = hi;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        lo = threadIdx.x < (blockDim.x >> 5) ? s_lo[threadIdx.x] : INFINITY;
-        hi = threadIdx.x < (blockDim.x >> 5) ? s_hi[threadIdx.x] : 0.0f;
-        lo = warp_min(lo);
-        hi = warp_max(hi);
-        if (threadIdx.x == 0) partials[img * gridDim.x + blockIdx.x] = make_float2(lo, hi);
-    }
-}
-
-__global__ void __launch_bounds__(256) hdr_pass2_kernel(const float* __restrict__ gray,
-                                                         const float2* __restrict__ partials,
-                                                         int nparts, uint8_t* __restrict__ out,
-                                                         int64_t ppi, float m, float slope) {
-    const int64_t img = blockIdx.y;
-    __shared__ float s_lo[8], s_hi[8];
-    __shared__ float s_stat[3];
-    float lo = INFINITY, hi = 0.0f;
-    for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
-        const float2 pr = partials[img * nparts + i];
-        lo = fminf(lo, pr.x);
-        hi = fmaxf(hi, pr.y);
-    }
-    lo = warp_min(lo);
-    hi = warp_max(hi);
-    if ((threadIdx.x & 31) == 0) {
-        s_lo[threadIdx.x >> 5] = lo;
-        s_hi[threadIdx.x >> 5] = hi;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
-            lo = fminf(lo, s_lo[w]);
-            hi = fmaxf(hi, s_hi[w]);
-        }
-        // per-image constants in fp64, rounded once
-        const bool has_pos = lo <= hi && hi > 0.0f;
-        const bool range = has_pos && hi > lo;
-        s_stat[0] = has_pos ? static_cast<float>(1.0 / static_cast<double>(lo)) : 0.0f;
-        s_stat[1] = range ? static_cast<float>(1.0 / log2(static_cast<double>(hi) / lo)) : 0.0f;
-        s_stat[2] = range ? 1.0f : 0.0f;
-    }
-    __syncthreads();
-    const float inv_gmin = s_stat[0], inv_lrange = s_stat[1];
-    const bool range = s_stat[2] != 0.0f;
-    const SigF s = make_sig_f(m, slope);
-    const int64_t chunk = ((ppi + gridDim.x - 1) / gridDim.x + 3) & ~int64_t(3);
-    const int64_t p0 = imin64(ppi, blockIdx.x * chunk);
-    const int64_t p1 = imin64(ppi, p0 + chunk);
-    const float* g = gray + img * ppi;
-    uint8_t* o = out + img * ppi;
-    for (int64_t q = p0 + threadIdx.x; q < p1; q += blockDim.x) {
-        const float v = g[q];
-        float t;
-        if (!(v > 0.0f)) t = 0.0f;
-        else if (range) t = fminf(fmaxf(__fmul_rn(log2f(__fmul_rn(v, inv_gmin)), inv_lrange), 0.0f), 1.0f);
-        else t = 1.0f;
-        o[q] = quantize_f32(sigmoid_f(t, s));
-    }
-}
-
 }  // namespace wg
 
 using namespace wg;
@@ -625,33 +500,4 @@ extern "C" int wg_dequantize_u8_f64(const uint8_t* in, double* out, int64_t n, v
     if (n == 0) return WG_OK;
     dequantize_u8_f64_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(in, out, n);
     return check_launch("dequantize_u8_f64");
-}
-
-extern "C" size_t wg_hdr_scratch_bytes(int64_t nimg, int64_t pix_per_img) {
-    if (nimg < 0 || pix_per_img < 0) return 0;
-    const size_t gray = static_cast<size_t>(nimg) * static_cast<size_t>(pix_per_img) * sizeof(float);
-    const size_t parts = static_cast<size_t>(nimg) * kHdrBlocksPerImage * sizeof(float2);
-    return ((gray + 255) & ~size_t(255)) + parts;
-}
-
-extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
-                                 float beta_r, float beta_k, float midpoint, float slope,
-                                 void* scratch, size_t scratch_bytes, void* stream) {
-    WG_CHECK_ARGS(check_npix(nimg) || check_npix(pix_per_img) || check_params(beta_r, beta_k) ||
-                  check_curve(midpoint, slope));
-    if (nimg > 65535) return set_error(WG_EINVAL, "hdr: at most 65535 images per call");
-    if (nimg == 0 || pix_per_img == 0) return WG_OK;
-    if (!rgb || !out || !scratch) return set_error(WG_EINVAL, "hdr: null pointer");
-    if (scratch_bytes < wg_hdr_scratch_bytes(nimg, pix_per_img))
-        return set_error(WG_ESCRATCH, "hdr: scratch buffer smaller than wg_hdr_scratch_bytes()");
-    const size_t gray_bytes = (static_cast<size_t>(nimg) * pix_per_img * sizeof(float) + 255) & ~size_t(255);
-    float* gray = static_cast<float*>(scratch);
-    float2* parts = reinterpret_cast<float2*>(static_cast<uint8_t*>(scratch) + gray_bytes);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const dim3 grid(kHdrBlocksPerImage, static_cast<unsigned>(nimg));
-    hdr_pass1_kernel<<<grid, 256, 0, st>>>(rgb, gray, parts, pix_per_img,
-                                           make_acc_consts(beta_r, beta_k));
-    hdr_pass2_kernel<<<grid, 256, 0, st>>>(gray, parts, kHdrBlocksPerImage, out, pix_per_img,
-                                           midpoint, slope);
-    return check_launch("hdr_tonemap_u8");
 }

@@ -13,6 +13,7 @@
 extern "C" void or_decolor_u8(const uint8_t*, uint8_t*, int64_t, double, double, int);
 
 using namespace wg;
+__host__ __device__ inline float kc4(const U8Consts& k) { return sqrtf(1.0f / k.inv_c4sq); }
 
 // ---------------- math variants (16 px from 12 words) ----------------
 // MATH 0: library formulation. MATH 1: c4 folded into the unpack FMA and the
@@ -28,10 +29,10 @@ __device__ __forceinline__ uint4 decolor16(const uint32_t (&w)[12], const U8Cons
             const int b0 = 3 * (2 * j) + c, b1 = 3 * (2 * j + 1) + c;
             ch[c] = make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3));
             if (MATH == 7) {
-                const float sc = c == 1 ? k.c1 * k.c4 : k.c4;
+                const float sc = c == 1 ? k.c1 * kc4(k) : kc4(k);
                 ch[c] = fma2(ch[c], bc2(sc), bc2(-kMagic * sc));
             } else if (MATH != 1) ch[c] = add2(ch[c], bc2(-kMagic));
-            else ch[c] = fma2(ch[c], bc2(k.c4), bc2(-kMagic * k.c4));
+            else ch[c] = fma2(ch[c], bc2(kc4(k)), bc2(-kMagic * kc4(k)));
         }
         if (MATH == 0) {
             f[j] = decolor255_x2(ch[0], ch[1], ch[2], k);
@@ -63,7 +64,7 @@ __device__ __forceinline__ uint4 decolor16(const uint32_t (&w)[12], const U8Cons
             float2 A2 = mul2(A, A);
             float2 T = fma2(B2, bc2(k.c3), A2);
             float2 S2 = mul2(S, S);
-            float2 S2k = mul2(S2, bc2(1.0f / (k.c4 * k.c4)));
+            float2 S2k = mul2(S2, bc2(1.0f / (kc4(k) * kc4(k))));
             float2 X = fma2(T, S2k, bc2(1e-30f));
             float2 y = MATH == 5 ? mul2(X, bc2(0.5f)) : X;
             f[j] = fma2(T, y, bc2(kMagic));
@@ -116,7 +117,7 @@ __device__ __forceinline__ uint4 decolor16(const uint32_t (&w)[12], const U8Cons
             float2 A2 = mul2(A, A);
             float2 T = fma2(B2, bc2(k.c3), A2);
             float2 S2 = mul2(S, S);
-            float2 S2k = mul2(S2, bc2(1.0f / (k.c4 * k.c4)));
+            float2 S2k = mul2(S2, bc2(1.0f / (kc4(k) * kc4(k))));
             float2 X = fma2(T, S2k, bc2(1e-30f));
             float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
             f[j] = fma2(T, y, bc2(kMagic));
@@ -269,6 +270,78 @@ __global__ void __launch_bounds__(256, MINB) k_ldg(const uint8_t* __restrict__ i
     }
 }
 
+// ---------------- variant D: 2-deep register prefetch ----------------
+template <int MINB, int MATH>
+__global__ void __launch_bounds__(256, MINB) k_ldg2(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                    int64_t ntiles, U8Consts k) {
+    const int tid = threadIdx.x;
+    const int64_t stride = gridDim.x;
+    int64_t t = blockIdx.x;
+    if (t >= ntiles) return;
+    auto ld = [&](int64_t tt, uint4* v) {
+        if (tt < ntiles) {
+            const uint4* p = reinterpret_cast<const uint4*>(in + tt * kTileBytes) + tid * 3;
+            v[0] = __ldcs(p); v[1] = __ldcs(p + 1); v[2] = __ldcs(p + 2);
+        }
+    };
+    uint4 a[3], b[3];
+    ld(t, a);
+    ld(t + stride, b);
+    for (; t < ntiles; t += stride) {
+        uint4 c[3] = {b[0], b[1], b[2]};
+        ld(t + 2 * stride, c);
+        const uint32_t w[12] = {a[0].x, a[0].y, a[0].z, a[0].w, a[1].x, a[1].y, a[1].z, a[1].w, a[2].x, a[2].y, a[2].z, a[2].w};
+        st_global_cs_v4(out + t * 4096 + tid * 16, decolor16<MATH>(w, k));
+        a[0] = b[0]; a[1] = b[1]; a[2] = b[2];
+        b[0] = c[0]; b[1] = c[1]; b[2] = c[2];
+    }
+}
+
+// ---------------- variant E: per-warp bulk-copy rings (no CTA barriers) ----------------
+constexpr int kWarpTile = 32 * 48;  // 1536 B = 512 px
+template <int STAGES, int MINB, int MATH>
+__global__ void __launch_bounds__(256, MINB) k_wtma(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                    int64_t nwtiles, U8Consts k) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* ring = smem + warp * STAGES * kWarpTile;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 8 * STAGES * kWarpTile) + warp * STAGES;
+    const int64_t gw = (int64_t)blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
+    if (lane == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncwarp();
+    uint64_t pol = l2_policy_evict_first();
+    if (lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            int64_t t = gw + s * nw;
+            if (t < nwtiles) {
+                mbar_arrive_expect_tx(&bars[s], kWarpTile);
+                bulk_g2s(ring + s * kWarpTile, in + t * kWarpTile, kWarpTile, &bars[s], pol);
+            }
+        }
+    }
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = gw; t < nwtiles; t += nw) {
+        mbar_wait(&bars[s], ph);
+        const uint4* src = reinterpret_cast<const uint4*>(ring + s * kWarpTile) + lane * 3;
+        uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+        __syncwarp();
+        if (lane == 0) {
+            int64_t tn = t + STAGES * nw;
+            if (tn < nwtiles) {
+                mbar_arrive_expect_tx(&bars[s], kWarpTile);
+                bulk_g2s(ring + s * kWarpTile, in + tn * kWarpTile, kWarpTile, &bars[s], pol);
+            }
+        }
+        const uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
+        st_global_cs_v4(out + t * 512 + lane * 16, decolor16<MATH>(w, k));
+        if (++s == STAGES) { s = 0; ph ^= 1u; }
+    }
+}
+
 __global__ void fill(uint8_t* p, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x)
         reinterpret_cast<uint32_t*>(p)[i] = hash3(1, 2, (uint32_t)i);
@@ -315,14 +388,24 @@ int main() {
     res.push_back(time_it("ws   st=" #ST " minb=" #MB " math=" #M, [&] { kern<<<g, 288, sm>>>(in, out, ntiles, k); }, out, ref, npx)); }
 #define LDG(MB, M, MULT) { auto kern = k_ldg<MB, M>; int64_t g = std::min<int64_t>(ntiles, (int64_t)sms * MULT); \
     res.push_back(time_it("ldg  minb=" #MB " math=" #M " grid=" #MULT "xSM", [&] { kern<<<g, 256>>>(in, out, ntiles, k); }, out, ref, npx)); }
+#define LDG2(MB, M, MULT) { auto kern = k_ldg2<MB, M>; int64_t g = std::min<int64_t>(ntiles, (int64_t)sms * MULT); \
+    res.push_back(time_it("ldg2 minb=" #MB " math=" #M " grid=" #MULT "xSM", [&] { kern<<<g, 256>>>(in, out, ntiles, k); }, out, ref, npx)); }
+#define WTMA(ST, MB, M) { auto kern = k_wtma<ST, MB, M>; int sm = 8 * ST * kWarpTile + 8 * ST * 8; \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); int occ = 0; \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, sm); int64_t g = (int64_t)occ * sms; \
+    res.push_back(time_it("wtma st=" #ST " minb=" #MB " math=" #M, [&] { kern<<<g, 256, sm>>>(in, out, npx / 512, k); }, out, ref, npx)); }
     SYNC(4, 4, 0)
     SYNC(4, 4, 2)
-    SYNC(4, 4, 7)
-    SYNC(3, 5, 7)
     LDG(4, 2, 16)
-    LDG(4, 7, 16)
-    LDG(4, 7, 8)
-    LDG(5, 7, 20)
+    LDG(4, 2, 4)
+    LDG2(4, 2, 16)
+    LDG2(4, 2, 4)
+    LDG2(3, 2, 12)
+    WTMA(4, 4, 2)
+    WTMA(6, 3, 2)
+    WTMA(8, 3, 2)
+    WTMA(3, 4, 2)
+    WTMA(8, 2, 2)
     // cube parity of each math variant vs the fp64 oracle
     {
         const int64_t nc = 1 << 24;
