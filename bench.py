@@ -229,7 +229,7 @@ def main():
 
     if wl.output == "hdr_u8":
         # wg_hdr.cu: gray + stats + tone per group of images whose gray plane fits 128 MiB
-        group = max(1, min(32, n_img, (128 << 20) // (wl.pix_per_image * 4)))
+        group = max(1, min(32, n_img))
         launches_per_step = 3 * (-(-n_img // group))
     else:
         launches_per_step = 1
