@@ -49,6 +49,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Consumers of a cp.async.bulk ring must order their generic-proxy reads of a
+// stage before the async-proxy (TMA) write that refills it: bar.sync alone
+// does not (measured: LDS still in flight were overwritten by the next tile).
+// Every consumer executes this after reading its stage, before the barrier
+// that precedes the refill.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

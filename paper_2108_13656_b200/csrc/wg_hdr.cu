@@ -38,6 +38,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 
 #include "../../include/warmgray_b200.h"
 #include "wg_device.cuh"
@@ -242,6 +243,140 @@ __global__ void __launch_bounds__(kT) hdr_stats_kernel(const float2* __restrict_
 }
 
 // ---------------------------------------------------------------- pass 3: tone (image-uniform blocks)
+// One 16-px chunk (4 x 16 B loads, one 16 B store) per thread per iteration;
+// the per-image mode is hoisted out of the loop.
+template <class Px>
+__device__ __forceinline__ void tone_loop(const float* __restrict__ g, uint8_t* __restrict__ o, int64_t ppi,
+                                          bool discard, Px px) {
+    if ((ppi & 15) == 0) {
+        // register prefetch: chunk ch + step is in flight while chunk ch is toned
+        const int64_t nchunks = ppi >> 4;
+        const int64_t step = static_cast<int64_t>(gridDim.x) * kT;
+        int64_t ch = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x;
+        float4 nx[4];
+        if (ch < nchunks) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) nx[j] = __ldcs(reinterpret_cast<const float4*>(g + (ch << 4)) + j);
+        }
+        for (; ch < nchunks; ch += step) {
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                v[4 * j] = nx[j].x;
+                v[4 * j + 1] = nx[j].y;
+                v[4 * j + 2] = nx[j].z;
+                v[4 * j + 3] = nx[j].w;
+            }
+            if (ch + step < nchunks) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) nx[j] = __ldcs(reinterpret_cast<const float4*>(g + ((ch + step) << 4)) + j);
+            }
+            uint32_t w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                w[j] = px(v[4 * j]) | (px(v[4 * j + 1]) << 8) | (px(v[4 * j + 2]) << 16) | (px(v[4 * j + 3]) << 24);
+            st_global_cs_v4(o + (ch << 4), make_uint4(w[0], w[1], w[2], w[3]));
+            // chunks (even, even + 1) are held by lanes (l, l + 1) of one warp, whose
+            // loads this lane's results already waited on: one 128 B gray line
+            if (discard && (ch & 1) == 0 && ch + 1 < nchunks) discard_l2_line(g + (ch << 4));
+        }
+    } else {
+        for (int64_t p = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; p < ppi;
+             p += static_cast<int64_t>(gridDim.x) * kT)
+            o[p] = static_cast<uint8_t>(px(g[p]));
+    }
+}
+
+// table lookup of one pixel; r = 0 (black) falls in bin 0 whose count is 0
+__device__ __forceinline__ uint32_t lut_px(float v, float inv, const float2* s_lut) {
+    const float r = __fmul_rn(v, inv);
+    const uint32_t b = min(max(__float_as_uint(r) >> 17, 127u << 6), (127u << 6) + kLutBins - 1);
+    const float2 e = s_lut[b - (127u << 6)];
+    return static_cast<uint32_t>(__float_as_int(e.y)) + (r >= e.x ? 1u : 0u);
+}
+
+// Table path for images of a multiple of 4096 px: gray tiles of 16 KiB stream
+// through a 3-stage cp.async.bulk ring; thread t takes float4 t + 256 j
+// (conflict-free LDS.128) and stores 4 coalesced 32-bit words.
+constexpr int kToneTilePx = 4096;
+constexpr int kToneStages = 3;
+constexpr int kToneSmem = kToneStages * kToneTilePx * 4 + kToneStages * 8;
+
+template <class Px>
+__device__ __forceinline__ void tone_tiles(const float* __restrict__ g, uint8_t* __restrict__ o, int64_t ppi,
+                                           bool discard, uint8_t* smem, Px px) {
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kToneStages * kToneTilePx * 4);
+    const int tid = threadIdx.x;
+    const int64_t ntiles = ppi / kToneTilePx;
+    if (tid == 0) {
+        for (int s = 0; s < kToneStages; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    uint64_t pol = 0;
+    if (tid == 0) {
+        pol = l2_policy_evict_first();
+        for (int s = 0; s < kToneStages; ++s) {
+            const int64_t t = blockIdx.x + s * static_cast<int64_t>(gridDim.x);
+            if (t < ntiles) {
+                mbar_arrive_expect_tx(&bars[s], kToneTilePx * 4);
+                bulk_g2s(smem + s * kToneTilePx * 4, g + t * kToneTilePx, kToneTilePx * 4, &bars[s], pol);
+            }
+        }
+    }
+    int s = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        mbar_wait(&bars[s], phase);
+        const float4* src = reinterpret_cast<const float4*>(smem + s * kToneTilePx * 4);
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = src[tid + 256 * j];
+        fence_proxy_async_smem();  // reads of stage s ordered before its TMA refill
+        __syncthreads();
+        if (tid == 0) {
+            const int64_t tn = t + kToneStages * static_cast<int64_t>(gridDim.x);
+            if (tn < ntiles) {
+                mbar_arrive_expect_tx(&bars[s], kToneTilePx * 4);
+                bulk_g2s(smem + s * kToneTilePx * 4, g + tn * kToneTilePx, kToneTilePx * 4, &bars[s], pol);
+            }
+        }
+        if (discard && tid < kToneTilePx * 4 / 128) discard_l2_line(g + t * kToneTilePx + tid * 32);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(o + t * kToneTilePx);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            __stcs(dst + tid + 256 * j, px(v[j].x) | (px(v[j].y) << 8) | (px(v[j].z) << 16) | (px(v[j].w) << 24));
+        if (++s == kToneStages) {
+            s = 0;
+            phase ^= 1u;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kT) hdr_tone_tiled_kernel(const float* __restrict__ gray, uint8_t* __restrict__ out,
+                                                            int64_t ppi, const HdrStat* __restrict__ stats,
+                                                            const float2* __restrict__ luts, float m, float slope,
+                                                            bool discard) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ float2 s_lut[kLutBins];
+    const int64_t img = blockIdx.y;
+    const HdrStat st = stats[img];
+    const float* g = gray + img * ppi;
+    uint8_t* o = out + img * ppi;
+    if (st.mode == 1 && st.lut) {  // block-uniform
+        const float2* lut = luts + img * kLutBins;
+        for (int q = threadIdx.x; q < kLutBins; q += kT) s_lut[q] = lut[q];
+        // (made visible by the __syncthreads inside tone_tiles before first use)
+        const float inv = st.inv_gmin;
+        tone_tiles(g, o, ppi, discard, smem, [&](float v) -> uint32_t { return lut_px(v, inv, s_lut); });
+    } else if (st.mode == 2) {
+        tone_tiles(g, o, ppi, discard, smem, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });
+    } else {
+        const ToneU8 c = make_tone_u8(m, slope);
+        tone_tiles(g, o, ppi, discard, smem, [&](float v) -> uint32_t { return tone_arith(v, st, c); });
+    }
+}
+
 __global__ void __launch_bounds__(kT) hdr_tone_kernel(const float* __restrict__ gray, uint8_t* __restrict__ out,
                                                       int64_t ppi, const HdrStat* __restrict__ stats,
                                                       const float2* __restrict__ luts, float m, float slope,
@@ -249,58 +384,19 @@ __global__ void __launch_bounds__(kT) hdr_tone_kernel(const float* __restrict__ 
     __shared__ float2 s_lut[kLutBins];
     const int64_t img = blockIdx.y;
     const HdrStat st = stats[img];
-    const bool use_lut = st.mode == 1 && st.lut;
-    if (use_lut) {
+    const float* g = gray + img * ppi;
+    uint8_t* o = out + img * ppi;
+    if (st.mode == 1 && st.lut) {
         const float2* lut = luts + img * kLutBins;
         for (int q = threadIdx.x; q < kLutBins; q += kT) s_lut[q] = lut[q];
         __syncthreads();
-    }
-    const ToneU8 c = make_tone_u8(m, slope);
-    const float* g = gray + img * ppi;
-    uint8_t* o = out + img * ppi;
-    auto px = [&](float v) -> uint32_t {
-        if (use_lut) return tone_lut(v, st.inv_gmin, s_lut);
-        if (st.mode == 2) return v > 0.0f ? 255u : 0u;  // t = 1 -> sigmoid(1) = 1
-        return tone_arith(v, st, c);
-    };
-    if ((ppi & 15) == 0) {
-        // two 16-px chunks per thread per iteration: 8 independent 16 B loads in flight
-        const int64_t nchunks = ppi >> 4;
-        const int64_t step = static_cast<int64_t>(gridDim.x) * kT;
-        for (int64_t ch = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; ch < nchunks; ch += 2 * step) {
-            const int64_t ch2 = ch + step;
-            const bool two = ch2 < nchunks;
-            float v[32];
-            const float4* s0 = reinterpret_cast<const float4*>(g + (ch << 4));
-            const float4* s1 = reinterpret_cast<const float4*>(g + ((two ? ch2 : ch) << 4));
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float4 q = __ldcs(s0 + j), r = __ldcs(s1 + j);
-                v[4 * j] = q.x;
-                v[4 * j + 1] = q.y;
-                v[4 * j + 2] = q.z;
-                v[4 * j + 3] = q.w;
-                v[16 + 4 * j] = r.x;
-                v[16 + 4 * j + 1] = r.y;
-                v[16 + 4 * j + 2] = r.z;
-                v[16 + 4 * j + 3] = r.w;
-            }
-            uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-#pragma unroll
-            for (int j = 0; j < 32; ++j) w[j >> 2] |= px(v[j]) << (8 * (j & 3));
-            st_global_cs_v4(o + (ch << 4), make_uint4(w[0], w[1], w[2], w[3]));
-            if (two) st_global_cs_v4(o + (ch2 << 4), make_uint4(w[4], w[5], w[6], w[7]));
-            // chunk pairs (even, even + 1) held by lanes (l, l + 1) of one warp, whose
-            // loads this lane's results already waited on, form one 128 B gray line
-            if (discard) {
-                if ((ch & 1) == 0 && ch + 1 < nchunks) discard_l2_line(g + (ch << 4));
-                if (two && (ch2 & 1) == 0 && ch2 + 1 < nchunks) discard_l2_line(g + (ch2 << 4));
-            }
-        }
+        const float inv = st.inv_gmin;
+        tone_loop(g, o, ppi, discard, [&](float v) -> uint32_t { return lut_px(v, inv, s_lut); });
+    } else if (st.mode == 2) {
+        tone_loop(g, o, ppi, discard, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });  // t = 1
     } else {
-        for (int64_t p = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; p < ppi;
-             p += static_cast<int64_t>(gridDim.x) * kT)
-            o[p] = static_cast<uint8_t>(px(g[p]));
+        const ToneU8 c = make_tone_u8(m, slope);
+        tone_loop(g, o, ppi, discard, [&](float v) -> uint32_t { return tone_arith(v, st, c); });
     }
 }
 
@@ -402,6 +498,7 @@ __global__ void __launch_bounds__(kT) hdr_fused_kernel(const float* __restrict__
                 mbar_wait(&bars[s], phase);
                 const uint4* src = reinterpret_cast<const uint4*>(ring + s * kWT) + lane * 3;
                 const uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+                fence_proxy_async_smem();  // reads ordered before the TMA refill of this stage
                 __syncwarp();
                 if (lane == 0 && kk + kStagesF < total) {
                     mbar_arrive_expect_tx(&bars[s], kWT);
@@ -571,11 +668,39 @@ size_t fused_bytes(int64_t nimg, int64_t ppi) {
     return align256(3 * static_cast<size_t>(ppi) * sizeof(float)) + align256(3 * kSlots * sizeof(float2)) +
            align256(static_cast<size_t>(nimg) * sizeof(HdrSync));
 }
+// two scratch sets (double buffering across the two streams) when there is more than one group
+int scratch_sets(int64_t nimg, int64_t ppi) {
+    const int g = group_size(nimg, ppi);
+    return (nimg + g - 1) / g > 1 ? 2 : 1;
+}
 size_t grouped_bytes(int64_t nimg, int64_t ppi) {
-    // G gray planes | G slot arrays | G tables | stats[G]
+    // per set: G gray planes | G slot arrays | G tables | stats[G]
     const size_t g = static_cast<size_t>(group_size(nimg, ppi));
-    return align256(g * ppi * sizeof(float)) + align256(g * kSlots * sizeof(float2)) +
-           align256(g * kLutBins * sizeof(float2)) + align256(g * sizeof(HdrStat));
+    return scratch_sets(nimg, ppi) * (align256(g * ppi * sizeof(float)) + align256(g * kSlots * sizeof(float2)) +
+                                      align256(g * kLutBins * sizeof(float2)) + align256(g * sizeof(HdrStat)));
+}
+
+// per-device auxiliary stream + events of the pipelined grouped schedule
+struct HdrStreams {
+    std::mutex mu;
+    cudaStream_t aux = nullptr;
+    cudaEvent_t start = nullptr, gray_done[2] = {nullptr, nullptr}, tone_done[2] = {nullptr, nullptr};
+};
+HdrStreams* hdr_streams(int device) {
+    static HdrStreams hs[kMaxDevices];
+    static std::mutex init_mu;
+    if (device < 0 || device >= kMaxDevices) return nullptr;
+    std::lock_guard<std::mutex> g(init_mu);
+    HdrStreams& h = hs[device];
+    if (!h.aux) {
+        if (cudaStreamCreateWithFlags(&h.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        cudaEventCreateWithFlags(&h.start, cudaEventDisableTiming);
+        for (int q = 0; q < 2; ++q) {
+            cudaEventCreateWithFlags(&h.gray_done[q], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&h.tone_done[q], cudaEventDisableTiming);
+        }
+    }
+    return &h;
 }
 
 Theta make_theta(double m, double k) {
@@ -655,32 +780,92 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
             return check_launch("hdr_fused_kernel");
         }
     }
+    // ---- grouped schedule. Consecutive groups alternate between two scratch
+    // sets so the HBM-bound gray pass of group n+1 (caller's stream) overlaps
+    // the L2-bound stats + tone of group n (an internal stream); events order
+    // the reuse of each set and join the internal stream back into `stream`.
     const int G = group_size(nimg, pix_per_img);
+    const int64_t ngroups = (nimg + G - 1) / G;
+    const int nsets = scratch_sets(nimg, pix_per_img);
+    struct Set {
+        float* gray;
+        float2* parts;
+        float2* luts;
+        HdrStat* stats;
+    } sets[2];
     uint8_t* base = static_cast<uint8_t*>(scratch);
-    float* gray = reinterpret_cast<float*>(base);
-    base += align256(static_cast<size_t>(G) * pix_per_img * sizeof(float));
-    float2* parts = reinterpret_cast<float2*>(base);
-    base += align256(static_cast<size_t>(G) * kSlots * sizeof(float2));
-    float2* luts = reinterpret_cast<float2*>(base);
-    base += align256(static_cast<size_t>(G) * kLutBins * sizeof(float2));
-    HdrStat* stats = reinterpret_cast<HdrStat*>(base);
-    for (int64_t i0 = 0; i0 < nimg; i0 += G) {
+    for (int q = 0; q < nsets; ++q) {
+        sets[q].gray = reinterpret_cast<float*>(base);
+        base += align256(static_cast<size_t>(G) * pix_per_img * sizeof(float));
+        sets[q].parts = reinterpret_cast<float2*>(base);
+        base += align256(static_cast<size_t>(G) * kSlots * sizeof(float2));
+        sets[q].luts = reinterpret_cast<float2*>(base);
+        base += align256(static_cast<size_t>(G) * kLutBins * sizeof(float2));
+        sets[q].stats = reinterpret_cast<HdrStat*>(base);
+        base += align256(static_cast<size_t>(G) * sizeof(HdrStat));
+    }
+    HdrStreams* hs = nullptr;
+    std::unique_lock<std::mutex> lock;
+    if (nsets == 2) {
+        hs = hdr_streams(device);
+        if (!hs) return set_error(WG_ENODEV, "hdr: could not create the auxiliary stream");
+        lock = std::unique_lock<std::mutex>(hs->mu);
+        cudaEventRecord(hs->start, st);
+        cudaStreamWaitEvent(hs->aux, hs->start, 0);
+    }
+    for (int64_t gi = 0; gi < ngroups; ++gi) {
+        const int64_t i0 = gi * G;
         const int g = static_cast<int>(std::min<int64_t>(G, nimg - i0));
+        const Set& S = sets[gi % nsets];
+        float* gray = S.gray;
+        float2* parts = S.parts;
+        float2* luts = S.luts;
+        HdrStat* stats = S.stats;
+        cudaStream_t sb = st;
+        if (nsets == 2) {
+            if (gi >= 2) cudaStreamWaitEvent(st, hs->tone_done[gi % 2], 0);  // set free again
+            sb = hs->aux;
+        }
         // gray: ~8 waves of blocks over the group, at most kSlots warps per image
         const int64_t work = (pix_per_img & 3) == 0 ? pix_per_img / 4 : pix_per_img;
         const int64_t bx = std::max<int64_t>(
             1, std::min<int64_t>({(work + kT - 1) / kT, std::max<int64_t>(1, 8LL * sms / g), kSlots / kWarps}));
         hdr_gray_kernel<<<dim3(static_cast<unsigned>(bx), static_cast<unsigned>(g)), kT, 0, st>>>(
             rgb + i0 * pix_per_img * 3, gray, parts, pix_per_img, k);
-        hdr_stats_kernel<<<g, kT, 0, st>>>(parts, static_cast<int>(bx) * kWarps, stats, luts, theta);
+        if (nsets == 2) {
+            cudaEventRecord(hs->gray_done[gi % 2], st);
+            cudaStreamWaitEvent(sb, hs->gray_done[gi % 2], 0);
+        }
+        hdr_stats_kernel<<<g, kT, 0, sb>>>(parts, static_cast<int>(bx) * kWarps, stats, luts, theta);
         const int64_t twork = (pix_per_img & 15) == 0 ? pix_per_img / 16 : pix_per_img;
         const int64_t bt = std::max<int64_t>(1, std::min<int64_t>((twork + kT - 1) / kT, std::max<int64_t>(1, 8LL * sms / g)));
         // drop the gray lines from L2 only when the group's plane can actually be resident there
-        const bool discard = static_cast<size_t>(g) * pix_per_img * sizeof(float) <= (size_t(96) << 20);
-        hdr_tone_kernel<<<dim3(static_cast<unsigned>(bt), static_cast<unsigned>(g)), kT, 0, st>>>(
-            gray, out + i0 * pix_per_img, pix_per_img, stats, luts, midpoint, slope, discard);
+        const bool discard = static_cast<size_t>(g) * pix_per_img * sizeof(float) <= (size_t(96) << 20) &&
+                             !getenv("WG_HDR_NO_DISCARD");
+        if (pix_per_img % kToneTilePx == 0 && !getenv("WG_HDR_NO_TILED")) {
+            static int tone_occ[kMaxDevices] = {0};
+            if (device >= 0 && device < kMaxDevices && !tone_occ[device]) {
+                cudaFuncSetAttribute(hdr_tone_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kToneSmem);
+                int occ = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hdr_tone_tiled_kernel, kT, kToneSmem);
+                tone_occ[device] = std::max(occ, 1);
+            }
+            const int occ = device >= 0 && device < kMaxDevices ? tone_occ[device] : 1;
+            const int64_t ntiles = pix_per_img / kToneTilePx;
+            const int64_t bt2 = std::max<int64_t>(1, std::min<int64_t>(ntiles, (static_cast<int64_t>(occ) * sms + g - 1) / g));
+            hdr_tone_tiled_kernel<<<dim3(static_cast<unsigned>(bt2), static_cast<unsigned>(g)), kT, kToneSmem, sb>>>(
+                gray, out + i0 * pix_per_img, pix_per_img, stats, luts, midpoint, slope, discard);
+        } else {
+            hdr_tone_kernel<<<dim3(static_cast<unsigned>(bt), static_cast<unsigned>(g)), kT, 0, sb>>>(
+                gray, out + i0 * pix_per_img, pix_per_img, stats, luts, midpoint, slope, discard);
+        }
+        if (nsets == 2) cudaEventRecord(hs->tone_done[gi % 2], sb);
         const int rc = check_launch("hdr_tonemap_u8");
-        if (rc != WG_OK) return rc;
+        if (rc != WG_OK) {
+            if (nsets == 2) cudaStreamWaitEvent(st, hs->tone_done[gi % 2], 0);
+            return rc;
+        }
     }
-    return WG_OK;
+    if (nsets == 2) cudaStreamWaitEvent(st, hs->tone_done[(ngroups - 1) % 2], 0);  // join
+    return check_launch("hdr_tonemap_u8");
 }

@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(Op op, const uint8_t* 
         v[0] = src[0];
         v[1] = src[1];
         v[2] = src[2];
-        __syncthreads();  // every thread has drained slot s
+        fence_proxy_async_smem();  // reads of slot s ordered before its TMA refill
+        __syncthreads();           // every thread has drained slot s
         if (tid == 0) {
             const int64_t tn = t + kStages * stride;
             if (tn < ntiles) {
