@@ -32,6 +32,7 @@ from .batch import (
     sigmoid,
 )
 from .codec import dequantize_u8, quantize_u8
+from .perf import BenchResult, format_table, run_benchmark
 from .colorspaces import METHOD_NAMES, luminance_image
 from .core import (
     DEFAULT_PARAMS,
@@ -66,6 +67,9 @@ __all__ = [
     "set_device",
     "quantize_u8",
     "dequantize_u8",
+    "BenchResult",
+    "format_table",
+    "run_benchmark",
     "METHOD_NAMES",
     "luminance_image",
     "DEFAULT_PARAMS",

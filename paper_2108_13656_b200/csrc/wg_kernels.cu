@@ -240,8 +240,10 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(Op op, const uint8_t* 
 // no barriers; used where the per-pixel math, not the memory pipe, is the
 // limiter (the uint8 path: scripts/tune_u8.cu measured it ahead of the
 // bulk-copy ring at equal parity).
+// Occupancy 5 CTAs/SM (<= 51 registers, no spills) and a 40 x SM grid measured
+// best on C3 (scripts/tune_u8.cu: 74.7% of the HBM roofline vs 70.9% at 4 CTAs/SM).
 template <class Op>
-__global__ void __launch_bounds__(kThreads, 4) ldg_stream_kernel(Op op, const uint8_t* __restrict__ in,
+__global__ void __launch_bounds__(kThreads, 5) ldg_stream_kernel(Op op, const uint8_t* __restrict__ in,
                                                                  int64_t ntiles, int64_t npix) {
     constexpr int kTilePx = kThreads * Op::kPx;
     const int tid = threadIdx.x;
@@ -308,7 +310,7 @@ static int launch_stream(const Op& op, const void* in, const void* const* outs, 
     constexpr int64_t kTilePx = kThreads * Op::kPx;
     const int64_t ntiles = npix / kTilePx;
     if (aligned && Op::kLdg) {
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, 16LL * sm_count(device)));
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, 40LL * sm_count(device)));
         ldg_stream_kernel<Op><<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(
             op, static_cast<const uint8_t*>(in), ntiles, npix);
     } else if (aligned) {

@@ -156,6 +156,59 @@ __device__ __forceinline__ uint4 decolor16(const uint32_t (&w)[12], const U8Cons
     return o;
 }
 
+// structural variants around the library math (decolor255_x2):
+//   VAR 10: unpack all 16 px first (48 PRMT grouped -> constant-register reuse), then 8 pairs
+//   VAR 11: unpack per pair, but issue two pairs' math back to back (j, j + 4)
+template <int VAR>
+__device__ __forceinline__ uint4 decolor16v(const uint32_t (&w)[12], const U8Consts& k) {
+    float2 f[8];
+    if (VAR == 10) {
+        float2 ch[8][3];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int b0 = 6 * j + c, b1 = 6 * j + 3 + c;
+                ch[j][c] = make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3));
+            }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ch[j][c] = add2(ch[j][c], bc2(-kMagic));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = decolor255_x2(ch[j][0], ch[j][1], ch[j][2], k);
+    } else {
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            float2 ch[2][3];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int j = h + 4 * q;
+                    const int b0 = 6 * j + c, b1 = 6 * j + 3 + c;
+                    ch[q][c] = add2(make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3)),
+                                    bc2(-kMagic));
+                }
+            f[h] = decolor255_x2(ch[0][0], ch[0][1], ch[0][2], k);
+            f[h + 4] = decolor255_x2(ch[1][0], ch[1][1], ch[1][2], k);
+        }
+    }
+    uint4 o;
+    o.x = __byte_perm(pack_lo2(f[0].x, f[0].y), pack_lo2(f[1].x, f[1].y), 0x5410u);
+    o.y = __byte_perm(pack_lo2(f[2].x, f[2].y), pack_lo2(f[3].x, f[3].y), 0x5410u);
+    o.z = __byte_perm(pack_lo2(f[4].x, f[4].y), pack_lo2(f[5].x, f[5].y), 0x5410u);
+    o.w = __byte_perm(pack_lo2(f[6].x, f[6].y), pack_lo2(f[7].x, f[7].y), 0x5410u);
+    return o;
+}
+
+// dispatch: MATH < 10 -> decolor16<MATH>, else decolor16v<MATH>
+template <int M>
+__device__ __forceinline__ uint4 dec16(const uint32_t (&w)[12], const U8Consts& k) {
+    if constexpr (M >= 10) return decolor16v<M>(w, k);
+    else return decolor16<M>(w, k);
+}
+
 constexpr int kTileBytes = 256 * 48;  // 4096 px
 
 // ---------------- variant A: CTA-wide barrier ring (library kernel) ----------------
@@ -188,6 +241,7 @@ __global__ void __launch_bounds__(256, MINB) k_sync(const uint8_t* __restrict__ 
         mbar_wait(&bars[s], ph);
         const uint4* src = reinterpret_cast<const uint4*>(smem + s * kTileBytes) + tid * 3;
         uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+        fence_proxy_async_smem();
         __syncthreads();
         if (tid == 0) {
             int64_t tn = t + STAGES * stride;
@@ -240,6 +294,7 @@ __global__ void __launch_bounds__(288, MINB) k_ws(const uint8_t* __restrict__ in
         mbar_wait(&full[s], ph);
         const uint4* src = reinterpret_cast<const uint4*>(smem + s * kTileBytes) + tid * 3;
         uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
         const uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
@@ -265,8 +320,39 @@ __global__ void __launch_bounds__(256, MINB) k_ldg(const uint8_t* __restrict__ i
             n0 = __ldcs(q); n1 = __ldcs(q + 1); n2 = __ldcs(q + 2);
         }
         const uint32_t w[12] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y, v2.z, v2.w};
-        st_global_cs_v4(out + t * 4096 + tid * 16, decolor16<MATH>(w, k));
+        st_global_cs_v4(out + t * 4096 + tid * 16, dec16<MATH>(w, k));
         v0 = n0; v1 = n1; v2 = n2;
+    }
+}
+
+// ---------------- variant C2: 32 px per thread (two 16-px groups), register prefetch ----------------
+template <int MINB, int MATH>
+__global__ void __launch_bounds__(256, MINB) k_ldg32(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                                                     int64_t ntiles2, U8Consts k) {
+    // tile = 8192 px = 24576 B; thread owns 96 B = 6 x uint4 (two 48 B halves 12 KiB apart)
+    const int tid = threadIdx.x;
+    const int64_t stride = gridDim.x;
+    int64_t t = blockIdx.x;
+    if (t >= ntiles2) return;
+    auto ld = [&](int64_t tt, uint4 (&v)[6]) {
+        const uint4* p = reinterpret_cast<const uint4*>(in + tt * 2 * kTileBytes) + tid * 3;
+        const uint4* q = p + kTileBytes / 16;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) { v[j] = __ldcs(p + j); v[3 + j] = __ldcs(q + j); }
+    };
+    uint4 v[6];
+    ld(t, v);
+    for (; t < ntiles2; t += stride) {
+        uint4 n[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) n[j] = v[j];
+        if (t + stride < ntiles2) ld(t + stride, n);
+        const uint32_t w0[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
+        const uint32_t w1[12] = {v[3].x, v[3].y, v[3].z, v[3].w, v[4].x, v[4].y, v[4].z, v[4].w, v[5].x, v[5].y, v[5].z, v[5].w};
+        st_global_cs_v4(out + t * 8192 + tid * 16, dec16<MATH>(w0, k));
+        st_global_cs_v4(out + t * 8192 + 4096 + tid * 16, dec16<MATH>(w1, k));
+#pragma unroll
+        for (int j = 0; j < 6; ++j) v[j] = n[j];
     }
 }
 
@@ -328,6 +414,7 @@ __global__ void __launch_bounds__(256, MINB) k_wtma(const uint8_t* __restrict__ 
         mbar_wait(&bars[s], ph);
         const uint4* src = reinterpret_cast<const uint4*>(ring + s * kWarpTile) + lane * 3;
         uint4 v0 = src[0], v1 = src[1], v2 = src[2];
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
             int64_t tn = t + STAGES * nw;
@@ -394,18 +481,23 @@ int main() {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, sm); int occ = 0; \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, sm); int64_t g = (int64_t)occ * sms; \
     res.push_back(time_it("wtma st=" #ST " minb=" #MB " math=" #M, [&] { kern<<<g, 256, sm>>>(in, out, npx / 512, k); }, out, ref, npx)); }
-    SYNC(4, 4, 0)
-    SYNC(4, 4, 2)
-    LDG(4, 2, 16)
-    LDG(4, 2, 4)
-    LDG2(4, 2, 16)
-    LDG2(4, 2, 4)
-    LDG2(3, 2, 12)
-    WTMA(4, 4, 2)
-    WTMA(6, 3, 2)
-    WTMA(8, 3, 2)
-    WTMA(3, 4, 2)
-    WTMA(8, 2, 2)
+#define LDG32(MB, M, MULT) { auto kern = k_ldg32<MB, M>; int64_t g = std::min<int64_t>(ntiles / 2, (int64_t)sms * MULT); \
+    res.push_back(time_it("ldg32 minb=" #MB " math=" #M " grid=" #MULT "xSM", [&] { kern<<<g, 256>>>(in, out, ntiles / 2, k); }, out, ref, npx)); }
+    LDG(4, 0, 16)
+    if (ref.empty()) { ref.resize(npx); cudaMemcpy(ref.data(), out, npx, cudaMemcpyDeviceToHost); }
+    LDG(5, 0, 20)
+    LDG(5, 0, 10)
+    LDG(5, 0, 40)
+    LDG(5, 0, 5)
+    LDG(5, 10, 20)
+    LDG(5, 11, 20)
+    LDG(6, 0, 24)
+    LDG(6, 0, 12)
+    LDG(6, 0, 6)
+    LDG(6, 11, 24)
+    LDG(7, 0, 28)
+    LDG(8, 0, 32)
+    LDG32(5, 0, 10)
     // cube parity of each math variant vs the fp64 oracle
     {
         const int64_t nc = 1 << 24;
