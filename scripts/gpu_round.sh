@@ -1,18 +1,23 @@
 #!/bin/bash
-# One GPU pass: parity tests, the bench line per workload, and the ncu evidence
-# (launch list + one full capture of the hot kernel) for the C3 bench command.
+# One GPU pass: smoke, parity tests, the bench line per workload (+ reference arm
+# and a torchrun launch), and the ncu evidence (launch list + one full capture of
+# the hot kernel) for the C3 bench command.
 # Usage (from the repo root, under gpurun):  bash scripts/gpu_round.sh [tag]
 TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/nvsmi_$TAG.txt 2>&1
-python __graft_entry__.py smoke > $OUT/smoke_$TAG.log 2>&1; echo "smoke=$?"
+timeout 300 python __graft_entry__.py smoke > $OUT/smoke_$TAG.log 2>&1; echo "smoke=$?"
 timeout 1200 python -m pytest tests -m gpu -q -s -p no:cacheprovider > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest_gpu=$?"
-tail -2 $OUT/pytest_gpu_$TAG.log
-for W in C3 C2 C4 C1; do
+tail -1 $OUT/pytest_gpu_$TAG.log
+timeout 600 python bench.py > $OUT/bench_default_$TAG.json 2> $OUT/bench_default_$TAG.err; echo "bench_default=$?"
+for W in C2 C4 C1; do
   timeout 600 python bench.py --workload $W --steps 50 --warmup 5 --cpu-seconds 5 > $OUT/bench_${W}_$TAG.json 2> $OUT/bench_${W}_$TAG.err; echo "bench_$W=$?"
 done
-timeout 900 python bench.py --workload C5 --steps 5 --warmup 3 --no-cpu > $OUT/bench_C5_$TAG.json 2> $OUT/bench_C5_$TAG.err; echo "bench_C5=$?"
+timeout 900 python bench.py --workload C5 --steps 5 --warmup 3 --cpu-seconds 5 > $OUT/bench_C5_$TAG.json 2> $OUT/bench_C5_$TAG.err; echo "bench_C5=$?"
+timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err; echo "bench_ref=$?"
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
+  bench.py --gpus 1 --steps 20 --warmup 3 --no-cpu > $OUT/bench_torchrun_$TAG.json 2> $OUT/bench_torchrun_$TAG.err; echo "bench_torchrun=$?"
 B="python bench.py --workload C3 --steps 5 --warmup 3 --no-e2e --no-cpu"
 $B > $OUT/ncu_plain_$TAG.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $B > $OUT/ncu_launch_$TAG.log 2>&1
