@@ -119,7 +119,24 @@ WG_API int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64
                       float beta_r, float beta_k, float midpoint, float slope, void* scratch,
                       size_t scratch_bytes, void* stream);
 
+/* ---- baseline luminance extractors (_kernels.pyx:59-132) ----
+ * method: 0 = BT.601 luma (bt601_rows, also "weighted"), 1 = HSV V
+ * (hsv_value_rows), 2 = CIELAB lightness / 100 (lab_lightness_rows). fp64
+ * follows the reference's operation order (BT.601 and V bit-identical; Lab to
+ * the last ulp of pow/cbrt). wg_lab_f64 = lab_rows: (L*, a*, b*) per pixel. */
+WG_API int wg_luma_f64(const double* rgb, double* out, int64_t npix, int method, void* stream);
+WG_API int wg_lab_f64(const double* rgb, double* lab, int64_t npix, void* stream);
+WG_API int wg_luma_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, int method, void* stream);
+
 /* ---- host-buffer entry points (synchronous; pipelined H2D/compute/D2H) ---- */
+
+/* bt601_rows / hsv_value_rows / lab_lightness_rows and lab_rows on host fp64
+ * buffers, with the plugin's (rgb, out, ..., row0, row1) contract. */
+WG_API int wg_host_luma_rows_f64(const double* rgb, double* out, int64_t height, int64_t width, int method,
+                                 int64_t row0, int64_t row1, int device);
+WG_API int wg_host_lab_rows_f64(const double* rgb, double* lab, int64_t height, int64_t width, int64_t row0,
+                                int64_t row1, int device);
+WG_API int wg_host_luma_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, int method, int device);
 
 /* The plugin call itself: fills out[row0:row1] of an (height, width) fp64
  * gray image from rgb (height, width, 3) fp64, like

@@ -32,6 +32,9 @@ _SIGS = {
     "or_decolor_f64": [_c_dp, _c_dp, _i64, _d, _d, _i],
     "or_decolor_f32in": [_c_fp, _c_dp, _i64, _d, _d, _i],
     "or_decolor_u8": [_c_u8p, _c_u8p, _i64, _d, _d, _i],
+    "or_luma_f64": [_c_dp, _c_dp, _i64, _i, _i],
+    "or_lab_f64": [_c_dp, _c_dp, _i64, _i],
+    "or_luma_u8": [_c_u8p, _c_u8p, _i64, _i, _i],
     "or_sigmoid_f64": [_c_dp, _c_dp, _i64, _d, _d],
     "or_reinstate_f64": [_c_dp, _c_dp, _c_dp, _c_dp, _i64],
     "or_tone_u8": [_c_u8p, _c_u8p, _c_u8p, _i64, _d, _d, _d, _d, _i],
@@ -97,6 +100,35 @@ def decolor_u8(rgb: np.ndarray, beta_r=0.55, beta_k=0.8, threads: int = 1) -> np
     out = np.empty(rgb.shape[:-1], dtype=np.uint8)
     lib().or_decolor_u8(_ptr(rgb, ctypes.c_uint8), _ptr(out, ctypes.c_uint8),
                         out.size, beta_r, beta_k, threads)
+    return out
+
+
+LUMA_METHODS = {"y": 0, "weighted": 0, "v": 1, "lab": 2}
+
+
+def luma_f64(rgb: np.ndarray, method: str, threads: int = 1) -> np.ndarray:
+    """bt601_rows / hsv_value_rows / lab_lightness_rows (_kernels.pyx:59-112) on fp64 rgb."""
+    rgb = np.ascontiguousarray(rgb, dtype=np.float64)
+    out = np.empty(rgb.shape[:-1], dtype=np.float64)
+    lib().or_luma_f64(_ptr(rgb, ctypes.c_double), _ptr(out, ctypes.c_double), out.size,
+                      LUMA_METHODS[method], threads)
+    return out
+
+
+def lab_f64(rgb: np.ndarray, threads: int = 1) -> np.ndarray:
+    """lab_rows (_kernels.pyx:115-132): (..., 3) CIELAB of fp64 rgb."""
+    rgb = np.ascontiguousarray(rgb, dtype=np.float64)
+    out = np.empty_like(rgb)
+    lib().or_lab_f64(_ptr(rgb, ctypes.c_double), _ptr(out, ctypes.c_double), rgb.size // 3, threads)
+    return out
+
+
+def luma_u8(rgb: np.ndarray, method: str, threads: int = 1) -> np.ndarray:
+    """quantize_u8(luminance_image(dequantize_u8(rgb), method).data)."""
+    rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+    out = np.empty(rgb.shape[:-1], dtype=np.uint8)
+    lib().or_luma_u8(_ptr(rgb, ctypes.c_uint8), _ptr(out, ctypes.c_uint8), out.size,
+                     LUMA_METHODS[method], threads)
     return out
 
 

@@ -158,6 +158,88 @@ OR_API void or_decolor_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, double
     run_spans(npix, threads, dec8_span, &c);
 }
 
+/* ------------------------------------------------------------------ */
+/* baseline luminance extractors, _kernels.pyx:59-132 */
+
+/* D65 sRGB -> XYZ rows and white point, _kernels.pyx:14-20 */
+static const double CS_M[3][3] = {{0.4124564, 0.3575761, 0.1804375},
+                                  {0.2126729, 0.7151522, 0.0721750},
+                                  {0.0193339, 0.1191920, 0.9503041}};
+static const double CS_WX = 0.95047, CS_WZ = 1.08883;
+#define CS_EPS (216.0 / 24389.0)
+#define CS_KAPPA (24389.0 / 27.0)
+
+/* bt601_rows (_kernels.pyx:59-68): weighted sum then clamp */
+static inline double cs_bt601(double r, double g, double b) {
+    return clamp01(0.2989 * r + 0.5870 * g + 0.1140 * b);
+}
+/* hsv_value_rows (_kernels.pyx:71-84): strict-greater max, r first */
+static inline double cs_hsv_v(double r, double g, double b) {
+    double v = r;
+    if (g > v) v = g;
+    if (b > v) v = b;
+    return v;
+}
+/* _srgb_to_linear / _lab_f (_kernels.pyx:87-96): glibc pow / cbrt */
+static inline double cs_lin(double c) { return c <= 0.04045 ? c / 12.92 : pow((c + 0.055) / 1.055, 2.4); }
+static inline double cs_f(double t) { return t > CS_EPS ? cbrt(t) : (CS_KAPPA * t + 16.0) / 116.0; }
+static inline double cs_row(int k, double lr, double lg, double lb) {
+    return CS_M[k][0] * lr + CS_M[k][1] * lg + CS_M[k][2] * lb;
+}
+/* lab_lightness_rows (_kernels.pyx:99-112) */
+static inline double cs_lab_l(double r, double g, double b) {
+    double l = 116.0 * cs_f(cs_row(1, cs_lin(r), cs_lin(g), cs_lin(b))) - 16.0;
+    return clamp01(l / 100.0);
+}
+static inline double cs_luma(int method, double r, double g, double b) {
+    return method == 0 ? cs_bt601(r, g, b) : method == 1 ? cs_hsv_v(r, g, b) : cs_lab_l(r, g, b);
+}
+
+typedef struct { const double* rgb; double* out; int method; } luma64_ctx;
+static void luma64_span(void* c, int64_t p0, int64_t p1) {
+    luma64_ctx* x = (luma64_ctx*)c;
+    for (int64_t i = p0; i < p1; ++i)
+        x->out[i] = cs_luma(x->method, x->rgb[3 * i], x->rgb[3 * i + 1], x->rgb[3 * i + 2]);
+}
+/* method 0 = bt601_rows, 1 = hsv_value_rows, 2 = lab_lightness_rows */
+OR_API void or_luma_f64(const double* rgb, double* out, int64_t npix, int method, int threads) {
+    luma64_ctx c = {rgb, out, method};
+    run_spans(npix, threads, luma64_span, &c);
+}
+
+typedef struct { const double* rgb; double* lab; } lab64_ctx;
+static void lab64_span(void* c, int64_t p0, int64_t p1) {
+    lab64_ctx* x = (lab64_ctx*)c;
+    for (int64_t i = p0; i < p1; ++i) {
+        const double* p = x->rgb + 3 * i;
+        double lr = cs_lin(p[0]), lg = cs_lin(p[1]), lb = cs_lin(p[2]);
+        double fx = cs_f(cs_row(0, lr, lg, lb) / CS_WX);
+        double fy = cs_f(cs_row(1, lr, lg, lb));
+        double fz = cs_f(cs_row(2, lr, lg, lb) / CS_WZ);
+        x->lab[3 * i] = 116.0 * fy - 16.0;
+        x->lab[3 * i + 1] = 500.0 * (fx - fy);
+        x->lab[3 * i + 2] = 200.0 * (fy - fz);
+    }
+}
+/* lab_rows (_kernels.pyx:115-132) */
+OR_API void or_lab_f64(const double* rgb, double* lab, int64_t npix, int threads) {
+    lab64_ctx c = {rgb, lab};
+    run_spans(npix, threads, lab64_span, &c);
+}
+
+/* uint8 -> uint8: quantize_u8(luminance_image(dequantize_u8(u8), method).data) */
+typedef struct { const uint8_t* rgb; uint8_t* out; int method; } luma8_ctx;
+static void luma8_span(void* c, int64_t p0, int64_t p1) {
+    luma8_ctx* x = (luma8_ctx*)c;
+    for (int64_t i = p0; i < p1; ++i)
+        x->out[i] = quantize(cs_luma(x->method, dequantize(x->rgb[3 * i]), dequantize(x->rgb[3 * i + 1]),
+                                     dequantize(x->rgb[3 * i + 2])));
+}
+OR_API void or_luma_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, int method, int threads) {
+    luma8_ctx c = {rgb, out, method};
+    run_spans(npix, threads, luma8_span, &c);
+}
+
 /* apply_sigmoid on fp64 luminance (tonemap.py:72-83) */
 OR_API void or_sigmoid_f64(const double* in, double* out, int64_t n, double midpoint,
                            double slope) {

@@ -29,11 +29,24 @@ from .batch import (
     decolor_tone_host,
     hdr_tonemap,
     hdr_tonemap_host,
+    lab,
+    luma,
+    luma_host,
     sigmoid,
 )
 from .codec import dequantize_u8, quantize_u8
 from .perf import BenchResult, format_table, run_benchmark
-from .colorspaces import METHOD_NAMES, luminance_image
+from .colorspaces import (
+    METHOD_NAMES,
+    LabColor,
+    delta_e76,
+    hsv_v,
+    lab_image,
+    lab_lightness,
+    luma_weighted,
+    luminance_image,
+    rgb_to_lab,
+)
 from .core import (
     DEFAULT_PARAMS,
     DecolorParams,
@@ -72,6 +85,13 @@ __all__ = [
     "run_benchmark",
     "METHOD_NAMES",
     "luminance_image",
+    "lab_image",
+    "LabColor",
+    "luma_weighted",
+    "hsv_v",
+    "rgb_to_lab",
+    "lab_lightness",
+    "delta_e76",
     "DEFAULT_PARAMS",
     "DecolorParams",
     "PlanarImage",
@@ -97,4 +117,7 @@ __all__ = [
     "decolor_host",
     "decolor_tone_host",
     "hdr_tonemap_host",
+    "luma",
+    "lab",
+    "luma_host",
 ]

@@ -58,6 +58,12 @@ SIGNATURES = {
     "wg_dequantize_u8_f64": (_i, [_vp, _vp, _i64, _vp]),
     "wg_hdr_scratch_bytes": (_sz, [_i64, _i64]),
     "wg_hdr_tonemap_u8": (_i, [_vp, _vp, _i64, _i64, _f, _f, _f, _f, _vp, _sz, _vp]),
+    "wg_luma_f64": (_i, [_vp, _vp, _i64, _i, _vp]),
+    "wg_lab_f64": (_i, [_vp, _vp, _i64, _vp]),
+    "wg_luma_u8": (_i, [_vp, _vp, _i64, _i, _vp]),
+    "wg_host_luma_rows_f64": (_i, [_vp, _vp, _i64, _i64, _i, _i64, _i64, _i]),
+    "wg_host_lab_rows_f64": (_i, [_vp, _vp, _i64, _i64, _i64, _i64, _i]),
+    "wg_host_luma_u8": (_i, [_vp, _vp, _i64, _i, _i]),
     "wg_host_decolor_rows_f64": (_i, [_vp, _vp, _i64, _i64, _d, _d, _i64, _i64, _i]),
     "wg_host_decolor_u8": (_i, [_vp, _vp, _i64, _f, _f, _i]),
     "wg_host_decolor_f32": (_i, [_vp, _vp, _i64, _f, _f, _i]),

@@ -124,6 +124,41 @@ def sigmoid(lum, curve: SigmoidCurve = SigmoidCurve(), stream=None):
     return out
 
 
+_LUMA_METHOD = {"y": 0, "weighted": 0, "v": 1, "lab": 2}
+
+
+def _luma_code(method: str) -> int:
+    if method not in _LUMA_METHOD:
+        raise ValueError(f"unknown luma method {method!r} (have: {', '.join(_LUMA_METHOD)})")
+    return _LUMA_METHOD[method]
+
+
+def luma(rgb, method: str = "y", stream=None):
+    """Baseline gray of a device (..., 3) uint8 / float64 batch.
+
+    float64 follows the reference's bt601_rows / hsv_value_rows /
+    lab_lightness_rows; uint8 is quantize_u8 of that on dequantized input.
+    """
+    torch = _torch()
+    name = _check_rgb_tensor(rgb, ("uint8", "float64"))
+    code = _luma_code(method)
+    out = torch.empty(rgb.shape[:-1], dtype=rgb.dtype, device=rgb.device)
+    with torch.cuda.device(rgb.device):
+        _lib.call("wg_luma_u8" if name == "uint8" else "wg_luma_f64", rgb.data_ptr(), out.data_ptr(),
+                  out.numel(), code, _stream(stream, rgb.device))
+    return out
+
+
+def lab(rgb, stream=None):
+    """CIELAB (L*, a*, b*) of a device (..., 3) float64 sRGB batch (lab_rows)."""
+    torch = _torch()
+    _check_rgb_tensor(rgb, ("float64",))
+    out = torch.empty_like(rgb)
+    with torch.cuda.device(rgb.device):
+        _lib.call("wg_lab_f64", rgb.data_ptr(), out.data_ptr(), rgb.numel() // 3, _stream(stream, rgb.device))
+    return out
+
+
 class HdrScratch:
     """Reusable device scratch for :func:`hdr_tonemap` (gray plane + per-block partials)."""
 
@@ -185,6 +220,17 @@ def decolor_host(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, device: 
         else:
             _lib.call("wg_host_decolor_rows_f64", arr.ctypes.data, out.ctypes.data, 1, n,
                       params.beta_r, params.beta_k, 0, 1, dev)
+    return out
+
+
+def luma_host(rgb, method: str = "y", device: int | None = None):
+    """Baseline gray of a host uint8 (..., 3) array -> uint8 via the pipelined host path."""
+    arr = _host_rgb(rgb, ("uint8",))
+    code = _luma_code(method)
+    out = np.empty(arr.shape[:-1], dtype=np.uint8)
+    if out.size:
+        _lib.call("wg_host_luma_u8", arr.ctypes.data, out.ctypes.data, out.size, code,
+                  get_device() if device is None else device)
     return out
 
 

@@ -255,6 +255,52 @@ extern "C" int wg_host_decolor_rows_f64(const double* rgb, double* out, int64_t 
                          });
 }
 
+extern "C" int wg_host_luma_rows_f64(const double* rgb, double* out, int64_t height, int64_t width, int method,
+                                     int64_t row0, int64_t row1, int device) {
+    WG_CHECK_ARGS(check_npix(height) || check_npix(width));
+    if (row0 < 0 || row1 > height || row0 > row1)
+        return set_error(WG_EINVAL, "row range [%lld, %lld) outside [0, %lld]", (long long)row0,
+                         (long long)row1, (long long)height);
+    if (method < 0 || method > 2) return set_error(WG_EINVAL, "luma method must be 0, 1 or 2");
+    const int64_t npix = (row1 - row0) * width;
+    WG_CHECK_ARGS(check_ptrs(npix, rgb, out));
+    HostIn in[1] = {{rgb + row0 * width * 3, 24}};
+    HostOut o[1] = {{out + row0 * width, 8}};
+    return host_pipeline(device, npix, in, 1, o, 1, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_luma_f64(static_cast<const double*>(di[0]), static_cast<double*>(dout[0]), n,
+                                                method, st);
+                         });
+}
+
+extern "C" int wg_host_lab_rows_f64(const double* rgb, double* lab, int64_t height, int64_t width, int64_t row0,
+                                    int64_t row1, int device) {
+    WG_CHECK_ARGS(check_npix(height) || check_npix(width));
+    if (row0 < 0 || row1 > height || row0 > row1)
+        return set_error(WG_EINVAL, "row range [%lld, %lld) outside [0, %lld]", (long long)row0,
+                         (long long)row1, (long long)height);
+    const int64_t npix = (row1 - row0) * width;
+    WG_CHECK_ARGS(check_ptrs(npix, rgb, lab));
+    HostIn in[1] = {{rgb + row0 * width * 3, 24}};
+    HostOut o[1] = {{lab + row0 * width * 3, 24}};
+    return host_pipeline(device, npix, in, 1, o, 1, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_lab_f64(static_cast<const double*>(di[0]), static_cast<double*>(dout[0]), n, st);
+                         });
+}
+
+extern "C" int wg_host_luma_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, int method, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, out));
+    if (method < 0 || method > 2) return set_error(WG_EINVAL, "luma method must be 0, 1 or 2");
+    HostIn in[1] = {{rgb, 3}};
+    HostOut o[1] = {{out, 1}};
+    return host_pipeline(device, npix, in, 1, o, 1, 4096, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_luma_u8(static_cast<const uint8_t*>(di[0]), static_cast<uint8_t*>(dout[0]), n,
+                                               method, st);
+                         });
+}
+
 extern "C" int wg_host_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r,
                                   float beta_k, int device) {
     WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));

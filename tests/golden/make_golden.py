@@ -22,6 +22,11 @@ into this repository; only the outputs below are committed:
   tonemap_global.npz  tonemap_image(mode="global") on a seeded image
   hdr.npz             HDR adapter evaluated with the
                       reference's decolor_image/apply_sigmoid/quantize_u8
+  colorspaces.npz     bt601/hsv/lab_lightness/lab rows (compiled backend) on
+                      seeded fp64 images incl. sRGB / Lab branch points
+  colorspaces.json    scalar known answers (luma_weighted, hsv_v, rgb_to_lab,
+                      lab_lightness, delta_e76) and sha256 of the u8 cube
+                      through luminance_image for y / v / lab
 """
 
 from __future__ import annotations
@@ -194,8 +199,57 @@ def main() -> None:
             t = np.where(pos, 1.0, 0.0)
         outs.append(wg.quantize_u8(wg.apply_sigmoid(wg.PlanarImage(t)).data))
     np.savez_compressed(os.path.join(HERE, "hdr.npz"), rgb=hdr, out=np.stack(outs))
+    colorspaces_golden(wg, get_kernels)
     print("golden fixtures written to", HERE)
 
 
+def colorspaces_golden(wg, get_kernels) -> None:
+    """the reference's baseline extractors."""
+    comp = get_kernels("compiled")
+    rng = np.random.default_rng(2108)
+    rgb = rng.random((37, 53, 3))
+    # exact branch points of the sRGB linearisation and the Lab compander
+    special = np.array([0.0, 1.0, 0.04045, np.nextafter(0.04045, 1), np.nextafter(0.04045, 0),
+                        0.5, 1e-300, 0.01, 0.2, 0.99999999])
+    edge = np.stack(np.meshgrid(special, special, special, indexing="ij"), -1).reshape(-1, 1, 3)
+    edge = np.ascontiguousarray(edge.reshape(len(special), -1, 3))
+    out = {"rgb": rgb, "edge": edge}
+    for tag, img in (("rgb", rgb), ("edge", edge)):
+        h = img.shape[0]
+        for name in ("bt601_rows", "hsv_value_rows", "lab_lightness_rows"):
+            o = np.empty(img.shape[:2])
+            getattr(comp, name)(img, o, 0, h)
+            out[f"{tag}_{name}"] = o
+        o3 = np.empty(img.shape)
+        comp.lab_rows(img, o3, 0, h)
+        out[f"{tag}_lab_rows"] = o3
+    np.savez_compressed(os.path.join(HERE, "colorspaces.npz"), **out)
+
+    pix = [(1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 1), (0, 0, 0), (0.3, 0.7, 0.2), (0.2, 0.5, 0.3),
+           (0.04045, 0.5, 0.9), (0.01, 0.02, 0.03)]
+    kat = {
+        "luma_weighted": [[list(map(float, p)), wg.luma_weighted(p)] for p in pix],
+        "hsv_v": [[list(map(float, p)), wg.hsv_v(p)] for p in pix],
+        "lab_lightness": [[list(map(float, p)), wg.lab_lightness(p)] for p in pix],
+        "rgb_to_lab": [[list(map(float, p)), list(map(float, (lambda c: (c.l_star, c.a_star, c.b_star))(
+            wg.rgb_to_lab(p))))] for p in pix],
+        "delta_e76": [[list(map(float, p)), list(map(float, q)),
+                       wg.delta_e76(wg.rgb_to_lab(p), wg.rgb_to_lab(q))] for p, q in zip(pix, pix[1:])],
+    }
+    cube = wg.PlanarImage(wg.dequantize_u8(color_cube_u8()))
+    for method in ("y", "v", "lab"):
+        g = wg.quantize_u8(wg.luminance_image(cube, method=method, backend="compiled").data)
+        kat[f"cube_{method}_u8_sha256"] = sha(g)
+        kat[f"cube_{method}_u8_histogram"] = np.bincount(g.ravel(), minlength=256).tolist()
+    with open(os.path.join(HERE, "colorspaces.json"), "w") as f:
+        json.dump(kat, f, indent=1)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["colorspaces"]:
+        sys.path.insert(0, build_reference())
+        import warmgray as _wg
+        from warmgray.backend import get_kernels as _gk
+        colorspaces_golden(_wg, _gk)
+        sys.exit(0)
     main()
