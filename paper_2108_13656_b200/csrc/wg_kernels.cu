@@ -21,13 +21,9 @@
 #include "../../include/warmgray_b200.h"
 #include "wg_device.cuh"
 #include "wg_internal.h"
+#include "wg_stream.cuh"
 
 namespace wg {
-
-constexpr int kThreads = 256;
-constexpr int kStages = 4;
-constexpr int kTileBytes = kThreads * 48;  // 12288 B: 48 input bytes per thread
-constexpr int kSmemBytes = kStages * kTileBytes + kStages * 8;
 
 // ------------------------------------------------------------------ ops
 // An Op consumes the 48 input bytes of one thread (3 x uint4, already in
@@ -172,157 +168,6 @@ struct OpToneF32 {
         one(in + 3 * p, s, p);
     }
 };
-
-// ------------------------------------------------------------------ streaming kernels
-template <class Op>
-__global__ void __launch_bounds__(kThreads) stream_kernel(Op op, const uint8_t* __restrict__ in,
-                                                          int64_t ntiles, int64_t npix) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kTileBytes);
-    constexpr int kTilePx = kThreads * Op::kPx;
-    const int tid = threadIdx.x;
-    const int64_t stride = gridDim.x;
-
-    if (tid == 0) {
-#pragma unroll
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-
-    uint64_t policy = 0;
-    if (tid == 0) {
-        policy = l2_policy_evict_first();
-#pragma unroll
-        for (int s = 0; s < kStages; ++s) {
-            const int64_t t = blockIdx.x + s * stride;
-            if (t < ntiles) {
-                mbar_arrive_expect_tx(&bars[s], kTileBytes);
-                bulk_g2s(smem + s * kTileBytes, in + t * kTileBytes, kTileBytes, &bars[s], policy);
-            }
-        }
-    }
-
-    int s = 0;
-    uint32_t phase = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += stride) {
-        mbar_wait(&bars[s], phase);
-        uint4 v[3];
-        const uint4* src = reinterpret_cast<const uint4*>(smem + s * kTileBytes) + tid * 3;
-        v[0] = src[0];
-        v[1] = src[1];
-        v[2] = src[2];
-        fence_proxy_async_smem();  // reads of slot s ordered before its TMA refill
-        __syncthreads();           // every thread has drained slot s
-        if (tid == 0) {
-            const int64_t tn = t + kStages * stride;
-            if (tn < ntiles) {
-                mbar_arrive_expect_tx(&bars[s], kTileBytes);
-                bulk_g2s(smem + s * kTileBytes, in + tn * kTileBytes, kTileBytes, &bars[s], policy);
-            }
-        }
-        op.vec(v, t * kTilePx + static_cast<int64_t>(tid) * Op::kPx);
-        if (++s == kStages) {
-            s = 0;
-            phase ^= 1u;
-        }
-    }
-
-    // tail (< one tile) by the last CTA
-    if (blockIdx.x == gridDim.x - 1) {
-        for (int64_t p = ntiles * kTilePx + tid; p < npix; p += kThreads) op.scalar(p);
-    }
-}
-
-// Register-prefetch variant: each thread loads its 48 bytes of tile t + grid
-// with three 128-bit loads (evict-first) before computing tile t, so the
-// next tile's HBM latency hides under this tile's math. No shared memory and
-// no barriers; used where the per-pixel math, not the memory pipe, is the
-// limiter (the uint8 path: scripts/tune_u8.cu measured it ahead of the
-// bulk-copy ring at equal parity).
-// Occupancy 5 CTAs/SM (<= 51 registers, no spills) and a 40 x SM grid measured
-// best on C3 (scripts/tune_u8.cu: 74.7% of the HBM roofline vs 70.9% at 4 CTAs/SM).
-template <class Op>
-__global__ void __launch_bounds__(kThreads, 5) ldg_stream_kernel(Op op, const uint8_t* __restrict__ in,
-                                                                 int64_t ntiles, int64_t npix) {
-    constexpr int kTilePx = kThreads * Op::kPx;
-    const int tid = threadIdx.x;
-    const int64_t stride = gridDim.x;
-    int64_t t = blockIdx.x;
-    if (t < ntiles) {
-        const uint4* p = reinterpret_cast<const uint4*>(in + t * kTileBytes) + tid * 3;
-        uint4 v[3] = {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)};
-        for (; t < ntiles; t += stride) {
-            uint4 n[3] = {v[0], v[1], v[2]};
-            if (t + stride < ntiles) {
-                const uint4* q = reinterpret_cast<const uint4*>(in + (t + stride) * kTileBytes) + tid * 3;
-                n[0] = __ldcs(q);
-                n[1] = __ldcs(q + 1);
-                n[2] = __ldcs(q + 2);
-            }
-            op.vec(v, t * kTilePx + static_cast<int64_t>(tid) * Op::kPx);
-            v[0] = n[0];
-            v[1] = n[1];
-            v[2] = n[2];
-        }
-    }
-    if (blockIdx.x == gridDim.x - 1) {
-        for (int64_t p = ntiles * kTilePx + tid; p < npix; p += kThreads) op.scalar(p);
-    }
-}
-
-template <class Op>
-__global__ void __launch_bounds__(kThreads) scalar_kernel(Op op, int64_t npix) {
-    for (int64_t p = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; p < npix;
-         p += static_cast<int64_t>(gridDim.x) * kThreads)
-        op.scalar(p);
-}
-
-// ------------------------------------------------------------------ launch helpers
-template <class Op>
-static int stream_grid(int device) {
-    static int occ_cache[kMaxDevices] = {0};
-    static int attr_set[kMaxDevices] = {0};
-    if (!attr_set[device]) {
-        cudaFuncSetAttribute(stream_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kSmemBytes);
-        attr_set[device] = 1;
-    }
-    if (!occ_cache[device]) {
-        int occ = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<Op>, kThreads,
-                                                      kSmemBytes);
-        occ_cache[device] = std::max(occ, 1);
-    }
-    return occ_cache[device] * sm_count(device);
-}
-
-template <class Op>
-static int launch_stream(const Op& op, const void* in, const void* const* outs, int nouts,
-                         int64_t npix, cudaStream_t stream) {
-    if (npix == 0) return WG_OK;
-    int device = 0;
-    cudaGetDevice(&device);
-    if (device < 0 || device >= kMaxDevices) return set_error(WG_ENODEV, "device ordinal out of range");
-    bool aligned = (reinterpret_cast<uintptr_t>(in) & 15) == 0;
-    for (int i = 0; i < nouts; ++i)
-        if (outs[i] && (reinterpret_cast<uintptr_t>(outs[i]) & 15) != 0) aligned = false;
-    constexpr int64_t kTilePx = kThreads * Op::kPx;
-    const int64_t ntiles = npix / kTilePx;
-    if (aligned && Op::kLdg) {
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, 40LL * sm_count(device)));
-        ldg_stream_kernel<Op><<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(
-            op, static_cast<const uint8_t*>(in), ntiles, npix);
-    } else if (aligned) {
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, stream_grid<Op>(device)));
-        stream_kernel<Op><<<static_cast<unsigned>(grid), kThreads, kSmemBytes, stream>>>(
-            op, static_cast<const uint8_t*>(in), ntiles, npix);
-    } else {
-        const int64_t blocks = std::min<int64_t>((npix + kThreads - 1) / kThreads, 148LL * 32);
-        scalar_kernel<Op><<<static_cast<unsigned>(blocks), kThreads, 0, stream>>>(op, npix);
-    }
-    return check_launch("stream kernel");
-}
 
 // ------------------------------------------------------------------ elementwise fp64 kernels
 __global__ void decolor_f64_kernel(const double* __restrict__ rgb, double* __restrict__ out,
