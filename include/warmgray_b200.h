@@ -128,6 +128,31 @@ WG_API int wg_luma_f64(const double* rgb, double* out, int64_t npix, int method,
 WG_API int wg_lab_f64(const double* rgb, double* lab, int64_t npix, void* stream);
 WG_API int wg_luma_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, int method, void* stream);
 
+/* ---- local tone map (tonemap.py:36-69, 86-169, 195-216) ----
+ * nimg images of height x width, tile-histogram equalisation with tiles of
+ * tile_w x tile_h (clamped to the image), `bins` >= 2 histogram bins and
+ * blend `strength` in [0, 1] (LocalHistogramGrid). Scratch from
+ * wg_lhe_scratch_bytes (0 = invalid arguments). */
+WG_API size_t wg_lhe_scratch_bytes(int64_t nimg, int64_t height, int64_t width, int64_t tile_w, int64_t tile_h,
+                                   int64_t bins);
+/* apply_local_lhe on fp64 luminance: bit-identical to the reference. */
+WG_API int wg_local_lhe_f64(const double* lum, double* out, int64_t nimg, int64_t height, int64_t width,
+                            int64_t tile_w, int64_t tile_h, int64_t bins, double strength, void* scratch,
+                            size_t scratch_bytes, void* stream);
+/* tonemap_image(mode="local") on fp64 rgb: gray = decolor, l_out = local lhe of gray,
+ * rgb_out = reinstate_color(rgb, gray, l_out). */
+WG_API int wg_tonemap_local_f64(const double* rgb, double* gray, double* l_out, double* rgb_out, int64_t nimg,
+                                int64_t height, int64_t width, double beta_r, double beta_k, int64_t tile_w,
+                                int64_t tile_h, int64_t bins, double strength, void* scratch, size_t scratch_bytes,
+                                void* stream);
+/* Fused uint8 batch: toned = quantize_u8(apply_local_lhe(decolor(rgb / 255))) and
+ * gray_or_null = quantize_u8(decolor(rgb / 255)); bit-identical to the fp64 reference
+ * (hence fp64 beta / strength: the exact route evaluates the reference chain with them). */
+WG_API int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null, int64_t nimg,
+                                    int64_t height, int64_t width, double beta_r, double beta_k, int64_t tile_w,
+                                    int64_t tile_h, int64_t bins, double strength, void* scratch,
+                                    size_t scratch_bytes, void* stream);
+
 /* ---- host-buffer entry points (synchronous; pipelined H2D/compute/D2H) ---- */
 
 /* bt601_rows / hsv_value_rows / lab_lightness_rows and lab_rows on host fp64
@@ -160,6 +185,14 @@ WG_API int wg_host_tonemap_global_f64(const double* rgb, double* l_out, double* 
                                int device);
 WG_API int wg_host_quantize_u8_f64(const double* in, uint8_t* out, int64_t n, int device);
 WG_API int wg_host_dequantize_u8_f64(const uint8_t* in, double* out, int64_t n, int device);
+WG_API int wg_host_local_lhe_f64(const double* lum, double* out, int64_t height, int64_t width, int64_t tile_w,
+                                 int64_t tile_h, int64_t bins, double strength, int device);
+WG_API int wg_host_tonemap_local_f64(const double* rgb, double* l_out, double* rgb_out, int64_t height,
+                                     int64_t width, double beta_r, double beta_k, int64_t tile_w, int64_t tile_h,
+                                     int64_t bins, double strength, int device);
+WG_API int wg_host_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null, int64_t nimg,
+                                         int64_t height, int64_t width, double beta_r, double beta_k, int64_t tile_w,
+                                         int64_t tile_h, int64_t bins, double strength, int device);
 WG_API int wg_host_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
                            float beta_r, float beta_k, float midpoint, float slope, int device);
 

@@ -35,6 +35,8 @@ _SIGS = {
     "or_luma_f64": [_c_dp, _c_dp, _i64, _i, _i],
     "or_lab_f64": [_c_dp, _c_dp, _i64, _i],
     "or_luma_u8": [_c_u8p, _c_u8p, _i64, _i, _i],
+    "or_local_lhe_f64": [_c_dp, _c_dp, _i64, _i64, _i64, _i64, _i64, _i, _d, _i],
+    "or_tone_local_u8": [_c_u8p, _c_u8p, _c_u8p, _i64, _i64, _i64, _d, _d, _i64, _i64, _i, _d, _i],
     "or_sigmoid_f64": [_c_dp, _c_dp, _i64, _d, _d],
     "or_reinstate_f64": [_c_dp, _c_dp, _c_dp, _c_dp, _i64],
     "or_tone_u8": [_c_u8p, _c_u8p, _c_u8p, _i64, _d, _d, _d, _d, _i],
@@ -130,6 +132,30 @@ def luma_u8(rgb: np.ndarray, method: str, threads: int = 1) -> np.ndarray:
     lib().or_luma_u8(_ptr(rgb, ctypes.c_uint8), _ptr(out, ctypes.c_uint8), out.size,
                      LUMA_METHODS[method], threads)
     return out
+
+
+def local_lhe_f64(lum: np.ndarray, tile_w: int, tile_h: int, bins: int = 256, strength: float = 0.7,
+                  threads: int = 1) -> np.ndarray:
+    """apply_local_lhe (tonemap.py:103-169) on (H, W) or (N, H, W) fp64 luminance."""
+    lum = np.ascontiguousarray(lum, dtype=np.float64)
+    n, h, w = (1,) + lum.shape if lum.ndim == 2 else lum.shape
+    out = np.empty_like(lum)
+    lib().or_local_lhe_f64(_ptr(lum, ctypes.c_double), _ptr(out, ctypes.c_double), n, h, w, tile_w, tile_h,
+                           bins, strength, threads)
+    return out
+
+
+def tone_local_u8(rgb: np.ndarray, tile_w: int, tile_h: int, bins: int = 256, strength: float = 0.7,
+                  beta_r=0.55, beta_k=0.8, threads: int = 1, with_gray: bool = False):
+    """quantize_u8(apply_local_lhe(decolor_image(dequantize_u8(rgb)))) per image of (N, H, W, 3) / (H, W, 3)."""
+    rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+    n, h, w = (1,) + rgb.shape[:2] if rgb.ndim == 3 else rgb.shape[:3]
+    toned = np.empty(rgb.shape[:-1], dtype=np.uint8)
+    gray = np.empty_like(toned) if with_gray else None
+    lib().or_tone_local_u8(_ptr(rgb, ctypes.c_uint8), _ptr(toned, ctypes.c_uint8),
+                           _ptr(gray, ctypes.c_uint8) if gray is not None else None, n, h, w, beta_r, beta_k,
+                           tile_w, tile_h, bins, strength, threads)
+    return (toned, gray) if with_gray else toned
 
 
 def sigmoid_f64(x: np.ndarray, midpoint=0.5, slope=8.0) -> np.ndarray:

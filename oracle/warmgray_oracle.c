@@ -348,6 +348,155 @@ OR_API void or_hdr_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_
 }
 
 /* ------------------------------------------------------------------ */
+/* Local tone map: apply_local_lhe (tonemap.py:103-169) on one fp64
+ * luminance image, written as plain loops in the reference's operation
+ * order. Tiles of min(tile, side) pixels (:128-129); bin = min(int(v*nb),
+ * nb-1) (:136); per-tile CDF curves clip((cdf-low)/(total-low), 0, 1) with
+ * identity tiles where low == total (:139-148); neighbour tiles and blend
+ * fractions from the tile centres (_axis_weights, :90-100); bilinear blend
+ * and identity mix (:150-166). */
+
+static inline int lhe_bin(double v, int nb) {
+    int k = (int)(v * (double)nb);
+    return k < nb - 1 ? k : nb - 1;
+}
+
+static inline double lhe_centre(int64_t k, int64_t step, int64_t len) {
+    int64_t s0 = k * step, s1 = s0 + step < len ? s0 + step : len;
+    return (double)(s0 + s1 - 1) / 2.0;
+}
+
+/* idx[pos], frac[pos] for one axis of `len` positions split into n spans of `step` */
+static void lhe_axis(int64_t len, int64_t step, int n, int* idx, double* frac) {
+    for (int64_t pos = 0; pos < len; ++pos) {
+        if (n == 1) {
+            idx[pos] = 0;
+            frac[pos] = 0.0;
+            continue;
+        }
+        int cnt = 0; /* number of centres <= pos (searchsorted side="right") */
+        while (cnt < n && lhe_centre(cnt, step, len) <= (double)pos) ++cnt;
+        int i = cnt - 1;
+        if (i < 0) i = 0;
+        if (i > n - 2) i = n - 2;
+        double c0 = lhe_centre(i, step, len), c1 = lhe_centre(i + 1, step, len);
+        double f = ((double)pos - c0) / (c1 - c0);
+        idx[pos] = i;
+        frac[pos] = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+    }
+}
+
+static void lhe_image(const double* data, double* out, int64_t h, int64_t w, int64_t tile_w, int64_t tile_h,
+                      int nb, double strength) {
+    if (h == 0 || w == 0) return;
+    int64_t tw = tile_w < w ? tile_w : w, th = tile_h < h ? tile_h : h;
+    int nx = (int)((w + tw - 1) / tw), ny = (int)((h + th - 1) / th);
+    int64_t ntile = (int64_t)nx * ny;
+    double* curves = (double*)calloc((size_t)(ntile * nb), sizeof(double));
+    char* ident = (char*)calloc((size_t)ntile, 1);
+    int64_t* hist = (int64_t*)malloc(sizeof(int64_t) * (size_t)nb);
+    for (int ty = 0; ty < ny; ++ty) {
+        for (int tx = 0; tx < nx; ++tx) {
+            memset(hist, 0, sizeof(int64_t) * (size_t)nb);
+            int64_t y1 = (ty + 1) * th < h ? (ty + 1) * th : h, x1 = (tx + 1) * tw < w ? (tx + 1) * tw : w;
+            for (int64_t y = ty * th; y < y1; ++y)
+                for (int64_t x = tx * tw; x < x1; ++x) hist[lhe_bin(data[y * w + x], nb)]++;
+            int64_t total = 0, low = -1;
+            for (int k = 0; k < nb; ++k) {
+                total += hist[k];
+                if (low < 0 && hist[k]) low = total;
+            }
+            double* c = curves + ((int64_t)ty * nx + tx) * nb;
+            if (low == total) {
+                ident[(int64_t)ty * nx + tx] = 1;
+            } else {
+                int64_t cdf = 0;
+                for (int k = 0; k < nb; ++k) {
+                    cdf += hist[k];
+                    double v = (double)(cdf - low) / (double)(total - low);
+                    c[k] = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+                }
+            }
+        }
+    }
+    int* xi = (int*)malloc(sizeof(int) * (size_t)w);
+    int* yi = (int*)malloc(sizeof(int) * (size_t)h);
+    double* xf = (double*)malloc(sizeof(double) * (size_t)w);
+    double* yf = (double*)malloc(sizeof(double) * (size_t)h);
+    lhe_axis(w, tw, nx, xi, xf);
+    lhe_axis(h, th, ny, yi, yf);
+    for (int64_t y = 0; y < h; ++y) {
+        int j0 = yi[y], j1 = ny > 1 ? j0 + 1 : 0;
+        double wy = yf[y];
+        for (int64_t x = 0; x < w; ++x) {
+            int i0 = xi[x], i1 = nx > 1 ? i0 + 1 : 0;
+            double wx = xf[x], v = data[y * w + x];
+            int b = lhe_bin(v, nb);
+            int64_t t00 = (int64_t)j0 * nx + i0, t01 = (int64_t)j0 * nx + i1;
+            int64_t t10 = (int64_t)j1 * nx + i0, t11 = (int64_t)j1 * nx + i1;
+            double c00 = ident[t00] ? v : curves[t00 * nb + b];
+            double c01 = ident[t01] ? v : curves[t01 * nb + b];
+            double c10 = ident[t10] ? v : curves[t10 * nb + b];
+            double c11 = ident[t11] ? v : curves[t11 * nb + b];
+            double top = c00 + wx * (c01 - c00);
+            double bottom = c10 + wx * (c11 - c10);
+            double eq = top + wy * (bottom - top);
+            out[y * w + x] = clamp01(v + strength * (eq - v));
+        }
+    }
+    free(curves);
+    free(ident);
+    free(hist);
+    free(xi);
+    free(yi);
+    free(xf);
+    free(yf);
+}
+
+typedef struct { const double* lum; double* out; int64_t h, w, tw, th; int nb; double s; } lhe_ctx;
+static void lhe_span(void* c, int64_t i0, int64_t i1) {
+    lhe_ctx* x = (lhe_ctx*)c;
+    for (int64_t i = i0; i < i1; ++i)
+        lhe_image(x->lum + i * x->h * x->w, x->out + i * x->h * x->w, x->h, x->w, x->tw, x->th, x->nb, x->s);
+}
+/* nimg images of h x w fp64 luminance, one image per thread */
+OR_API void or_local_lhe_f64(const double* lum, double* out, int64_t nimg, int64_t h, int64_t w, int64_t tile_w,
+                             int64_t tile_h, int nb, double strength, int threads) {
+    lhe_ctx c = {lum, out, h, w, tile_w, tile_h, nb, strength};
+    run_spans(nimg, threads, lhe_span, &c);
+}
+
+/* uint8 batch: toned = quantize_u8(apply_local_lhe(decolor_image(dequantize_u8(rgb)))),
+ * gray = quantize_u8(decolor_image(...)) (gray may be NULL) */
+typedef struct {
+    const uint8_t* rgb; uint8_t* toned; uint8_t* gray; int64_t h, w, tw, th; int nb; double s, br, bk;
+} tonel_ctx;
+static void tonel_span(void* c, int64_t i0, int64_t i1) {
+    tonel_ctx* x = (tonel_ctx*)c;
+    int64_t n = x->h * x->w;
+    double* g = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double* o = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = i0; i < i1; ++i) {
+        const uint8_t* p = x->rgb + i * n * 3;
+        for (int64_t k = 0; k < n; ++k)
+            g[k] = decolor_px(dequantize(p[3 * k]), dequantize(p[3 * k + 1]), dequantize(p[3 * k + 2]), x->br, x->bk);
+        lhe_image(g, o, x->h, x->w, x->tw, x->th, x->nb, x->s);
+        for (int64_t k = 0; k < n; ++k) {
+            x->toned[i * n + k] = quantize(o[k]);
+            if (x->gray) x->gray[i * n + k] = quantize(g[k]);
+        }
+    }
+    free(g);
+    free(o);
+}
+OR_API void or_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray, int64_t nimg, int64_t h, int64_t w,
+                             double beta_r, double beta_k, int64_t tile_w, int64_t tile_h, int nb, double strength,
+                             int threads) {
+    tonel_ctx c = {rgb, toned, gray, h, w, tile_w, tile_h, nb, strength, beta_r, beta_k};
+    run_spans(nimg, threads, tonel_span, &c);
+}
+
+/* ------------------------------------------------------------------ */
 /* Synthetic-workload restatements (integer-exact, so the device generators
  * in paper_2108_13656_b200/csrc/wg_synth.cu can be checked bit for bit). */
 

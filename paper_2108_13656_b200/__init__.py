@@ -27,6 +27,8 @@ from .batch import (
     decolor_host,
     decolor_tone,
     decolor_tone_host,
+    decolor_tone_local,
+    decolor_tone_local_host,
     hdr_tonemap,
     hdr_tonemap_host,
     lab,
@@ -120,4 +122,6 @@ __all__ = [
     "luma",
     "lab",
     "luma_host",
+    "decolor_tone_local",
+    "decolor_tone_local_host",
 ]

@@ -61,6 +61,15 @@ SIGNATURES = {
     "wg_luma_f64": (_i, [_vp, _vp, _i64, _i, _vp]),
     "wg_lab_f64": (_i, [_vp, _vp, _i64, _vp]),
     "wg_luma_u8": (_i, [_vp, _vp, _i64, _i, _vp]),
+    "wg_lhe_scratch_bytes": (_sz, [_i64, _i64, _i64, _i64, _i64, _i64]),
+    "wg_local_lhe_f64": (_i, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _d, _vp, _sz, _vp]),
+    "wg_tonemap_local_f64": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _d, _d, _i64, _i64, _i64, _d, _vp, _sz,
+                                  _vp]),
+    "wg_decolor_tone_local_u8": (_i, [_vp, _vp, _vp, _i64, _i64, _i64, _d, _d, _i64, _i64, _i64, _d, _vp, _sz,
+                                      _vp]),
+    "wg_host_local_lhe_f64": (_i, [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _d, _i]),
+    "wg_host_tonemap_local_f64": (_i, [_vp, _vp, _vp, _i64, _i64, _d, _d, _i64, _i64, _i64, _d, _i]),
+    "wg_host_decolor_tone_local_u8": (_i, [_vp, _vp, _vp, _i64, _i64, _i64, _d, _d, _i64, _i64, _i64, _d, _i]),
     "wg_host_luma_rows_f64": (_i, [_vp, _vp, _i64, _i64, _i, _i64, _i64, _i]),
     "wg_host_lab_rows_f64": (_i, [_vp, _vp, _i64, _i64, _i64, _i64, _i]),
     "wg_host_luma_u8": (_i, [_vp, _vp, _i64, _i, _i]),

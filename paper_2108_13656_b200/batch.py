@@ -159,6 +159,45 @@ def lab(rgb, stream=None):
     return out
 
 
+def _grid_for(h, w, grid):
+    from .tonemap import LocalHistogramGrid
+
+    return grid or LocalHistogramGrid.for_image(w, h)
+
+
+def _nhw(shape):
+    if len(shape) == 3:
+        return 1, shape[0], shape[1]
+    if len(shape) == 4:
+        return shape[0], shape[1], shape[2]
+    raise ValueError(f"expected (H, W, 3) or (N, H, W, 3), got shape {tuple(shape)}")
+
+
+def decolor_tone_local(rgb, grid=None, params: DecolorParams = DEFAULT_PARAMS, return_gray: bool = False,
+                       scratch=None, stream=None):
+    """Fused decolor + local tone map of a device uint8 (N, H, W, 3) / (H, W, 3) batch.
+
+    Per image: toned = quantize_u8(apply_local_lhe(decolor_image(rgb / 255), grid)),
+    bit-identical to the fp64 reference; ``return_gray`` adds quantize_u8 of the
+    gray. ``grid`` defaults to LocalHistogramGrid.for_image(W, H).
+    """
+    torch = _torch()
+    _check_rgb_tensor(rgb, ("uint8",))
+    n, h, w = _nhw(rgb.shape)
+    g = _grid_for(h, w, grid)
+    toned = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=rgb.device)
+    gray = torch.empty_like(toned) if return_gray else None
+    need = int(_lib.load().wg_lhe_scratch_bytes(n, h, w, g.tile_w, g.tile_h, g.bins))
+    if scratch is None or scratch.numel() < need:
+        scratch = torch.empty(max(need, 1), dtype=torch.uint8, device=rgb.device)
+    with torch.cuda.device(rgb.device):
+        _lib.call("wg_decolor_tone_local_u8", rgb.data_ptr(), toned.data_ptr(),
+                  gray.data_ptr() if gray is not None else None, n, h, w, params.beta_r, params.beta_k,
+                  g.tile_w, g.tile_h, g.bins, g.strength, scratch.data_ptr(), scratch.numel(),
+                  _stream(stream, rgb.device))
+    return (toned, gray) if return_gray else toned
+
+
 class HdrScratch:
     """Reusable device scratch for :func:`hdr_tonemap` (gray plane + per-block partials)."""
 
@@ -232,6 +271,20 @@ def luma_host(rgb, method: str = "y", device: int | None = None):
         _lib.call("wg_host_luma_u8", arr.ctypes.data, out.ctypes.data, out.size, code,
                   get_device() if device is None else device)
     return out
+
+
+def decolor_tone_local_host(rgb, grid=None, params: DecolorParams = DEFAULT_PARAMS, return_gray: bool = False,
+                            device: int | None = None):
+    """:func:`decolor_tone_local` on a host uint8 (N, H, W, 3) / (H, W, 3) array (pipelined per image)."""
+    arr = _host_rgb(rgb, ("uint8",))
+    n, h, w = _nhw(arr.shape)
+    g = _grid_for(h, w, grid)
+    toned = np.empty(arr.shape[:-1], dtype=np.uint8)
+    gray = np.empty_like(toned) if return_gray else None
+    _lib.call("wg_host_decolor_tone_local_u8", arr.ctypes.data, toned.ctypes.data,
+              gray.ctypes.data if gray is not None else None, n, h, w, params.beta_r, params.beta_k,
+              g.tile_w, g.tile_h, g.bins, g.strength, get_device() if device is None else device)
+    return (toned, gray) if return_gray else toned
 
 
 def decolor_tone_host(rgb, curve: SigmoidCurve = SigmoidCurve(),

@@ -109,19 +109,6 @@ struct LabTables {
     float prodf[3][256];  // the same products rounded to fp32 (hot path)
 };
 
-__device__ __forceinline__ uint32_t quantize_d(double v) {
-    // codec.py:22-25: floor(clip(v, 0, 1) * 255 + 0.5)
-    return static_cast<uint32_t>(__dadd_rn(__dmul_rn(clamp01_d(v), 255.0), 0.5));
-}
-
-// k / 255.0 correctly rounded for every byte k (one FMA correction of k * fl(1/255);
-// checked exhaustively against IEEE division over k = 0..255)
-__device__ __forceinline__ double deq_byte(uint32_t k) {
-    const double inv = 1.0 / 255.0, x = static_cast<double>(k);
-    const double q0 = __dmul_rn(x, inv);
-    return __fma_rn(__fma_rn(-q0, 255.0, x), inv, q0);
-}
-
 // the reference's fp64 expression, for the exact-tie pixels
 __device__ __forceinline__ uint32_t bt601_u8_tie(uint32_t r, uint32_t g, uint32_t b) {
     return quantize_d(bt601_d(deq_byte(r), deq_byte(g), deq_byte(b)));

@@ -365,6 +365,20 @@ __device__ __forceinline__ double decolor_f64(double r, double g, double b, doub
                                           __dmul_rn(__dmul_rn(__dsub_rn(1.0, bk), cool), cool))));
 }
 
+// dequantize_u8 (codec.py:28-29): k / 255.0 correctly rounded for every byte k,
+// as one FMA correction of k * fl(1/255) (checked exhaustively against IEEE
+// division over k = 0..255).
+__device__ __forceinline__ double deq_byte(uint32_t k) {
+    const double inv = 1.0 / 255.0, x = static_cast<double>(k);
+    const double q0 = __dmul_rn(x, inv);
+    return __fma_rn(__fma_rn(-q0, 255.0, x), inv, q0);
+}
+
+// quantize_u8 (codec.py:22-25) in fp64: floor(clip(v, 0, 1) * 255 + 0.5)
+__device__ __forceinline__ uint32_t quantize_d(double v) {
+    return static_cast<uint32_t>(__dadd_rn(__dmul_rn(clamp01_d(v), 255.0), 0.5));
+}
+
 // apply_sigmoid in fp64, logistic form exactly as tonemap.py:76-83.
 struct SigD {
     double m, k, lo, hi;

@@ -405,6 +405,81 @@ extern "C" int wg_host_dequantize_u8_f64(const uint8_t* in_, double* out, int64_
                          });
 }
 
+// LocalHistogramGrid validation (tonemap.py:45-51), also for empty images
+static int check_lhe(int64_t tile_w, int64_t tile_h, int64_t bins, double strength) {
+    if (tile_w < 1 || tile_h < 1)
+        return set_error(WG_EINVAL, "tile size must be >= 1, got %lldx%lld", static_cast<long long>(tile_w),
+                         static_cast<long long>(tile_h));
+    if (bins < 2 || bins > (1 << 24))
+        return set_error(WG_EINVAL, "bins must lie in [2, 2^24], got %lld", static_cast<long long>(bins));
+    if (!(strength >= 0.0 && strength <= 1.0))
+        return set_error(WG_EINVAL, "strength must lie in [0, 1], got %.17g", strength);
+    return 0;
+}
+
+extern "C" int wg_host_local_lhe_f64(const double* lum, double* out, int64_t height, int64_t width, int64_t tile_w,
+                                     int64_t tile_h, int64_t bins, double strength, int device) {
+    WG_CHECK_ARGS(check_npix(height) || check_npix(width) || check_lhe(tile_w, tile_h, bins, strength));
+    const int64_t npix = height * width;
+    if (npix == 0) return WG_OK;
+    WG_CHECK_ARGS(check_ptrs(1, lum, out));
+    HostIn in[1] = {{lum, static_cast<size_t>(npix) * 8}};
+    HostOut o[1] = {{out, static_cast<size_t>(npix) * 8}};
+    auto scratch = [&](int64_t n) { return wg_lhe_scratch_bytes(n, height, width, tile_w, tile_h, bins); };
+    return host_pipeline(device, 1, in, 1, o, 1, 1, scratch,
+                         [&](const void** di, void** dout, void* sc, int64_t n, cudaStream_t st) {
+                             return wg_local_lhe_f64(static_cast<const double*>(di[0]), static_cast<double*>(dout[0]),
+                                                     n, height, width, tile_w, tile_h, bins, strength, sc,
+                                                     scratch(n), st);
+                         });
+}
+
+extern "C" int wg_host_tonemap_local_f64(const double* rgb, double* l_out, double* rgb_out, int64_t height,
+                                         int64_t width, double beta_r, double beta_k, int64_t tile_w, int64_t tile_h,
+                                         int64_t bins, double strength, int device) {
+    WG_CHECK_ARGS(check_npix(height) || check_npix(width) || check_params(beta_r, beta_k) ||
+                  check_lhe(tile_w, tile_h, bins, strength));
+    const int64_t npix = height * width;
+    if (npix == 0) return WG_OK;
+    WG_CHECK_ARGS(check_ptrs(1, rgb, l_out) || check_ptrs(1, rgb_out, rgb_out));
+    HostIn in[1] = {{rgb, static_cast<size_t>(npix) * 24}};
+    HostOut o[2] = {{l_out, static_cast<size_t>(npix) * 8}, {rgb_out, static_cast<size_t>(npix) * 24}};
+    // scratch = the decolor gray (l_in) followed by the lhe tables
+    const size_t gray_bytes = align256(static_cast<size_t>(npix) * 8);
+    auto lhe_bytes = [&](int64_t n) { return wg_lhe_scratch_bytes(n, height, width, tile_w, tile_h, bins); };
+    return host_pipeline(device, 1, in, 1, o, 2, 1, [&](int64_t n) { return gray_bytes + lhe_bytes(n); },
+                         [&](const void** di, void** dout, void* sc, int64_t n, cudaStream_t st) {
+                             uint8_t* base = static_cast<uint8_t*>(sc);
+                             return wg_tonemap_local_f64(static_cast<const double*>(di[0]),
+                                                         reinterpret_cast<double*>(base),
+                                                         static_cast<double*>(dout[0]), static_cast<double*>(dout[1]),
+                                                         n, height, width, beta_r, beta_k, tile_w, tile_h, bins,
+                                                         strength, base + gray_bytes, lhe_bytes(n), st);
+                         });
+}
+
+extern "C" int wg_host_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null, int64_t nimg,
+                                             int64_t height, int64_t width, double beta_r, double beta_k,
+                                             int64_t tile_w, int64_t tile_h, int64_t bins, double strength,
+                                             int device) {
+    WG_CHECK_ARGS(check_npix(nimg) || check_npix(height) || check_npix(width) || check_params(beta_r, beta_k) ||
+                  check_lhe(tile_w, tile_h, bins, strength));
+    const int64_t ppi = height * width;
+    if (nimg == 0 || ppi == 0) return WG_OK;
+    WG_CHECK_ARGS(check_ptrs(1, rgb, toned));
+    HostIn in[1] = {{rgb, static_cast<size_t>(ppi) * 3}};
+    HostOut o[2] = {{toned, static_cast<size_t>(ppi)}, {gray_or_null, static_cast<size_t>(ppi)}};
+    auto scratch = [&](int64_t n) { return wg_lhe_scratch_bytes(n, height, width, tile_w, tile_h, bins); };
+    return host_pipeline(device, nimg, in, 1, o, 2, 1, scratch,
+                         [&](const void** di, void** dout, void* sc, int64_t n, cudaStream_t st) {
+                             return wg_decolor_tone_local_u8(static_cast<const uint8_t*>(di[0]),
+                                                             static_cast<uint8_t*>(dout[0]),
+                                                             static_cast<uint8_t*>(dout[1]), n, height, width,
+                                                             beta_r, beta_k, tile_w, tile_h, bins, strength, sc,
+                                                             scratch(n), st);
+                         });
+}
+
 extern "C" int wg_host_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
                                       float beta_r, float beta_k, float midpoint, float slope,
                                       int device) {

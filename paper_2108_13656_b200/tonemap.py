@@ -1,14 +1,16 @@
-"""Global tone mapping of the gray channel and ratio-based colour reinstatement.
+"""Tone mapping of the gray channel and ratio-based colour reinstatement.
 
-Drop-in for the global half of /root/reference/pkg/src/warmgray/tonemap.py:
-``SigmoidCurve`` (tonemap.py:22-33), ``apply_sigmoid`` (:72-83),
-``reinstate_color`` (:172-192) and ``tonemap_image`` (:195-216). All image
-work runs in fp64 device kernels (the reference's own precision), and
-``tonemap_image(mode="global")`` is ONE fused device pass
-(decolor -> sigmoid -> reinstate) instead of three NumPy passes.
+Drop-in for /root/reference/pkg/src/warmgray/tonemap.py: ``SigmoidCurve``
+(tonemap.py:22-33), ``LocalHistogramGrid`` (:36-69), ``apply_sigmoid``
+(:72-83), ``apply_local_lhe`` (:103-169), ``reinstate_color`` (:172-192) and
+``tonemap_image`` (:195-216). All image work runs in fp64 device kernels (the
+reference's own precision, bit-identical results):
 
-``mode="local"`` (tile-histogram equalisation, tonemap.py:36-69,86-169) is
-the next scope row and is not available yet.
+* ``tonemap_image(mode="global")`` is ONE fused device pass
+  (decolor -> sigmoid -> reinstate) instead of three NumPy passes;
+* ``mode="local"`` runs decolor, the tile-histogram equalisation
+  (histograms -> CDF curves -> bilinear blend; csrc/wg_lhe.cu) and the
+  reinstatement back to back on the device with the gray kept resident.
 """
 
 from __future__ import annotations
@@ -87,11 +89,28 @@ def reinstate_color(rgb: PlanarImage, l_in: PlanarImage, l_out: PlanarImage) -> 
     return PlanarImage._from_kernel(out)
 
 
-def apply_local_lhe(img: PlanarImage, grid: LocalHistogramGrid, threads: int | None = None):
-    """Local histogram equalisation (tonemap.py:103-169): next scope row, SURVEY 8 f1."""
+def apply_local_lhe(img: PlanarImage, grid: LocalHistogramGrid, threads: int | None = None) -> PlanarImage:
+    """Local histogram equalisation with bilinearly blended tile curves.
+
+    Each tile's cumulative histogram, stretched over its occupied range, is a
+    tone curve; per pixel the four surrounding tile curves are blended and
+    the result mixed with the identity by ``grid.strength``. Single-bin tiles
+    (constant content) keep their values; tiles larger than the image are
+    clamped to it. ``threads`` is validated only: the GPU result does not
+    depend on it (the reference's test_thread_count_invariance).
+    """
     if img.kind != "luminance":
         raise ValueError("apply_local_lhe expects a luminance image")
-    raise NotImplementedError("local tone mapping (SURVEY.md 8 f1) is not implemented yet")
+    resolve_threads(threads)
+    data = img.data
+    h, w = data.shape
+    out = np.empty_like(data)
+    if h and w:
+        _lib.call("wg_host_local_lhe_f64", data.ctypes.data, out.ctypes.data, h, w, int(grid.tile_w),
+                  int(grid.tile_h), int(grid.bins), float(grid.strength), get_device())
+    else:
+        out = data.copy()
+    return PlanarImage._from_kernel(out)
 
 
 def tonemap_image(
@@ -118,10 +137,12 @@ def tonemap_image(
                       float(c.midpoint), float(c.slope), get_device())
         return PlanarImage._from_kernel(rgb_out), PlanarImage._from_kernel(l_out)
     if mode == "local":
-        from .core import decolor_image
-
-        l_in = decolor_image(rgb, params, threads=threads, backend=backend)
         g = grid or LocalHistogramGrid.for_image(rgb.width, rgb.height)
-        l_out = apply_local_lhe(l_in, g, threads=threads)
-        return reinstate_color(rgb, l_in, l_out), l_out
+        l_out = np.empty((rgb.height, rgb.width), dtype=np.float64)
+        rgb_out = np.empty_like(rgb.data)
+        if l_out.size:
+            _lib.call("wg_host_tonemap_local_f64", rgb.data.ctypes.data, l_out.ctypes.data,
+                      rgb_out.ctypes.data, rgb.height, rgb.width, params.beta_r, params.beta_k,
+                      int(g.tile_w), int(g.tile_h), int(g.bins), float(g.strength), get_device())
+        return PlanarImage._from_kernel(rgb_out), PlanarImage._from_kernel(l_out)
     raise ValueError(f"unknown tonemap mode {mode!r} (use 'global' or 'local')")

@@ -24,6 +24,10 @@ into this repository; only the outputs below are committed:
                       reference's decolor_image/apply_sigmoid/quantize_u8
   colorspaces.npz     bt601/hsv/lab_lightness/lab rows (compiled backend) on
                       seeded fp64 images incl. sRGB / Lab branch points
+  lhe.npz             apply_local_lhe on seeded / structured luminance over
+                      grids incl. 1x1 tiles, oversize tiles, 2..1000 bins,
+                      strength 0 and 1; tonemap_image(mode="local") on seeded
+                      rgb; quantize_u8 of the local tone map of uint8 images
   colorspaces.json    scalar known answers (luma_weighted, hsv_v, rgb_to_lab,
                       lab_lightness, delta_e76) and sha256 of the u8 cube
                       through luminance_image for y / v / lab
@@ -200,7 +204,56 @@ def main() -> None:
         outs.append(wg.quantize_u8(wg.apply_sigmoid(wg.PlanarImage(t)).data))
     np.savez_compressed(os.path.join(HERE, "hdr.npz"), rgb=hdr, out=np.stack(outs))
     colorspaces_golden(wg, get_kernels)
+    lhe_golden(wg)
     print("golden fixtures written to", HERE)
+
+
+LHE_CASES = [  # (h, w, tile_w, tile_h, bins, strength)
+    (11, 13, 5, 4, 32, 0.7), (30, 17, 6, 7, 256, 0.9), (64, 80, 10, 8, 256, 0.7), (1, 1, 4, 4, 16, 1.0),
+    (1, 50, 3, 3, 8, 0.5), (50, 1, 3, 3, 8, 0.5), (6, 6, 10000, 10000, 256, 1.0), (40, 33, 1, 1, 7, 0.3),
+    (37, 41, 9, 5, 1000, 1.0), (20, 20, 4, 4, 2, 0.7), (16, 16, 4, 4, 256, 0.0), (97, 131, 17, 13, 256, 0.7),
+]
+
+
+def lhe_golden(wg) -> None:
+    """the reference's local tone map."""
+    rng = np.random.default_rng(2109)
+    out = {"cases": np.array(LHE_CASES, dtype=np.float64)}
+    for i, (h, w, tw, th, nb, s) in enumerate(LHE_CASES):
+        d = rng.random((h, w))
+        if i == 2:
+            d = np.round(d * 255) / 255  # u8-derived values: many exact bin edges
+        out[f"in{i}"] = d
+        out[f"out{i}"] = wg.apply_local_lhe(wg.PlanarImage(d), wg.LocalHistogramGrid(tw, th, nb, s)).data
+    # structured: two-tile halves, ramp, constant (test_tonemap.py fixtures' shapes)
+    xs = np.linspace(0.0, 1.0, 4)
+    halves = np.hstack([0.3 * np.tile(xs, (8, 1)), 0.7 + 0.3 * np.tile(xs, (8, 1))])
+    ramp = np.tile(np.linspace(0.0, 1.0, 64), (32, 1))
+    const = np.full((12, 10), 0.37)
+    for name, d, grid in (("halves", halves, wg.LocalHistogramGrid(4, 8, 16, 1.0)),
+                          ("ramp", ramp, wg.LocalHistogramGrid(8, 8, strength=1.0)),
+                          ("const", const, wg.LocalHistogramGrid(4, 4, strength=1.0))):
+        out[f"{name}_in"] = d
+        out[f"{name}_grid"] = np.array([grid.tile_w, grid.tile_h, grid.bins, grid.strength])
+        out[f"{name}_out"] = wg.apply_local_lhe(wg.PlanarImage(d), grid).data
+    # tonemap_image(mode="local")
+    rgb = rng.random((24, 36, 3))
+    rgb[0, 0] = 0.0
+    r1, l1 = wg.tonemap_image(wg.PlanarImage(rgb), mode="local")
+    g2 = wg.LocalHistogramGrid(7, 5, 64, 0.9)
+    r2, l2 = wg.tonemap_image(wg.PlanarImage(rgb), mode="local", params=wg.DecolorParams(0.7, 0.9), grid=g2)
+    out.update(tm_rgb=rgb, tm_rgb_out=r1.data, tm_l_out=l1.data, tm_rgb_out2=r2.data, tm_l_out2=l2.data)
+    # uint8 batch: quantize_u8(local tone map) and quantize_u8(gray)
+    u8 = rng.integers(0, 256, (3, 48, 64, 3), dtype=np.uint8)
+    u8[1, :24] = u8[1, 0, 0]  # a flat region (identity tiles)
+    toned, gray = [], []
+    for im in u8:
+        img = wg.PlanarImage(wg.dequantize_u8(im))
+        _, lo = wg.tonemap_image(img, mode="local")
+        toned.append(wg.quantize_u8(lo.data))
+        gray.append(wg.quantize_u8(wg.decolor_image(img).data))
+    out.update(u8_rgb=u8, u8_toned=np.stack(toned), u8_gray=np.stack(gray))
+    np.savez_compressed(os.path.join(HERE, "lhe.npz"), **out)
 
 
 def colorspaces_golden(wg, get_kernels) -> None:
@@ -246,6 +299,12 @@ def colorspaces_golden(wg, get_kernels) -> None:
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["lhe"]:
+        sys.path.insert(0, build_reference())
+        import warmgray as _wg
+
+        lhe_golden(_wg)
+        sys.exit(0)
     if sys.argv[1:] == ["colorspaces"]:
         sys.path.insert(0, build_reference())
         import warmgray as _wg
