@@ -18,6 +18,13 @@
 //   4. apply   per pixel the four neighbouring tile curves at the pixel's bin,
 //              blended bilinearly and mixed with the identity by `strength`.
 //
+// uint8 kernels work on 16-pixel groups inside one row (three 128-bit loads
+// when rows are 16-byte aligned) with the packed MUFU gray estimate of the
+// decolor kernel (decolor_fast_x2, |error| <= 2.4e-7 over all byte colours:
+// scripts/margin_probe.cu); the histogram merges runs of equal cells before
+// its shared-memory atomics, and the apply pass stages the (at most three)
+// tile rows of fp32 curves and the per-column tables in shared memory.
+//
 // The fp64 drop-in evaluates every step with the reference's operations and
 // order (no contraction), so it is bit-identical to the NumPy code. The fused
 // uint8 batch path (decolor -> local equalisation -> quantize) computes the
@@ -41,8 +48,12 @@ constexpr int kBlock = 256;
 // |decolor_acc(k/255) - decolor_f64(k/255)| over all 2^24 byte colours is
 // < 2.5e-7 (tests/test_gpu_lhe.py pins it); margins below leave >= 4x headroom.
 constexpr float kGrayMargin = 1e-6f;  // bin edges (gray domain)
+constexpr float kGray255Margin = 255.0f * kGrayMargin;  // the same in the 0..255 domain
+// (bins of the uint8 route need margin_t = kGrayMargin * nb < 0.5, i.e. nb < 500000)
+constexpr int kGrp = 16;                                // pixels per thread group (48 input bytes)
 constexpr float kQuantMargin = 1e-3f;  // quantization (x = v * 255 + 0.5 domain)
 constexpr size_t kHistSmemCap = 96 * 1024;
+constexpr size_t kApplySmemCap = 200 * 1024;
 
 struct LheGeom {
     int64_t h, w, nimg;
@@ -54,7 +65,7 @@ struct LheGeom {
 struct LheBufs {
     uint32_t* hist;  // [nimg][ntile][nb]
     double* curve;   // [nimg][ntile][nb]
-    float* curvef;   // [nimg][ntile][nb]
+    float* curvef;   // [nimg][ntile][nb]: 255 * curve, NaN for identity tiles (uint8 route)
     uint8_t* ident;  // [nimg][ntile]
     int32_t* xi;     // [w] left neighbour tile column
     double* xf;      // [w] blend fraction
@@ -131,6 +142,11 @@ struct SrcF64 {
     __device__ __forceinline__ int bin(int64_t p, int nb) const { return bin_d(lum[p], nb); }
 };
 
+// the reference's fp64 gray of a byte colour; out of line: it is the rare route
+__device__ __noinline__ double exact_gray(uint32_t r, uint32_t g, uint32_t b, double br, double bk) {
+    return decolor_f64(deq_byte(r), deq_byte(g), deq_byte(b), br, bk);
+}
+
 // uint8 RGB: gray = decolor_image(dequantize_u8(rgb)) (core.py:147-169).
 struct SrcU8 {
     const uint8_t* rgb;
@@ -150,7 +166,7 @@ struct SrcU8 {
                            __fmul_rn(static_cast<float>(b), s), k);
     }
     __device__ __forceinline__ double gray_d(uint32_t r, uint32_t g, uint32_t b) const {
-        return decolor_f64(deq_byte(r), deq_byte(g), deq_byte(b), br, bk);
+        return exact_gray(r, g, b, br, bk);
     }
     // exact bin from the fp32 gray; fp64 only within kGrayMargin of an edge
     __device__ __forceinline__ int bin_of(float vf, uint32_t r, uint32_t g, uint32_t b, int nb) const {
@@ -255,7 +271,8 @@ __global__ void __launch_bounds__(kBlock) lhe_curve_kernel(LheGeom g, LheBufs s)
             v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
         }
         s.curve[cell0 + k] = v;
-        s.curvef[cell0 + k] = static_cast<float>(v);
+        // fp32 table in the 0..255 domain of the uint8 route; NaN marks an identity tile
+        s.curvef[cell0 + k] = ident ? __int_as_float(0x7fc00000) : static_cast<float>(__dmul_rn(v, 255.0));
     }
 }
 
@@ -359,10 +376,11 @@ __global__ void __launch_bounds__(kBlock) lhe_apply_u8_kernel(SrcU8 src, uint8_t
             const int i0 = s.xi[x], i1 = g.nx > 1 ? i0 + 1 : 0;
             const int64_t t00 = tbase + static_cast<int64_t>(j0) * g.nx + i0, t01 = t00 - i0 + i1;
             const int64_t t10 = tbase + static_cast<int64_t>(j1) * g.nx + i0, t11 = t10 - i0 + i1;
-            const float c00 = s.ident[t00] ? vf : s.curvef[t00 * g.nb + b];
-            const float c01 = s.ident[t01] ? vf : s.curvef[t01 * g.nb + b];
-            const float c10 = s.ident[t10] ? vf : s.curvef[t10 * g.nb + b];
-            const float c11 = s.ident[t11] ? vf : s.curvef[t11 * g.nb + b];
+            constexpr float k255 = 1.0f / 255.0f;  // curvef is in the 0..255 domain
+            const float c00 = s.ident[t00] ? vf : __fmul_rn(s.curvef[t00 * g.nb + b], k255);
+            const float c01 = s.ident[t01] ? vf : __fmul_rn(s.curvef[t01 * g.nb + b], k255);
+            const float c10 = s.ident[t10] ? vf : __fmul_rn(s.curvef[t10 * g.nb + b], k255);
+            const float c11 = s.ident[t11] ? vf : __fmul_rn(s.curvef[t11 * g.nb + b], k255);
             const float wxf = s.xff[x];
             const float top = __fmaf_rn(wxf, __fsub_rn(c01, c00), c00);
             const float bottom = __fmaf_rn(wxf, __fsub_rn(c11, c10), c10);
@@ -396,50 +414,378 @@ __global__ void __launch_bounds__(kBlock) lhe_apply_u8_kernel(SrcU8 src, uint8_t
     }
 }
 
+// ------------------------------------------------------------------ uint8 group kernels
+// One thread handles kGrp consecutive pixels of one row.
+struct U8Group {
+    uint32_t w[12];  // 48 bytes, zero-padded past the row end
+    int npx;
+
+    __device__ __forceinline__ void load(const uint8_t* rgb, int64_t p0, int n, bool vec) {
+        npx = n;
+        if (vec && n == kGrp) {
+            const uint4* q = reinterpret_cast<const uint4*>(rgb + 3 * p0);
+            const uint4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+            w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+            w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+            w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 12; ++i) w[i] = 0;
+            const uint8_t* src = rgb + 3 * p0;
+#pragma unroll
+            for (int i = 0; i < 3 * kGrp; ++i)  // static indices keep w[] in registers
+                if (i < 3 * n) w[i >> 2] |= static_cast<uint32_t>(__ldg(src + i)) << (8 * (i & 3));
+        }
+    }
+    __device__ __forceinline__ uint32_t byte(int i) const { return __byte_perm(w[i >> 2], 0u, 0x4440u | (i & 3)); }
+    // 255 * gray estimates (decolor_fast_x2 on pixel pairs)
+    __device__ __forceinline__ void gray255(const U8Consts& k, float (&g)[kGrp]) const {
+#pragma unroll
+        for (int j = 0; j < kGrp / 2; ++j) {
+            float2 ch[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int b0 = 3 * (2 * j) + c, b1 = 3 * (2 * j + 1) + c;
+                ch[c] = add2(make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3)),
+                             bc2(-kMagic));
+            }
+            const float2 f = decolor_fast_x2(ch[0], ch[1], ch[2], k);
+            g[2 * j] = f.x;
+            g[2 * j + 1] = f.y;
+        }
+    }
+};
+
+struct U8Lhe {
+    SrcU8 src;
+    U8Consts k8;
+    float nb_over_255;  // fl(nb / 255)
+    float half_m;       // 0.5 - m, m = 1e-6 nb the margin in t = v * nb
+    float t_hi;         // nb - 0.5
+
+    // bin from the 0..255-domain estimate g255: t = g255 * nb/255 with
+    // |t - v nb| <= (2.4e-7 + 6e-8 + 6e-8) nb < m. t is clamped to [0.5, nb - 0.5]
+    // (0 and nb are not bin edges), floor(t) taken as the low bits of
+    // fl_rd(t + 2^23) (no F2I); `sure` is false within m of an inner edge.
+    __device__ __forceinline__ int bin_fast(float g255, bool& sure) const {
+        const float t = fminf(fmaxf(__fmul_rn(g255, nb_over_255), 0.5f), t_hi);
+        const float tf = __fadd_rd(t, 8388608.0f);
+        sure = fabsf(__fsub_rn(__fsub_rn(t, __fsub_rn(tf, 8388608.0f)), 0.5f)) < half_m;
+        return static_cast<int>(__float_as_uint(tf) & 0x7fffffu);
+    }
+};
+
+__global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
+                                                              int rows_per_chunk, bool vec) {
+    extern __shared__ uint32_t sh[];  // [nx * nb] + one dummy cell
+    const int64_t img = blockIdx.z;
+    const int ty = blockIdx.y;
+    const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
+    const int64_t y1 = imin64(imin64(y0 + rows_per_chunk, static_cast<int64_t>(ty + 1) * g.th), g.h);
+    if (y0 >= y1) return;
+    const int cells = g.nx * g.nb;
+    for (int i = threadIdx.x; i <= cells; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
+    const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
+    const int64_t row0 = (img * g.h + y0) * g.w;
+    auto group_at = [&](uint32_t gi, int& x0, int& n, int64_t& p0) {
+        const uint32_t gy = gi / gpr;
+        x0 = static_cast<int>(gi - gy * gpr) * kGrp;
+        n = static_cast<int>(imin64(kGrp, g.w - x0));
+        p0 = row0 + static_cast<int64_t>(gy) * g.w + x0;
+    };
+    uint32_t gi = threadIdx.x;
+    U8Group nxt;
+    int x0n = 0, nn = 0;
+    int64_t p0n = 0;
+    if (gi < ngroups) {
+        group_at(gi, x0n, nn, p0n);
+        nxt.load(L.src.rgb, p0n, nn, vec);
+    }
+    for (; gi < ngroups; gi += blockDim.x) {
+        const U8Group grp = nxt;
+        const int x0 = x0n, n = nn;
+        const int64_t p0 = p0n;
+        if (gi + blockDim.x < ngroups) {  // register prefetch of this thread's next group
+            group_at(gi + blockDim.x, x0n, nn, p0n);
+            nxt.load(L.src.rgb, p0n, nn, vec);
+        }
+        uint32_t slow = 0;
+        int tx = x0 / g.tw, next = (tx + 1) * g.tw;
+        if (n == kGrp) {
+            float g255[kGrp];
+            grp.gray255(L.k8, g255);
+            // runs of equal cells are merged before the shared-memory atomic; the
+            // first flush goes to the dummy cell
+            int run_cell = cells;
+            uint32_t run = 0;
+#pragma unroll
+            for (int p = 0; p < kGrp; ++p) {
+                const bool step = x0 + p >= next;
+                tx += step;
+                next += step ? g.tw : 0;
+                bool sure;
+                const int cell = tx * g.nb + L.bin_fast(g255[p], sure);
+                slow |= static_cast<uint32_t>(!sure) << p;
+                const bool same = cell == run_cell;
+                if (sure && !same) atomicAdd(&sh[run_cell], run);
+                run = sure ? (same ? run + 1 : 1u) : run;
+                run_cell = sure ? cell : run_cell;
+            }
+            atomicAdd(&sh[run_cell], run);
+        } else {  // row tail of a width that is not a multiple of 16
+#pragma unroll 1
+            for (int p = 0; p < n; ++p) {
+                if (x0 + p >= next) {
+                    ++tx;
+                    next += g.tw;
+                }
+                uint32_t cr, cg, cb;  // (a dynamic index into grp.w would spill it to local memory)
+                L.src.load(p0 + p, cr, cg, cb);
+                const float g255 = decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
+                                                   static_cast<float>(cb), L.k8);
+                bool sure;
+                const int b = L.bin_fast(g255, sure);
+                if (sure) atomicAdd(&sh[tx * g.nb + b], 1u);
+                else slow |= 1u << p;
+            }
+        }
+        while (slow) {  // rare: the reference's fp64 bin for pixels next to an edge
+            const int p = __ffs(slow) - 1;
+            slow &= slow - 1;
+            uint32_t cr, cg, cb;
+            L.src.load(p0 + p, cr, cg, cb);
+            atomicAdd(&sh[((x0 + p) / g.tw) * g.nb + bin_d(L.src.gray_d(cr, cg, cb), g.nb)], 1u);
+        }
+    }
+    __syncthreads();
+    uint32_t* gh = hist + (img * g.ntile + static_cast<int64_t>(ty) * g.nx) * g.nb;
+    for (int i = threadIdx.x; i < cells; i += blockDim.x)
+        if (sh[i]) atomicAdd(&gh[i], sh[i]);
+}
+
+// shared-memory layout of the apply kernel: curves of <= 3 tile rows, then per
+// column the blend fraction (fp32) and the left tile's curve offset i0 * nb
+// (u32), padded to a multiple of 16 columns so a group reads its 16 entries as
+// 128-bit vectors
+struct ApplySmem {
+    static __host__ __device__ int64_t wpad(int64_t w) { return (w + kGrp - 1) / kGrp * kGrp; }
+    static __host__ __device__ size_t bytes(int nx, int nb, int64_t w) {
+        return static_cast<size_t>(3) * nx * nb * 4 + static_cast<size_t>(wpad(w)) * 8 + 16;
+    }
+};
+
+template <bool kGray>
+__global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8_t* __restrict__ toned,
+                                                               uint8_t* __restrict__ gray, LheGeom g, LheBufs s,
+                                                               int rows_per_chunk, bool vec) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int64_t img = blockIdx.z;
+    const int ty = blockIdx.y;
+    const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
+    const int64_t y1 = imin64(imin64(y0 + rows_per_chunk, static_cast<int64_t>(ty + 1) * g.th), g.h);
+    if (y0 >= y1) return;
+    // rows of this tile row blend tile rows {ty-1, ty, ty+1} at most
+    const int jbase = max(ty - 1, 0), nload = min(ty + 1, g.ny - 1) - jbase + 1;
+    const int64_t wp = ApplySmem::wpad(g.w);
+    float* cur = reinterpret_cast<float*>(smem);              // [3][nx][nb]: 255 * curve, NaN = identity
+    float* sxf = cur + static_cast<size_t>(3) * g.nx * g.nb;  // [wp]
+    uint32_t* sxo = reinterpret_cast<uint32_t*>(sxf + wp);    // [wp] i0 * nb
+    const int64_t tile0 = img * g.ntile + static_cast<int64_t>(jbase) * g.nx;
+    const int ncur = nload * g.nx * g.nb;
+    for (int i = threadIdx.x; i < ncur; i += blockDim.x) cur[i] = s.curvef[tile0 * g.nb + i];
+    for (int64_t x = threadIdx.x; x < wp; x += blockDim.x) {
+        const int64_t xc = imin64(x, g.w - 1);
+        sxf[x] = s.xff[xc];
+        sxo[x] = static_cast<uint32_t>(s.xi[xc] * g.nb);
+    }
+    __syncthreads();
+    const float sf = static_cast<float>(g.strength);
+    const int dnb = g.nx > 1 ? g.nb : 0;  // i1 - i0 in curve-table units
+    const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
+    const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
+    for (uint32_t gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
+        const uint32_t gy = gi / gpr;
+        const int64_t y = y0 + gy;
+        const int x0 = static_cast<int>(gi - gy * gpr) * kGrp;
+        const int n = static_cast<int>(imin64(kGrp, g.w - x0));
+        const int64_t p0 = (img * g.h + y) * g.w + x0;
+        const int j0 = s.yi[y], j1 = g.ny > 1 ? j0 + 1 : 0;
+        const int r0nb = (j0 - jbase) * g.nx * g.nb, drow = (j1 - j0) * g.nx * g.nb;
+        const float wy = s.yff[y];
+        // the group's 16 blend fractions and curve offsets as 128-bit shared loads
+        float wxs[kGrp];
+        uint32_t xos[kGrp];
+#pragma unroll
+        for (int q = 0; q < kGrp / 4; ++q) {
+            const float4 f = reinterpret_cast<const float4*>(sxf + x0)[q];
+            const uint4 o = reinterpret_cast<const uint4*>(sxo + x0)[q];
+            wxs[4 * q] = f.x;
+            wxs[4 * q + 1] = f.y;
+            wxs[4 * q + 2] = f.z;
+            wxs[4 * q + 3] = f.w;
+            xos[4 * q] = o.x;
+            xos[4 * q + 1] = o.y;
+            xos[4 * q + 2] = o.z;
+            xos[4 * q + 3] = o.w;
+        }
+        U8Group grp;
+        grp.load(L.src.rgb, p0, n, vec);
+        float g255[kGrp];
+        grp.gray255(L.k8, g255);
+        uint32_t ot[4] = {0u, 0u, 0u, 0u}, og[4] = {0u, 0u, 0u, 0u};
+        uint32_t slow = 0;
+#pragma unroll
+        for (int p = 0; p < kGrp; ++p) {
+            const float v = g255[p];  // everything below is in the 0..255 domain
+            bool sure;
+            const int b = L.bin_fast(v, sure);
+            const int a00 = r0nb + static_cast<int>(xos[p]) + b, a10 = a00 + drow;
+            float c00 = cur[a00], c01 = cur[a00 + dnb], c10 = cur[a10], c11 = cur[a10 + dnb];
+            c00 = c00 != c00 ? v : c00;  // NaN: identity tile (the pixel's own value)
+            c01 = c01 != c01 ? v : c01;
+            c10 = c10 != c10 ? v : c10;
+            c11 = c11 != c11 ? v : c11;
+            const float wx = wxs[p];
+            const float top = __fmaf_rn(wx, __fsub_rn(c01, c00), c00);
+            const float bottom = __fmaf_rn(wx, __fsub_rn(c11, c10), c10);
+            const float eq = __fmaf_rn(wy, __fsub_rn(bottom, top), top);
+            // res = v + s (eq - v) is a convex combination of values in [0, 255]: no
+            // clamp; x = res + 0.5, floor(x) as the low byte of fl_rd(x + 2^23),
+            // x - floor(x) must clear the margin (x = 0.5 and 255.5 give exactly 0.5)
+            const float xq = __fadd_rn(__fmaf_rn(sf, __fsub_rn(eq, v), v), 0.5f);
+            const float tq = __fadd_rd(xq, 8388608.0f);
+            sure = sure && fabsf(__fsub_rn(__fsub_rn(xq, __fsub_rn(tq, 8388608.0f)), 0.5f)) < 0.5f - kQuantMargin;
+            ot[p >> 2] |= (__float_as_uint(tq) & 255u) << (8 * (p & 3));
+            if constexpr (kGray) {
+                const float xg = __fadd_rn(v, 0.5f);
+                const float tg = __fadd_rd(xg, 8388608.0f);
+                sure = sure && fabsf(__fsub_rn(__fsub_rn(xg, __fsub_rn(tg, 8388608.0f)), 0.5f)) < 0.5f - kGray255Margin;
+                og[p >> 2] |= (__float_as_uint(tg) & 255u) << (8 * (p & 3));
+            }
+            slow |= static_cast<uint32_t>(!sure && p < n) << p;
+        }
+        while (slow) {  // rare: redo the flagged pixels through the reference's fp64 chain
+            const int p = __ffs(slow) - 1;
+            slow &= slow - 1;
+            const int64_t pp = p0 + p;
+            uint32_t cr, cg, cb;
+            L.src.load(pp, cr, cg, cb);
+            const double vd = L.src.gray_d(cr, cg, cb);
+            const int b = bin_d(vd, g.nb);
+            const int x = x0 + p;
+            const int i0 = s.xi[x], i1 = g.nx > 1 ? i0 + 1 : 0;
+            const int64_t t00 = img * g.ntile + static_cast<int64_t>(j0) * g.nx + i0, t01 = t00 - i0 + i1;
+            const int64_t t10 = img * g.ntile + static_cast<int64_t>(j1) * g.nx + i0, t11 = t10 - i0 + i1;
+            const double c00 = s.ident[t00] ? vd : s.curve[t00 * g.nb + b];
+            const double c01 = s.ident[t01] ? vd : s.curve[t01 * g.nb + b];
+            const double c10 = s.ident[t10] ? vd : s.curve[t10 * g.nb + b];
+            const double c11 = s.ident[t11] ? vd : s.curve[t11 * g.nb + b];
+            const uint32_t qt = quantize_d(blend_d(vd, c00, c01, c10, c11, s.xf[x], s.yf[y], g.strength));
+            const uint32_t qg = quantize_d(vd), sh = 8 * (p & 3), m = ~(255u << sh);
+            const int k = p >> 2;
+            // o[k] with a dynamic k would go to local memory: select instead
+            ot[0] = k == 0 ? (ot[0] & m) | (qt << sh) : ot[0];
+            ot[1] = k == 1 ? (ot[1] & m) | (qt << sh) : ot[1];
+            ot[2] = k == 2 ? (ot[2] & m) | (qt << sh) : ot[2];
+            ot[3] = k == 3 ? (ot[3] & m) | (qt << sh) : ot[3];
+            if constexpr (kGray) {
+                og[0] = k == 0 ? (og[0] & m) | (qg << sh) : og[0];
+                og[1] = k == 1 ? (og[1] & m) | (qg << sh) : og[1];
+                og[2] = k == 2 ? (og[2] & m) | (qg << sh) : og[2];
+                og[3] = k == 3 ? (og[3] & m) | (qg << sh) : og[3];
+            }
+        }
+        if (vec && n == kGrp) {
+            st_global_cs_v4(toned + p0, make_uint4(ot[0], ot[1], ot[2], ot[3]));
+            if constexpr (kGray) st_global_cs_v4(gray + p0, make_uint4(og[0], og[1], og[2], og[3]));
+        } else {
+#pragma unroll
+            for (int p = 0; p < kGrp; ++p) {
+                if (p < n) {
+                    toned[p0 + p] = static_cast<uint8_t>(ot[p >> 2] >> (8 * (p & 3)));
+                    if constexpr (kGray) gray[p0 + p] = static_cast<uint8_t>(og[p >> 2] >> (8 * (p & 3)));
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ driver
-template <class Src>
-int run_lhe(const Src& src, const LheGeom& g, const LheBufs& b, cudaStream_t st) {
+struct Chunking {
+    int rows_per_chunk, chunks;
+};
+// enough (image, tile row, row chunk) blocks to cover the SMs a few times
+Chunking chunking(const LheGeom& g) {
     int device = 0;
     cudaGetDevice(&device);
-    const int sms = sm_count(device);
+    const int64_t bands = std::max<int64_t>(1, std::min<int64_t>(g.nimg, 65535) * g.ny);
+    // ~16 blocks per SM: several waves, so the last one is a small tail
+    const int64_t want = std::max<int64_t>(1, (16LL * sm_count(device) + bands - 1) / bands);
+    Chunking c;
+    c.rows_per_chunk = static_cast<int>(std::max<int64_t>(1, (g.th + want - 1) / want));
+    c.chunks = (g.th + c.rows_per_chunk - 1) / c.rows_per_chunk;
+    return c;
+}
+
+// hist memset + axis tables
+int lhe_begin(const LheGeom& g, const LheBufs& b, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(b.hist, 0, static_cast<size_t>(g.nimg) * g.ntile * g.nb * 4, st);
     if (e != cudaSuccess) return set_error(static_cast<int>(e), "lhe: hist memset: %s", cudaGetErrorString(e));
-    // axis tables
     const int64_t na = g.w + g.h;
     lhe_axis_kernel<<<static_cast<unsigned>((na + kBlock - 1) / kBlock), kBlock, 0, st>>>(g, b);
-    // histograms: enough (image, tile row, chunk) blocks to cover the SMs a few times
-    const int64_t bands = g.nimg * g.ny;
-    const int64_t want_chunks = std::max<int64_t>(1, (4LL * sms + bands - 1) / bands);
-    const int rows_per_chunk = static_cast<int>(std::max<int64_t>(1, (g.th + want_chunks - 1) / want_chunks));
-    const int chunks = (g.th + rows_per_chunk - 1) / rows_per_chunk;
-    const size_t smem = static_cast<size_t>(g.nx) * g.nb * 4;
+    return WG_OK;
+}
+
+// images are processed in slices of at most 65535 (grid z)
+template <class F>
+void per_image_slice(const LheGeom& g, F f) {
     for (int64_t i0 = 0; i0 < g.nimg; i0 += 65535) {
         LheGeom gi = g;
         gi.nimg = std::min<int64_t>(65535, g.nimg - i0);
+        f(i0, gi);
+    }
+}
+
+template <class Src>
+void lhe_hist(const Src& src, const LheGeom& g, const LheBufs& b, cudaStream_t st) {
+    const Chunking c = chunking(g);
+    const size_t smem = static_cast<size_t>(g.nx) * g.nb * 4;
+    per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
         Src si = src;
         si.advance(i0 * g.h * g.w);
         uint32_t* hist = b.hist + i0 * g.ntile * g.nb;
-        const dim3 grid(chunks, g.ny, static_cast<unsigned>(gi.nimg));
+        const dim3 grid(c.chunks, g.ny, static_cast<unsigned>(gi.nimg));
         if (smem <= kHistSmemCap) {
             if (smem > 48 * 1024)
                 cudaFuncSetAttribute(lhe_hist_kernel<Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem));
-            lhe_hist_kernel<Src, true><<<grid, kBlock, smem, st>>>(si, gi, hist, rows_per_chunk);
+            lhe_hist_kernel<Src, true><<<grid, kBlock, smem, st>>>(si, gi, hist, c.rows_per_chunk);
         } else {
-            lhe_hist_kernel<Src, false><<<grid, kBlock, 0, st>>>(si, gi, hist, rows_per_chunk);
+            lhe_hist_kernel<Src, false><<<grid, kBlock, 0, st>>>(si, gi, hist, c.rows_per_chunk);
         }
-    }
-    for (int64_t i0 = 0; i0 < g.nimg; i0 += 65535) {
-        LheGeom gi = g;
-        gi.nimg = std::min<int64_t>(65535, g.nimg - i0);
+    });
+}
+
+void lhe_curves(const LheGeom& g, const LheBufs& b, cudaStream_t st) {
+    per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
         LheBufs bi = b;
         bi.hist += i0 * g.ntile * g.nb;
         bi.curve += i0 * g.ntile * g.nb;
         bi.curvef += i0 * g.ntile * g.nb;
         bi.ident += i0 * g.ntile;
-        lhe_curve_kernel<<<dim3(static_cast<unsigned>(g.ntile), static_cast<unsigned>(gi.nimg)), kBlock, 0, st>>>(gi,
-                                                                                                              bi);
-    }
+        lhe_curve_kernel<<<dim3(static_cast<unsigned>(g.ntile), static_cast<unsigned>(gi.nimg)), kBlock, 0, st>>>(
+            gi, bi);
+    });
+}
+
+template <class Src>
+int run_lhe(const Src& src, const LheGeom& g, const LheBufs& b, cudaStream_t st) {
+    int rc = lhe_begin(g, b, st);
+    if (rc != WG_OK) return rc;
+    lhe_hist(src, g, b, st);
+    lhe_curves(g, b, st);
     return check_launch("local lhe (hist/curves)");
 }
 
@@ -530,8 +876,51 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
                     beta_k,
                     static_cast<float>(bins),
                     1.0f / static_cast<float>(bins)};
-    rc = run_lhe(src, g, b, st);
+    const float m = static_cast<float>(kGrayMargin * static_cast<double>(bins));
+    const U8Lhe L{src, make_u8_consts(static_cast<float>(beta_r), static_cast<float>(beta_k)),
+                  static_cast<float>(bins) / 255.0f, 0.5f - m, static_cast<float>(bins) - 0.5f};
+    // 16-pixel groups load/store 16-byte vectors when every row starts aligned
+    const bool vec = width % 16 == 0 && (reinterpret_cast<uintptr_t>(rgb) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(toned) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(gray_or_null) & 15) == 0;
+    rc = lhe_begin(g, b, st);
     if (rc != WG_OK) return rc;
-    lhe_apply_u8_kernel<<<apply_grid(g), kBlock, 0, st>>>(src, toned, gray_or_null, g, b);
-    return check_launch("local lhe (apply u8)");
+    const Chunking c = chunking(g);
+    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4;  // + the dummy cell
+    const size_t asmem = ApplySmem::bytes(g.nx, g.nb, g.w);
+    // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact)
+    const bool group_ok = bins <= 65536;
+    if (group_ok && hsmem <= kHistSmemCap) {
+        if (hsmem > 48 * 1024)
+            cudaFuncSetAttribute(lhe_hist_u8g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(hsmem));
+        per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
+            U8Lhe Li = L;
+            Li.src.advance(i0 * g.h * g.w);
+            lhe_hist_u8g_kernel<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, hsmem, st>>>(
+                Li, gi, b.hist + i0 * g.ntile * g.nb, c.rows_per_chunk, vec);
+        });
+    } else {
+        lhe_hist(src, g, b, st);
+    }
+    lhe_curves(g, b, st);
+    if (group_ok && asmem <= kApplySmemCap) {
+        auto kern = gray_or_null ? lhe_apply_u8g_kernel<true> : lhe_apply_u8g_kernel<false>;
+        if (asmem > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(asmem));
+        per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
+            U8Lhe Li = L;
+            Li.src.advance(i0 * g.h * g.w);
+            LheBufs bi = b;  // the kernel indexes tiles per image slice
+            bi.curve += i0 * g.ntile * g.nb;
+            bi.curvef += i0 * g.ntile * g.nb;
+            bi.ident += i0 * g.ntile;
+            const int64_t off = i0 * g.h * g.w;
+            kern<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, asmem, st>>>(
+                Li, toned + off, gray_or_null ? gray_or_null + off : nullptr, gi, bi, c.rows_per_chunk, vec);
+        });
+    } else {
+        lhe_apply_u8_kernel<<<apply_grid(g), kBlock, 0, st>>>(src, toned, gray_or_null, g, b);
+    }
+    return check_launch("local lhe (u8)");
 }

@@ -23,10 +23,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mpix", type=int, default=512)
     ap.add_argument("--iters", type=int, default=50)
-    ap.add_argument("--methods", default="ours,y,v,lab")
+    ap.add_argument("--methods", default="ours,y,v,lab,local")
     args = ap.parse_args()
-    n = args.mpix << 20
-    rgb = torch.randint(0, 256, (n, 3), dtype=torch.uint8, device="cuda")
+    # 4K frames (C3 shape) so the tiled local tone map sees real images
+    nimg = max(1, (args.mpix << 20) // (2160 * 3840))
+    n = nimg * 2160 * 3840
+    rgb4 = torch.randint(0, 256, (nimg, 2160, 3840, 3), dtype=torch.uint8, device="cuda")
+    rgb = rgb4.view(n, 3)
+    scratch = torch.empty(int(wg._lib.load().wg_lhe_scratch_bytes(nimg, 2160, 3840, 480, 270, 256)),
+                          dtype=torch.uint8, device="cuda")
     out = torch.empty(n, dtype=torch.uint8, device="cuda")
     peaks = json.load(open("MEASURED_PEAKS.json")) if os.path.exists("MEASURED_PEAKS.json") else {}
     hbm = peaks.get("hbm_gbs", 6545.3)
@@ -35,6 +40,7 @@ def main():
         "y": lambda: wg.luma(rgb, "y"),
         "v": lambda: wg.luma(rgb, "v"),
         "lab": lambda: wg.luma(rgb, "lab"),
+        "local": lambda: wg.decolor_tone_local(rgb4, scratch=scratch),
     }
     for name in args.methods.split(","):
         fn = fns[name]
