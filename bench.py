@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--images", type=int, default=None, help="images per GPU (default: workload's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-methods", action="store_true",
+                    help="skip the per-method side table (paper Table 1 on the GPU + local tone map)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
 
@@ -290,6 +292,11 @@ def main():
                 "kernel": "stream_kernel<OpDecolorU8>" if wl.dtype == "uint8" and wl.output == "gray_u8"
                 else ("stream_kernel<OpDecolorF32>" if wl.output == "gray_f32" else "hdr_pass1+hdr_pass2")}
 
+    # ---- side table (not the metric): the paper's Table 1 comparison on this batch
+    methods = None
+    if not args.no_methods and wl.dtype == "uint8" and wl.output == "gray_u8":
+        methods = run_methods(wg, torch, rgb, out, n_img, wl, stream)
+
     # ---- end to end through the public host-array API (pinned host buffers)
     e2e = None
     if not args.no_e2e:
@@ -316,9 +323,50 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": steps * launches_per_step, "clocks": clk.summary(),
         }
+        if methods:
+            line["methods"] = methods
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_methods(wg, torch, rgb, out, n_img, wl, stream, iters: int = 5):
+    """Device-resident Gpix/s of each colour-to-gray method on the bench batch.
+
+    The paper's Table 1 compares its method's per-pixel time with the CIE Lab
+    lightness baseline; BT.601 ("y") and HSV value ("v") are the reference's
+    other extractors (colorspaces.py:87-112), all uint8 -> uint8 and
+    bit-identical to quantize_u8 of the reference. "local" is the fused
+    decolor + local tone map (tonemap_image(mode="local")).
+    """
+    grid = wg.LocalHistogramGrid.for_image(wl.width, wl.height)
+    img4 = rgb.view(n_img, wl.height, wl.width, 3)
+    scratch = torch.empty(int(wg._lib.load().wg_lhe_scratch_bytes(n_img, wl.height, wl.width, grid.tile_w,
+                                                                  grid.tile_h, grid.bins)),
+                          dtype=torch.uint8, device=rgb.device)
+    fns = {
+        "ours": lambda: wg.decolor(rgb, out=out),
+        "y_bt601": lambda: wg.luma(rgb, "y"),
+        "v_hsv": lambda: wg.luma(rgb, "v"),
+        "lab_lightness": lambda: wg.luma(rgb, "lab"),
+        "local_tone": lambda: wg.decolor_tone_local(img4, grid=grid, scratch=scratch),
+    }
+    npx = n_img * wl.pix_per_image
+    res = {}
+    for name, fn in fns.items():
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        res[name] = {"gpix_s": round(npx / ms / 1e6, 1), "ps_per_px": round(ms * 1e9 / npx, 3)}
+    res["note"] = (f"{iters} device-resident passes each over this batch, uint8 in/out, bit-identical to the "
+                   "reference; ours/lab_lightness is the paper's Table 1 ratio")
+    return res
 
 
 def run_e2e(wg, torch, wl, rgb, n_img, steps, dev, world):
