@@ -53,6 +53,8 @@ extern "C" {
 #define WG_EALIGN (-2)      /* reserved: misaligned buffer where alignment is mandatory */
 #define WG_ESCRATCH (-3)    /* scratch buffer too small */
 #define WG_ENODEV (-4)      /* no CUDA device / bad ordinal */
+#define WG_ECODEC (-5)      /* unsupported or malformed image file (reference: CodecError) */
+#define WG_EIO (-6)         /* file could not be opened / written (reference: OSError) */
 
 /* ---- library / device info ------------------------------------------------ */
 WG_API int wg_version(void);                              /* 100 * major + minor */
@@ -195,6 +197,19 @@ WG_API int wg_host_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uin
                                          int64_t tile_h, int64_t bins, double strength, int device);
 WG_API int wg_host_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
                            float beta_r, float beta_k, float midpoint, float slope, int device);
+
+/* ---- uint8 file ingest / egress (codec.py:37-82, 135-140) -----
+ * Binary PGM (P5, 1 channel) / PPM (P6, 3 channels), maxval 255, with the
+ * reference's header grammar and errors. Host-only; files are read straight
+ * into / written from the caller's batch buffer (pinned for the device path),
+ * one host thread per file up to `threads`. The batch is n images of
+ * height x width x channels uint8. */
+WG_API int wg_pnm_probe(const char* path, int64_t* width, int64_t* height, int32_t* channels,
+                        int64_t* data_offset);
+WG_API int wg_pnm_read_batch(const char* const* paths, int64_t n, uint8_t* dst, int64_t width, int64_t height,
+                             int32_t channels, int32_t threads);
+WG_API int wg_pnm_write_batch(const char* const* paths, int64_t n, const uint8_t* src, int64_t width,
+                              int64_t height, int32_t channels, int32_t threads);
 
 /* ---- synthetic workload generators (bench / test inputs, on device) ------- */
 

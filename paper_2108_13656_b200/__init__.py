@@ -36,7 +36,18 @@ from .batch import (
     luma_host,
     sigmoid,
 )
-from .codec import dequantize_u8, quantize_u8
+from .codec import (
+    CodecError,
+    decolor_files,
+    dequantize_u8,
+    load_image,
+    load_u8,
+    quantize_u8,
+    read_pnm_batch,
+    save_image,
+    save_u8,
+    write_pnm_batch,
+)
 from .perf import BenchResult, format_table, run_benchmark
 from .colorspaces import (
     METHOD_NAMES,
@@ -82,6 +93,14 @@ __all__ = [
     "set_device",
     "quantize_u8",
     "dequantize_u8",
+    "CodecError",
+    "load_image",
+    "save_image",
+    "load_u8",
+    "save_u8",
+    "read_pnm_batch",
+    "write_pnm_batch",
+    "decolor_files",
     "BenchResult",
     "format_table",
     "run_benchmark",

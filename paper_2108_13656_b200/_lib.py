@@ -20,11 +20,15 @@ PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "_build", "libwarmgray_b200.so")
 
 
-WG_EINVAL, WG_EALIGN, WG_ESCRATCH, ENODEV = -1, -2, -3, -4
+WG_EINVAL, WG_EALIGN, WG_ESCRATCH, ENODEV, WG_ECODEC, WG_EIO = -1, -2, -3, -4, -5, -6
 
 
 class CudaError(RuntimeError):
     """A CUDA runtime failure reported by the B200 kernels."""
+
+
+class CodecError(Exception):
+    """Unsupported or malformed image file (the reference's codec.CodecError)."""
 
 
 class ExtensionMissing(ImportError):
@@ -83,6 +87,12 @@ SIGNATURES = {
     "wg_host_quantize_u8_f64": (_i, [_vp, _vp, _i64, _i]),
     "wg_host_dequantize_u8_f64": (_i, [_vp, _vp, _i64, _i]),
     "wg_host_hdr_tonemap_u8": (_i, [_vp, _vp, _i64, _i64, _f, _f, _f, _f, _i]),
+    "wg_pnm_probe": (_i, [ctypes.c_char_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                          ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_i64)]),
+    "wg_pnm_read_batch": (_i, [ctypes.POINTER(ctypes.c_char_p), _i64, _vp, _i64, _i64, ctypes.c_int32,
+                               ctypes.c_int32]),
+    "wg_pnm_write_batch": (_i, [ctypes.POINTER(ctypes.c_char_p), _i64, _vp, _i64, _i64, ctypes.c_int32,
+                                ctypes.c_int32]),
     "wg_synth_uniform_u8": (_i, [_vp, _i64, _i64, _u32, _i64, _vp]),
     "wg_synth_voronoi_u8": (_i, [_vp, _i64, ctypes.c_int32, ctypes.c_int32, _vp, _vp,
                                  ctypes.c_int32, _u32, _i64, _vp]),
@@ -132,6 +142,10 @@ def check(status: int, what: str = "") -> None:
     if status == 0:
         return
     msg = last_error() or f"status {status}"
+    if status == WG_ECODEC:  # file errors carry the reference's message as is
+        raise CodecError(msg)
+    if status == WG_EIO:
+        raise OSError(msg)
     if what:
         msg = f"{what}: {msg}"
     if status == ENODEV:

@@ -172,7 +172,6 @@ __device__ __forceinline__ float* lab_prodf_smem() {
 template <int METHOD>
 struct OpLumaU8 {
     static constexpr bool kLdg = true;
-    static constexpr int kInBpp = 3;
     static constexpr int kPx = 16;
     const uint8_t* in;
     uint8_t* out;

@@ -437,7 +437,6 @@ struct U8Group {
                 if (i < 3 * n) w[i >> 2] |= static_cast<uint32_t>(__ldg(src + i)) << (8 * (i & 3));
         }
     }
-    __device__ __forceinline__ uint32_t byte(int i) const { return __byte_perm(w[i >> 2], 0u, 0x4440u | (i & 3)); }
     // 255 * gray estimates (decolor_fast_x2 on pixel pairs)
     __device__ __forceinline__ void gray255(const U8Consts& k, float (&g)[kGrp]) const {
 #pragma unroll

@@ -28,6 +28,10 @@ into this repository; only the outputs below are committed:
                       grids incl. 1x1 tiles, oversize tiles, 2..1000 bins,
                       strength 0 and 1; tonemap_image(mode="local") on seeded
                       rgb; quantize_u8 of the local tone map of uint8 images
+  codec/              PPM/PGM/PNG files written by the reference's save_image
+                      (plus hand-made headers and malformed files) and
+                      codec.json: what the reference's load_image returns for
+                      each (uint8 samples) or which exception it raises
   colorspaces.json    scalar known answers (luma_weighted, hsv_v, rgb_to_lab,
                       lab_lightness, delta_e76) and sha256 of the u8 cube
                       through luminance_image for y / v / lab
@@ -205,7 +209,56 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "hdr.npz"), rgb=hdr, out=np.stack(outs))
     colorspaces_golden(wg, get_kernels)
     lhe_golden(wg)
+    codec_golden(wg)
     print("golden fixtures written to", HERE)
+
+
+def codec_golden(wg) -> None:
+    """the reference's file codec on files it writes and on malformed ones."""
+    from PIL import Image
+    from warmgray.codec import CodecError
+
+    d = os.path.join(HERE, "codec")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(2110)
+    rgb = wg.PlanarImage(rng.integers(0, 256, (6, 9, 3)).astype(np.float64) / 255.0)
+    gray = wg.PlanarImage(rng.integers(0, 256, (4, 7)).astype(np.float64) / 255.0)
+    wg.save_image(os.path.join(d, "rgb.ppm"), rgb)
+    wg.save_image(os.path.join(d, "gray.pgm"), gray)
+    wg.save_image(os.path.join(d, "rgb.png"), rgb)
+    wg.save_image(os.path.join(d, "gray.png"), gray)
+    wg.save_image(os.path.join(d, "white.ppm"), wg.PlanarImage(np.ones((1, 1, 3))))
+    u8 = rng.integers(0, 256, (5, 4, 4), dtype=np.uint8)
+    Image.fromarray(u8, mode="RGBA").save(os.path.join(d, "rgba.png"))
+    Image.fromarray(u8[..., :2].copy(), mode="LA").save(os.path.join(d, "la.png"))
+    Image.fromarray(u8[..., 0].copy(), mode="L").convert("P").save(os.path.join(d, "pal.png"))
+    raw = {
+        "comments.ppm": b"P6\n# a comment\n2 1\n# another\n255\n" + bytes([255, 0, 0, 0, 255, 0]),
+        "trailing.pgm": b"P5 3 1 255 " + bytes([1, 2, 3]) + b"extra",
+        "ascii.ppm": b"P3\n1 1\n255\n255 0 0\n",
+        "deep.ppm": b"P6\n1 1\n65535\n" + bytes(6),
+        "short.ppm": b"P6\n2 2\n255\n\xff",
+        "badtoken.pgm": b"P5\n2 x\n255\n" + bytes(2),
+        "zero.pgm": b"P5\n0 1\n255\n",
+        "header.pgm": b"P5\n2",
+        "lone.pgm": b"P",
+        "text.png": b"hello world",
+    }
+    for name, data in raw.items():
+        with open(os.path.join(d, name), "wb") as f:
+            f.write(data)
+    expect = {}
+    for name in sorted(os.listdir(d)):
+        if name.endswith(".json"):
+            continue
+        try:
+            img = wg.load_image(os.path.join(d, name))
+            expect[name] = {"kind": img.kind, "shape": list(img.data.shape),
+                            "u8": wg.quantize_u8(img.data).ravel().tolist()}
+        except CodecError as e:
+            expect[name] = {"error": "CodecError", "message": str(e).replace(d + os.sep, "")}
+    with open(os.path.join(d, "codec.json"), "w") as f:
+        json.dump(expect, f, indent=1)
 
 
 LHE_CASES = [  # (h, w, tile_w, tile_h, bins, strength)
@@ -299,6 +352,12 @@ def colorspaces_golden(wg, get_kernels) -> None:
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["codec"]:
+        sys.path.insert(0, build_reference())
+        import warmgray as _wg
+
+        codec_golden(_wg)
+        sys.exit(0)
     if sys.argv[1:] == ["lhe"]:
         sys.path.insert(0, build_reference())
         import warmgray as _wg
