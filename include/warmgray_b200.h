@@ -198,6 +198,25 @@ WG_API int wg_host_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uin
 WG_API int wg_host_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
                            float beta_r, float beta_k, float midpoint, float slope, int device);
 
+/* ---- contrast metrics (metrics.py:84-135) -----------------
+ * Pair counts behind CCPR / CCFR / E-score for one (rgb, gray) fp64 image pair
+ * of npix pixels: per threshold tau_k (1..15 strictly increasing, positive)
+ * the numbers of pairs with delta_e >= tau (colour set), with both >= tau
+ * (kept), with gray_diff >= tau (gray set) and gray-but-not-colour
+ * (fabricated), delta_e being the CIE76 distance of the pixels' Lab colours
+ * and gray_diff |100 g_i - 100 g_j|. pair_i / pair_j (both NULL = all
+ * n(n-1)/2 unordered pairs) list the sampled pairs. The device entry writes
+ * the (ntau+1)^2 histogram of (#tau <= delta_e, #tau <= gray_diff);
+ * wg_metric_counts_from_hist turns it into counts[ntau][4]. */
+WG_API size_t wg_metric_scratch_bytes(int64_t npix);
+WG_API int wg_metric_hist_f64(const double* rgb, const double* gray, int64_t npix, const double* taus, int ntau,
+                              const int64_t* pair_i, const int64_t* pair_j, int64_t npairs,
+                              unsigned long long* hist, void* scratch, size_t scratch_bytes, void* stream);
+WG_API int wg_metric_counts_from_hist(const unsigned long long* hist, int ntau, int64_t* counts);
+WG_API int wg_host_metric_counts_f64(const double* rgb, const double* gray, int64_t npix, const double* taus,
+                                     int ntau, const int64_t* pair_i, const int64_t* pair_j, int64_t npairs,
+                                     int64_t* counts, int device);
+
 /* ---- uint8 file ingest / egress (codec.py:37-82, 135-140) -----
  * Binary PGM (P5, 1 channel) / PPM (P6, 3 channels), maxval 255, with the
  * reference's header grammar and errors. Host-only; files are read straight

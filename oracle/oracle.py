@@ -37,6 +37,8 @@ _SIGS = {
     "or_luma_u8": [_c_u8p, _c_u8p, _i64, _i, _i],
     "or_local_lhe_f64": [_c_dp, _c_dp, _i64, _i64, _i64, _i64, _i64, _i, _d, _i],
     "or_tone_local_u8": [_c_u8p, _c_u8p, _c_u8p, _i64, _i64, _i64, _d, _d, _i64, _i64, _i, _d, _i],
+    "or_metric_counts_f64": [_c_dp, _c_dp, _i64, _c_dp, _i, ctypes.POINTER(ctypes.c_int64),
+                             ctypes.POINTER(ctypes.c_int64), _i64, ctypes.POINTER(ctypes.c_int64), _i],
     "or_sigmoid_f64": [_c_dp, _c_dp, _i64, _d, _d],
     "or_reinstate_f64": [_c_dp, _c_dp, _c_dp, _c_dp, _i64],
     "or_tone_u8": [_c_u8p, _c_u8p, _c_u8p, _i64, _d, _d, _d, _d, _i],
@@ -156,6 +158,26 @@ def tone_local_u8(rgb: np.ndarray, tile_w: int, tile_h: int, bins: int = 256, st
                            _ptr(gray, ctypes.c_uint8) if gray is not None else None, n, h, w, beta_r, beta_k,
                            tile_w, tile_h, bins, strength, threads)
     return (toned, gray) if with_gray else toned
+
+
+def metric_counts(rgb: np.ndarray, gray: np.ndarray, taus, pairs=None, threads: int = 1) -> np.ndarray:
+    """_sweep_counts (metrics.py:118-135): (ntau, 4) counts; pairs = (i, j) arrays or None for all pairs."""
+    rgb = np.ascontiguousarray(rgb, dtype=np.float64)
+    gray = np.ascontiguousarray(gray, dtype=np.float64)
+    taus = np.ascontiguousarray(taus, dtype=np.float64)
+    out = np.zeros((len(taus), 4), dtype=np.int64)
+    pi = pj = None
+    npairs = 0
+    if pairs is not None:
+        pi = np.ascontiguousarray(pairs[0], dtype=np.int64)
+        pj = np.ascontiguousarray(pairs[1], dtype=np.int64)
+        npairs = len(pi)
+    lib().or_metric_counts_f64(_ptr(rgb, ctypes.c_double), _ptr(gray, ctypes.c_double), gray.size,
+                               _ptr(taus, ctypes.c_double), len(taus),
+                               _ptr(pi, ctypes.c_int64) if pi is not None else None,
+                               _ptr(pj, ctypes.c_int64) if pj is not None else None, npairs,
+                               _ptr(out, ctypes.c_int64), threads)
+    return out
 
 
 def sigmoid_f64(x: np.ndarray, midpoint=0.5, slope=8.0) -> np.ndarray:

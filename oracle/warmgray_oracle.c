@@ -240,6 +240,82 @@ OR_API void or_luma_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, int metho
     run_spans(npix, threads, luma8_span, &c);
 }
 
+/* ------------------------------------------------------------------ */
+/* Contrast metrics: _sweep_counts (metrics.py:84-135) written out per pair.
+ * lab = lab_rows of the colour image, g100 = gray * 100; for each pair
+ * de = sqrt((d0*d0 + d1*d1) + d2*d2), gd = |g100_i - g100_j|, and per tau the
+ * four counts (colour set, kept, gray set, fabricated). pair_i == NULL means
+ * all unordered pairs i < j. Threads split the anchor range. */
+typedef struct {
+    const double* lab; const double* g; int64_t n; const double* taus; int ntau;
+    const int64_t* pi; const int64_t* pj; int64_t npairs; int64_t* counts; /* [threads][ntau][4] */
+} met_ctx;
+static void met_pair(const met_ctx* x, int64_t i, int64_t j, int64_t* c) {
+    const double* a = x->lab + 3 * i;
+    const double* b = x->lab + 3 * j;
+    double d0 = a[0] - b[0], d1 = a[1] - b[1], d2 = a[2] - b[2];
+    double de = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    double gd = fabs(x->g[i] - x->g[j]);
+    for (int k = 0; k < x->ntau; ++k) {
+        double t = x->taus[k];
+        int in_c = de >= t, in_g = gd >= t;
+        c[4 * k] += in_c;
+        c[4 * k + 1] += in_c && in_g;
+        c[4 * k + 2] += in_g;
+        c[4 * k + 3] += in_g && !in_c;
+    }
+}
+typedef struct { const met_ctx* m; int64_t* c; int64_t p0, p1; } met_job;
+static void* met_thread(void* arg) {
+    met_job* jb = (met_job*)arg;
+    const met_ctx* x = jb->m;
+    if (x->pi) {
+        for (int64_t q = jb->p0; q < jb->p1; ++q) met_pair(x, x->pi[q], x->pj[q], jb->c);
+    } else {
+        for (int64_t i = jb->p0; i < jb->p1; ++i)
+            for (int64_t j = i + 1; j < x->n; ++j) met_pair(x, i, j, jb->c);
+    }
+    return NULL;
+}
+OR_API void or_metric_counts_f64(const double* rgb, const double* gray, int64_t npix, const double* taus,
+                                 int ntau, const int64_t* pair_i, const int64_t* pair_j, int64_t npairs,
+                                 int64_t* counts, int threads) {
+    memset(counts, 0, sizeof(int64_t) * 4 * (size_t)ntau);
+    if (npix < 2) return;
+    double* lab = (double*)malloc(sizeof(double) * 3 * (size_t)npix);
+    double* g = (double*)malloc(sizeof(double) * (size_t)npix);
+    lab64_ctx lc = {rgb, lab};
+    lab64_span(&lc, 0, npix);
+    for (int64_t p = 0; p < npix; ++p) g[p] = gray[p] * 100.0;
+    met_ctx m = {lab, g, npix, taus, ntau, pair_i, pair_j, npairs, NULL};
+    int64_t units = pair_i ? npairs : npix - 1;
+    if (threads < 1) threads = 1;
+    if (threads > units) threads = units > 0 ? (int)units : 1;
+    int64_t* part = (int64_t*)calloc((size_t)threads * 4 * (size_t)ntau, sizeof(int64_t));
+    pthread_t* tid = (pthread_t*)calloc((size_t)threads, sizeof(pthread_t));
+    met_job* jobs = (met_job*)calloc((size_t)threads, sizeof(met_job));
+    for (int t = 0; t < threads; ++t) {
+        /* anchors are interleaved so the triangular work balances */
+        jobs[t].m = &m;
+        jobs[t].c = part + (size_t)t * 4 * (size_t)ntau;
+        jobs[t].p0 = units * t / threads;
+        jobs[t].p1 = units * (t + 1) / threads;
+        if (pthread_create(&tid[t], NULL, met_thread, &jobs[t]) != 0) {
+            met_thread(&jobs[t]);
+            tid[t] = 0;
+        }
+    }
+    for (int t = 0; t < threads; ++t) {
+        if (tid[t]) pthread_join(tid[t], NULL);
+        for (int k = 0; k < 4 * ntau; ++k) counts[k] += part[(size_t)t * 4 * (size_t)ntau + (size_t)k];
+    }
+    free(part);
+    free(tid);
+    free(jobs);
+    free(lab);
+    free(g);
+}
+
 /* apply_sigmoid on fp64 luminance (tonemap.py:72-83) */
 OR_API void or_sigmoid_f64(const double* in, double* out, int64_t n, double midpoint,
                            double slope) {

@@ -60,6 +60,17 @@ from .colorspaces import (
     luminance_image,
     rgb_to_lab,
 )
+from .metrics import (
+    TAU_SWEEP,
+    MetricReport,
+    PairSampleConfig,
+    TauScore,
+    ccfr,
+    ccpr,
+    escore,
+    evaluate,
+    write_sweep_csv,
+)
 from .core import (
     DEFAULT_PARAMS,
     DecolorParams,
@@ -143,4 +154,13 @@ __all__ = [
     "luma_host",
     "decolor_tone_local",
     "decolor_tone_local_host",
+    "TAU_SWEEP",
+    "PairSampleConfig",
+    "TauScore",
+    "MetricReport",
+    "escore",
+    "ccpr",
+    "ccfr",
+    "evaluate",
+    "write_sweep_csv",
 ]

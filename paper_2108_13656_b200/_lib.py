@@ -87,6 +87,10 @@ SIGNATURES = {
     "wg_host_quantize_u8_f64": (_i, [_vp, _vp, _i64, _i]),
     "wg_host_dequantize_u8_f64": (_i, [_vp, _vp, _i64, _i]),
     "wg_host_hdr_tonemap_u8": (_i, [_vp, _vp, _i64, _i64, _f, _f, _f, _f, _i]),
+    "wg_metric_scratch_bytes": (_sz, [_i64]),
+    "wg_metric_hist_f64": (_i, [_vp, _vp, _i64, _vp, _i, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "wg_metric_counts_from_hist": (_i, [_vp, _i, _vp]),
+    "wg_host_metric_counts_f64": (_i, [_vp, _vp, _i64, _vp, _i, _vp, _vp, _i64, _vp, _i]),
     "wg_pnm_probe": (_i, [ctypes.c_char_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                           ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_i64)]),
     "wg_pnm_read_batch": (_i, [ctypes.POINTER(ctypes.c_char_p), _i64, _vp, _i64, _i64, ctypes.c_int32,

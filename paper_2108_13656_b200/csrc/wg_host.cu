@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include <string>
 
 #include "../../include/warmgray_b200.h"
@@ -216,6 +217,35 @@ static int host_pipeline(int device, int64_t nunits, const HostIn* ins, int nin,
 
 static size_t no_scratch(int64_t) { return 0; }
 
+// Runs fn(stream) on `device` with one of its pipeline streams (device
+// checks, lazy stream creation, the device lock held), then synchronises.
+template <class F>
+static int on_device(int device, F fn) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return set_error(WG_ENODEV, "no CUDA device available (this library has no CPU fallback)");
+    }
+    if (device < 0 || device >= ndev || device >= kMaxDevices)
+        return set_error(WG_ENODEV, "device ordinal %d out of range (have %d)", device, ndev);
+    DeviceGuard guard(device);
+    if (guard.status() != cudaSuccess) return cuda_fail(guard.status(), "cudaSetDevice");
+    DevCtx& ctx = g_ctx[device];
+    std::lock_guard<std::mutex> lock(ctx.mu);
+    if (!ctx.init) {
+        for (Slot& sl : ctx.slots) {
+            cudaError_t e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        }
+        ctx.init = true;
+    }
+    cudaStream_t st = ctx.slots[0].stream;
+    int rc = fn(st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess && rc == WG_OK) rc = cuda_fail(e, "cudaStreamSynchronize");
+    return rc;
+}
+
 }  // namespace wg
 
 using namespace wg;
@@ -403,6 +433,64 @@ extern "C" int wg_host_dequantize_u8_f64(const uint8_t* in_, double* out, int64_
                              return wg_dequantize_u8_f64(static_cast<const uint8_t*>(di[0]),
                                                          static_cast<double*>(dout[0]), k, st);
                          });
+}
+
+// CCPR / CCFR pair counts (metrics.py:84-135) for one (rgb, gray) image pair
+extern "C" int wg_host_metric_counts_f64(const double* rgb, const double* gray, int64_t npix, const double* taus,
+                                         int ntau, const int64_t* pair_i, const int64_t* pair_j, int64_t npairs,
+                                         int64_t* counts, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_npix(npairs) || check_ptrs(npix, rgb, gray));
+    if (!taus || !counts || ntau < 1 || ntau > 15) return set_error(WG_EINVAL, "need 1..15 thresholds and counts");
+    if ((pair_i == nullptr) != (pair_j == nullptr)) return set_error(WG_EINVAL, "pair_i / pair_j: both or neither");
+    if (pair_i) {
+        for (int64_t q = 0; q < npairs; ++q)
+            if (pair_i[q] < 0 || pair_i[q] >= npix || pair_j[q] < 0 || pair_j[q] >= npix)
+                return set_error(WG_EINVAL, "pair index out of range at %lld", static_cast<long long>(q));
+    }
+    const int stride = ntau + 1;
+    std::vector<unsigned long long> hist(static_cast<size_t>(stride * stride), 0ull);
+    int rc = on_device(device, [&](cudaStream_t st) {
+        const size_t b_rgb = align256(static_cast<size_t>(npix) * 24), b_gray = align256(static_cast<size_t>(npix) * 8);
+        const size_t b_pairs = pair_i ? align256(static_cast<size_t>(npairs) * 8) : 0;
+        const size_t b_hist = align256(hist.size() * 8);
+        const size_t b_scratch = wg_metric_scratch_bytes(npix);
+        const size_t b_taus = 256;
+        uint8_t* d = nullptr;
+        const size_t total = b_rgb + b_gray + 2 * b_pairs + b_hist + b_scratch + b_taus;
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), total, st);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(metric)");
+        uint8_t* p = d;
+        double* d_rgb = reinterpret_cast<double*>(p); p += b_rgb;
+        double* d_gray = reinterpret_cast<double*>(p); p += b_gray;
+        int64_t* d_pi = pair_i ? reinterpret_cast<int64_t*>(p) : nullptr; p += b_pairs;
+        int64_t* d_pj = pair_i ? reinterpret_cast<int64_t*>(p) : nullptr; p += b_pairs;
+        unsigned long long* d_hist = reinterpret_cast<unsigned long long*>(p); p += b_hist;
+        void* d_scratch = p;
+        int r = WG_OK;
+        auto h2d = [&](void* dst, const void* src, size_t bytes) {
+            if (r == WG_OK && bytes) {
+                cudaError_t ee = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+                if (ee != cudaSuccess) r = cuda_fail(ee, "cudaMemcpyAsync H2D");
+            }
+        };
+        h2d(d_rgb, rgb, static_cast<size_t>(npix) * 24);
+        h2d(d_gray, gray, static_cast<size_t>(npix) * 8);
+        if (pair_i) {
+            h2d(d_pi, pair_i, static_cast<size_t>(npairs) * 8);
+            h2d(d_pj, pair_j, static_cast<size_t>(npairs) * 8);
+        }
+        if (r == WG_OK)
+            r = wg_metric_hist_f64(d_rgb, d_gray, npix, taus, ntau, d_pi, d_pj, npairs, d_hist, d_scratch, b_scratch,
+                                   st);
+        if (r == WG_OK) {
+            e = cudaMemcpyAsync(hist.data(), d_hist, hist.size() * 8, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) r = cuda_fail(e, "cudaMemcpyAsync D2H");
+        }
+        cudaFreeAsync(d, st);
+        return r;
+    });
+    if (rc != WG_OK) return rc;
+    return wg_metric_counts_from_hist(hist.data(), ntau, counts);
 }
 
 // LocalHistogramGrid validation (tonemap.py:45-51), also for empty images

@@ -32,6 +32,9 @@ into this repository; only the outputs below are committed:
                       (plus hand-made headers and malformed files) and
                       codec.json: what the reference's load_image returns for
                       each (uint8 samples) or which exception it raises
+  metrics.npz/json    _sweep_counts / evaluate / ccpr / ccfr / write_sweep_csv of
+                      the reference on seeded image pairs (exhaustive and
+                      sampled pair sets, several gray methods)
   colorspaces.json    scalar known answers (luma_weighted, hsv_v, rgb_to_lab,
                       lab_lightness, delta_e76) and sha256 of the u8 cube
                       through luminance_image for y / v / lab
@@ -210,7 +213,48 @@ def main() -> None:
     colorspaces_golden(wg, get_kernels)
     lhe_golden(wg)
     codec_golden(wg)
+    metrics_golden(wg)
     print("golden fixtures written to", HERE)
+
+
+def metrics_golden(wg) -> None:
+    """the reference's contrast metrics."""
+    import io as _io
+
+    from warmgray import metrics as m
+
+    rng = np.random.default_rng(2111)
+    cases = []  # (name, rgb, gray, cfg)
+    rgb = rng.random((12, 10, 3))
+    cases.append(("exh_ours", rgb, wg.luminance_image(wg.PlanarImage(rgb)).data, m.PairSampleConfig(exhaustive=True)))
+    cases.append(("exh_lab", rgb, wg.luminance_image(wg.PlanarImage(rgb), method="lab").data,
+                  m.PairSampleConfig(exhaustive=True)))
+    u8 = rng.integers(0, 256, (40, 56, 3)).astype(np.float64) / 255.0
+    cases.append(("smp_ours", u8, wg.luminance_image(wg.PlanarImage(u8)).data, m.PairSampleConfig()))
+    cases.append(("smp_v", u8, wg.luminance_image(wg.PlanarImage(u8), method="v").data,
+                  m.PairSampleConfig(pair_count=3000, seed=9)))
+    small = rng.random((3, 3, 3))
+    cases.append(("cover", small, wg.luminance_image(wg.PlanarImage(small)).data,
+                  m.PairSampleConfig(pair_count=100, seed=7)))
+    out, js = {}, {}
+    taus = list(m.TAU_SWEEP)
+    for name, c, g, cfg in cases:
+        ci, gi = wg.PlanarImage(c), wg.PlanarImage(g)
+        out[f"{name}_rgb"] = c
+        out[f"{name}_gray"] = g
+        out[f"{name}_counts"] = m._sweep_counts(ci, gi, taus, cfg)
+        rep = m.evaluate(ci, gi, cfg)
+        js[name] = {"cfg": [cfg.pair_count, cfg.seed, cfg.exhaustive],
+                    "per_tau": [[r.tau, r.ccpr, r.ccfr, r.escore] for r in rep.per_tau],
+                    "mean_escore": rep.mean_escore,
+                    "ccpr_2.5": m.ccpr(ci, gi, 2.5, cfg), "ccfr_7": m.ccfr(ci, gi, 7.0, cfg)}
+    buf = _io.StringIO()
+    m.write_sweep_csv(buf, [("a", m.evaluate(wg.PlanarImage(cases[0][1]), wg.PlanarImage(cases[0][2]), cases[0][3])),
+                            ("b", m.evaluate(wg.PlanarImage(cases[2][1]), wg.PlanarImage(cases[2][2]), cases[2][3]))])
+    js["csv"] = buf.getvalue()
+    np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
+    with open(os.path.join(HERE, "metrics.json"), "w") as f:
+        json.dump(js, f, indent=1)
 
 
 def codec_golden(wg) -> None:
@@ -352,6 +396,12 @@ def colorspaces_golden(wg, get_kernels) -> None:
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["metrics"]:
+        sys.path.insert(0, build_reference())
+        import warmgray as _wg
+
+        metrics_golden(_wg)
+        sys.exit(0)
     if sys.argv[1:] == ["codec"]:
         sys.path.insert(0, build_reference())
         import warmgray as _wg

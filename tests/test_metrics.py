@@ -1,0 +1,178 @@
+"""Contrast metrics CCPR / CCFR / E-score.
+
+CPU: the oracle's pair counts against the reference's own _sweep_counts
+(tests/golden/metrics.npz), the host-side report logic (escore, sampling
+config, CSV layout) against the reference's reports and CSV bytes.
+GPU: the product's counts / reports against the same fixtures and against
+the oracle on larger images (exhaustive and sampled), plus the reference's
+boundary properties.
+"""
+
+import io
+import json
+import os
+
+import numpy as np
+import pytest
+from hypothesis import given
+from hypothesis import strategies as st
+
+from conftest import GOLDEN, rand_rgb
+
+import paper_2108_13656_b200 as wg
+from paper_2108_13656_b200 import metrics as m
+
+CASES = ["exh_ours", "exh_lab", "smp_ours", "smp_v", "cover"]
+EXHAUSTIVE = m.PairSampleConfig(exhaustive=True)
+
+
+@pytest.fixture(scope="module")
+def npz():
+    return np.load(os.path.join(GOLDEN, "metrics.npz"))
+
+
+@pytest.fixture(scope="module")
+def js():
+    with open(os.path.join(GOLDEN, "metrics.json")) as f:
+        return json.load(f)
+
+
+def _cfg(js, name):
+    pc, seed, exh = js[name]["cfg"]
+    return m.PairSampleConfig(pair_count=pc, seed=seed, exhaustive=exh)
+
+
+# ---------------------------------------------------------------- CPU
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_counts_match_reference(npz, js, name):
+    from oracle import oracle
+
+    rgb, gray = npz[f"{name}_rgb"], npz[f"{name}_gray"]
+    pairs = m.sample_pairs(gray.size, _cfg(js, name))
+    got = oracle.metric_counts(rgb, gray, list(m.TAU_SWEEP), pairs, threads=4)
+    np.testing.assert_array_equal(got, npz[f"{name}_counts"])
+
+
+def test_escore_and_config():
+    assert m.escore(1.0, 1.0) == 1.0
+    assert m.escore(0.5, 1.0) == pytest.approx(0.6667, abs=1e-4)
+    assert m.escore(0.0, 0.0) == 0.0
+    with pytest.raises(ValueError):
+        m.PairSampleConfig(pair_count=0)
+    m.PairSampleConfig(pair_count=0, exhaustive=True)
+    assert m.TAU_SWEEP == tuple(range(1, 16))
+
+
+@given(a=st.floats(0, 1), b=st.floats(0, 1))
+def test_escore_between(a, b):
+    e = m.escore(a, b)
+    assert min(a, b) - 1e-12 <= e <= max(a, b) + 1e-12
+    assert m.escore(a, a) == pytest.approx(a, abs=1e-12)
+
+
+def test_sample_pairs_is_the_reference_draw():
+    i, j = m.sample_pairs(1000, m.PairSampleConfig(pair_count=50, seed=5))
+    rng = np.random.default_rng(5)
+    ri = rng.integers(0, 1000, 50)
+    rj = (ri + rng.integers(1, 1000, 50)) % 1000
+    np.testing.assert_array_equal(i, ri)
+    np.testing.assert_array_equal(j, rj)
+    assert (i != j).all()
+    assert m.sample_pairs(3, m.PairSampleConfig(pair_count=3)) is None  # covers all 3 pairs
+
+
+def test_csv_bytes_match_reference(js):
+    def rep(name):
+        rows = tuple(m.TauScore(*r) for r in js[name]["per_tau"])
+        return m.MetricReport(rows, js[name]["mean_escore"])
+
+    buf = io.StringIO()
+    m.write_sweep_csv(buf, [("a", rep("exh_ours")), ("b", rep("smp_ours"))])
+    assert buf.getvalue() == js["csv"]
+    lines = buf.getvalue().strip().split("\n")
+    assert lines[0] == "image,tau,ccpr,ccfr,escore" and len(lines) == 1 + 2 * 16 + 1
+    assert lines[16].startswith("a,mean,") and lines[-1].startswith("ALL,mean,")
+
+
+def test_validation(rng):
+    with pytest.raises(ValueError):
+        m.evaluate(rand_rgb(rng, 3, 3), wg.PlanarImage(np.zeros((2, 3))))
+    with pytest.raises(ValueError):
+        m.evaluate(rand_rgb(rng, 3, 3), rand_rgb(rng, 3, 3))
+    for tau in (0, -1.0):
+        with pytest.raises(ValueError):
+            m.ccpr(rand_rgb(rng, 2, 2), wg.PlanarImage(np.zeros((2, 2))), tau)
+
+
+# ---------------------------------------------------------------- GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_product_matches_reference(npz, js, name):
+    rgb, gray = wg.PlanarImage(npz[f"{name}_rgb"]), wg.PlanarImage(npz[f"{name}_gray"])
+    cfg = _cfg(js, name)
+    np.testing.assert_array_equal(m.sweep_counts(rgb, gray, m.TAU_SWEEP, cfg), npz[f"{name}_counts"])
+    rep = m.evaluate(rgb, gray, cfg)
+    assert [[r.tau, r.ccpr, r.ccfr, r.escore] for r in rep.per_tau] == js[name]["per_tau"]
+    assert rep.mean_escore == js[name]["mean_escore"]
+    assert m.ccpr(rgb, gray, 2.5, cfg) == js[name]["ccpr_2.5"]
+    assert m.ccfr(rgb, gray, 7.0, cfg) == js[name]["ccfr_7"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,cfg", [((64, 64), EXHAUSTIVE), ((37, 53), EXHAUSTIVE),
+                                       ((256, 256), m.PairSampleConfig()),
+                                       ((300, 200), m.PairSampleConfig(pair_count=200_000, seed=1))])
+def test_counts_vs_oracle(shape, cfg):
+    from oracle import oracle
+
+    rng = np.random.default_rng(shape[0])
+    rgb = rng.integers(0, 256, shape + (3,)).astype(np.float64) / 255.0
+    gray = wg.luminance_image(wg.PlanarImage(rgb)).data
+    taus = [0.5, 1, 2, 3.5, 4, 5, 6, 7, 8, 9, 10, 11, 12.25, 13, 15]
+    got = m.sweep_counts(wg.PlanarImage(rgb), wg.PlanarImage(gray), taus, cfg)
+    want = oracle.metric_counts(rgb, gray, taus, m.sample_pairs(gray.size, cfg), threads=oracle.default_threads())
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.gpu
+def test_reference_properties(rng):
+    v = rng.random((6, 6))
+    color = wg.PlanarImage(np.repeat(v[:, :, None], 3, axis=2))
+    rep = m.evaluate(color, wg.luminance_image(color, method="lab"), EXHAUSTIVE)
+    assert all(r.escore == 1.0 for r in rep.per_tau) and rep.mean_escore == 1.0  # achromatic identity
+    color = rand_rgb(rng, 5, 5)
+    half = wg.PlanarImage(np.full((5, 5), 0.5))
+    assert m.ccpr(color, half, 5.0, EXHAUSTIVE) == 0.0 and m.ccfr(color, half, 5.0, EXHAUSTIVE) == 1.0
+    flat = wg.PlanarImage(np.full((1, 2, 3), 0.4))
+    split = wg.PlanarImage(np.array([[0.1, 0.9]]))
+    assert m.ccfr(flat, split, 5.0, EXHAUSTIVE) == 0.0 and m.ccpr(flat, split, 5.0, EXHAUSTIVE) == 1.0
+    one = m.evaluate(wg.PlanarImage(np.full((1, 1, 3), 0.3)), wg.PlanarImage(np.full((1, 1), 0.3)), EXHAUSTIVE)
+    assert one.mean_escore == 1.0
+    color = rand_rgb(rng, 5, 5)
+    gray = wg.luminance_image(color)
+    perm = rng.permutation(25)
+    cp = wg.PlanarImage(color.data.reshape(25, 3)[perm].reshape(5, 5, 3))
+    gp = wg.PlanarImage(gray.data.reshape(25)[perm].reshape(5, 5))
+    assert m.evaluate(color, gray, EXHAUSTIVE) == m.evaluate(cp, gp, EXHAUSTIVE)
+    small = rand_rgb(rng, 3, 3)
+    sg = wg.luminance_image(small)
+    assert m.evaluate(small, sg, m.PairSampleConfig(pair_count=100, seed=7)) == m.evaluate(small, sg, EXHAUSTIVE)
+
+
+@pytest.mark.gpu
+def test_bad_pairs_rejected():
+    from paper_2108_13656_b200 import _lib
+
+    rgb = np.zeros((4, 3))
+    g = np.zeros(4)
+    taus = np.array([1.0])
+    pi = np.array([0, 5], dtype=np.int64)
+    pj = np.array([1, 2], dtype=np.int64)
+    out = np.zeros((1, 4), dtype=np.int64)
+    with pytest.raises(ValueError):
+        _lib.call("wg_host_metric_counts_f64", rgb.ctypes.data, g.ctypes.data, 4, taus.ctypes.data, 1,
+                  pi.ctypes.data, pj.ctypes.data, 2, out.ctypes.data, 0)
+    bad = np.array([2.0, 1.0])
+    with pytest.raises(ValueError):
+        _lib.call("wg_host_metric_counts_f64", rgb.ctypes.data, g.ctypes.data, 4, bad.ctypes.data, 2,
+                  None, None, 0, out.ctypes.data, 0)
