@@ -111,21 +111,25 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(Op op, const uint8_t* 
 // bulk-copy ring at equal parity).
 // Occupancy 5 CTAs/SM (<= 51 registers, no spills) and a 40 x SM grid measured
 // best on C3 (scripts/tune_u8.cu: 74.7% of the HBM roofline vs 70.9% at 4 CTAs/SM).
-template <class Op>
-__global__ void __launch_bounds__(kThreads, 5) ldg_stream_kernel(Op op, const uint8_t* __restrict__ in,
-                                                                 int64_t ntiles, int64_t npix) {
-    constexpr int kTilePx = kThreads * Op::kPx;
+// kBlock = 256 is the throughput shape; small inputs (fewer tiles than a
+// couple of waves) use 64-thread CTAs so a single image still spreads over
+// every SM (C1: 256 CTAs instead of 64).
+template <class Op, int kBlock = kThreads>
+__global__ void __launch_bounds__(kBlock, kBlock == kThreads ? 5 : 20)
+    ldg_stream_kernel(Op op, const uint8_t* __restrict__ in, int64_t ntiles, int64_t npix) {
+    constexpr int kTilePx = kBlock * Op::kPx;
+    constexpr int64_t kBlockBytes = kBlock * 48;
     run_prologue(op);
     const int tid = threadIdx.x;
     const int64_t stride = gridDim.x;
     int64_t t = blockIdx.x;
     if (t < ntiles) {
-        const uint4* p = reinterpret_cast<const uint4*>(in + t * kTileBytes) + tid * 3;
+        const uint4* p = reinterpret_cast<const uint4*>(in + t * kBlockBytes) + tid * 3;
         uint4 v[3] = {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)};
         for (; t < ntiles; t += stride) {
             uint4 n[3] = {v[0], v[1], v[2]};
             if (t + stride < ntiles) {
-                const uint4* q = reinterpret_cast<const uint4*>(in + (t + stride) * kTileBytes) + tid * 3;
+                const uint4* q = reinterpret_cast<const uint4*>(in + (t + stride) * kBlockBytes) + tid * 3;
                 n[0] = __ldcs(q);
                 n[1] = __ldcs(q + 1);
                 n[2] = __ldcs(q + 2);
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 5) ldg_stream_kernel(Op op, const ui
         }
     }
     if (blockIdx.x == gridDim.x - 1) {
-        for (int64_t p = ntiles * kTilePx + tid; p < npix; p += kThreads) op.scalar(p);
+        for (int64_t p = ntiles * kTilePx + tid; p < npix; p += kBlock) op.scalar(p);
     }
 }
 
@@ -180,7 +184,13 @@ static int launch_stream(const Op& op, const void* in, const void* const* outs, 
         if (outs[i] && (reinterpret_cast<uintptr_t>(outs[i]) & 15) != 0) aligned = false;
     constexpr int64_t kTilePx = kThreads * Op::kPx;
     const int64_t ntiles = npix / kTilePx;
-    if (aligned && Op::kLdg) {
+    constexpr int kSmall = 64;
+    if (aligned && Op::kLdg && ntiles < 2LL * sm_count(device)) {
+        const int64_t st = npix / (kSmall * Op::kPx);
+        const int64_t grid = std::max<int64_t>(1, st);
+        ldg_stream_kernel<Op, kSmall><<<static_cast<unsigned>(grid), kSmall, 0, stream>>>(
+            op, static_cast<const uint8_t*>(in), st, npix);
+    } else if (aligned && Op::kLdg) {
         const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, 40LL * sm_count(device)));
         ldg_stream_kernel<Op><<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(
             op, static_cast<const uint8_t*>(in), ntiles, npix);
