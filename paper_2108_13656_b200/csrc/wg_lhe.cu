@@ -51,7 +51,11 @@ constexpr float kGrayMargin = 1e-6f;  // bin edges (gray domain)
 constexpr float kGray255Margin = 255.0f * kGrayMargin;  // the same in the 0..255 domain
 // (bins of the uint8 route need margin_t = kGrayMargin * nb < 0.5, i.e. nb < 500000)
 constexpr int kGrp = 16;                                // pixels per thread group (48 input bytes)
-constexpr float kQuantMargin = 1e-3f;  // quantization (x = v * 255 + 0.5 domain)
+// quantization margin in the x = 255 v + 0.5 domain. Error budget of the uint8
+// route's fp32 x: gray estimate <= 255 * 2.4e-7 = 6.1e-5, fp32 curves (255
+// domain) <= 7.6e-6, fp32 blend fractions <= 2 * 255 * 6e-8, the six roundings
+// of the blend <= 6e-5: < 1.6e-4, so 4e-4 leaves 2.5x headroom.
+constexpr float kQuantMargin = 4e-4f;
 constexpr size_t kHistSmemCap = 96 * 1024;
 constexpr size_t kApplySmemCap = 200 * 1024;
 
@@ -73,6 +77,7 @@ struct LheBufs {
     int32_t* yi;  // [h]
     double* yf;
     float* yff;
+    float* gray255;  // [nimg][h][w] uint8 route: the hist pass's 255 * gray estimate, reused by apply
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -97,6 +102,7 @@ size_t layout(const LheGeom& g, uint8_t* base, LheBufs* b) {
     t.yi = reinterpret_cast<int32_t*>(take(g.h * 4));
     t.yf = reinterpret_cast<double*>(take(g.h * 8));
     t.yff = reinterpret_cast<float*>(take(g.h * 4));
+    t.gray255 = reinterpret_cast<float*>(take(static_cast<size_t>(g.nimg) * g.h * g.w * 4));
     if (b) *b = t;
     return off;
 }
@@ -475,7 +481,8 @@ struct U8Lhe {
 };
 
 __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
-                                                              int rows_per_chunk, bool vec) {
+                                                              float* __restrict__ gplane, int rows_per_chunk,
+                                                              bool vec) {
     extern __shared__ uint32_t sh[];  // [nx * nb] + one dummy cell
     const int64_t img = blockIdx.z;
     const int ty = blockIdx.y;
@@ -515,6 +522,16 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
         if (n == kGrp) {
             float g255[kGrp];
             grp.gray255(L.k8, g255);
+            // keep the estimate for the apply pass (4 B/px instead of recomputing the gray)
+            if (vec) {
+#pragma unroll
+                for (int q = 0; q < kGrp / 4; ++q)
+                    reinterpret_cast<float4*>(gplane + p0)[q] =
+                        make_float4(g255[4 * q], g255[4 * q + 1], g255[4 * q + 2], g255[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < kGrp; ++q) gplane[p0 + q] = g255[q];
+            }
             // runs of equal cells are merged before the shared-memory atomic; the
             // first flush goes to the dummy cell
             int run_cell = cells;
@@ -544,6 +561,7 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
                 L.src.load(p0 + p, cr, cg, cb);
                 const float g255 = decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
                                                    static_cast<float>(cb), L.k8);
+                gplane[p0 + p] = g255;
                 bool sure;
                 const int b = L.bin_fast(g255, sure);
                 if (sure) atomicAdd(&sh[tx * g.nb + b], 1u);
@@ -594,32 +612,67 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
     const int64_t tile0 = img * g.ntile + static_cast<int64_t>(jbase) * g.nx;
     const int ncur = nload * g.nx * g.nb;
     for (int i = threadIdx.x; i < ncur; i += blockDim.x) cur[i] = s.curvef[tile0 * g.nb + i];
+    // column x = 16 gc + 4 q + r is stored at ((q * G + gc) * 4 + r), G = wp / 16: the
+    // lanes of a warp (consecutive groups gc) then read consecutive 16-byte vectors
+    const int64_t G = wp / kGrp;
     for (int64_t x = threadIdx.x; x < wp; x += blockDim.x) {
         const int64_t xc = imin64(x, g.w - 1);
-        sxf[x] = s.xff[xc];
-        sxo[x] = static_cast<uint32_t>(s.xi[xc] * g.nb);
+        const int64_t gc = x / kGrp, q = (x % kGrp) >> 2, r = x & 3;
+        const int64_t at = (q * G + gc) * 4 + r;
+        sxf[at] = s.xff[xc];
+        sxo[at] = static_cast<uint32_t>(s.xi[xc] * g.nb);
     }
     __syncthreads();
     const float sf = static_cast<float>(g.strength);
     const int dnb = g.nx > 1 ? g.nb : 0;  // i1 - i0 in curve-table units
     const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
     const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
+    // the hist pass's gray estimates (identical to recomputing them), one group of
+    // register prefetch ahead
+    auto load_est = [&](uint32_t gi, float4 (&e)[kGrp / 4]) {
+        const uint32_t gy = gi / gpr;
+        const int x0 = static_cast<int>(gi - gy * gpr) * kGrp;
+        const int n = static_cast<int>(imin64(kGrp, g.w - x0));
+        const float* src = s.gray255 + (img * g.h + y0 + gy) * g.w + x0;
+        if (vec && n == kGrp) {
+#pragma unroll
+            for (int q = 0; q < kGrp / 4; ++q) e[q] = __ldcs(reinterpret_cast<const float4*>(src) + q);
+        } else {
+            float t[kGrp];
+#pragma unroll
+            for (int q = 0; q < kGrp; ++q) t[q] = q < n ? src[q] : 0.0f;
+#pragma unroll
+            for (int q = 0; q < kGrp / 4; ++q) e[q] = make_float4(t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
+        }
+    };
+    float4 nxt[kGrp / 4];
+    if (threadIdx.x < ngroups) load_est(threadIdx.x, nxt);
     for (uint32_t gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
         const uint32_t gy = gi / gpr;
         const int64_t y = y0 + gy;
         const int x0 = static_cast<int>(gi - gy * gpr) * kGrp;
         const int n = static_cast<int>(imin64(kGrp, g.w - x0));
         const int64_t p0 = (img * g.h + y) * g.w + x0;
+        float g255[kGrp];
+#pragma unroll
+        for (int q = 0; q < kGrp / 4; ++q) {
+            g255[4 * q] = nxt[q].x;
+            g255[4 * q + 1] = nxt[q].y;
+            g255[4 * q + 2] = nxt[q].z;
+            g255[4 * q + 3] = nxt[q].w;
+        }
+        if (gi + blockDim.x < ngroups) load_est(gi + blockDim.x, nxt);
         const int j0 = s.yi[y], j1 = g.ny > 1 ? j0 + 1 : 0;
         const int r0nb = (j0 - jbase) * g.nx * g.nb, drow = (j1 - j0) * g.nx * g.nb;
         const float wy = s.yff[y];
         // the group's 16 blend fractions and curve offsets as 128-bit shared loads
         float wxs[kGrp];
         uint32_t xos[kGrp];
+        const int64_t gcol = x0 / kGrp;
 #pragma unroll
         for (int q = 0; q < kGrp / 4; ++q) {
-            const float4 f = reinterpret_cast<const float4*>(sxf + x0)[q];
-            const uint4 o = reinterpret_cast<const uint4*>(sxo + x0)[q];
+            const float4 f = reinterpret_cast<const float4*>(sxf)[q * G + gcol];
+            const uint4 o = reinterpret_cast<const uint4*>(sxo)[q * G + gcol];
             wxs[4 * q] = f.x;
             wxs[4 * q + 1] = f.y;
             wxs[4 * q + 2] = f.z;
@@ -629,10 +682,6 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
             xos[4 * q + 2] = o.z;
             xos[4 * q + 3] = o.w;
         }
-        U8Group grp;
-        grp.load(L.src.rgb, p0, n, vec);
-        float g255[kGrp];
-        grp.gray255(L.k8, g255);
         uint32_t ot[4] = {0u, 0u, 0u, 0u}, og[4] = {0u, 0u, 0u, 0u};
         uint32_t slow = 0;
 #pragma unroll
@@ -887,9 +936,10 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     const Chunking c = chunking(g);
     const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4;  // + the dummy cell
     const size_t asmem = ApplySmem::bytes(g.nx, g.nb, g.w);
-    // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact)
-    const bool group_ok = bins <= 65536;
-    if (group_ok && hsmem <= kHistSmemCap) {
+    // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact); the
+    // group apply reads the gray plane the group hist writes, so both or neither
+    const bool group_ok = bins <= 65536 && hsmem <= kHistSmemCap && asmem <= kApplySmemCap;
+    if (group_ok) {
         if (hsmem > 48 * 1024)
             cudaFuncSetAttribute(lhe_hist_u8g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(hsmem));
@@ -897,13 +947,13 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
             U8Lhe Li = L;
             Li.src.advance(i0 * g.h * g.w);
             lhe_hist_u8g_kernel<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, hsmem, st>>>(
-                Li, gi, b.hist + i0 * g.ntile * g.nb, c.rows_per_chunk, vec);
+                Li, gi, b.hist + i0 * g.ntile * g.nb, b.gray255 + i0 * g.h * g.w, c.rows_per_chunk, vec);
         });
     } else {
         lhe_hist(src, g, b, st);
     }
     lhe_curves(g, b, st);
-    if (group_ok && asmem <= kApplySmemCap) {
+    if (group_ok) {
         auto kern = gray_or_null ? lhe_apply_u8g_kernel<true> : lhe_apply_u8g_kernel<false>;
         if (asmem > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(asmem));
@@ -915,6 +965,7 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
             bi.curvef += i0 * g.ntile * g.nb;
             bi.ident += i0 * g.ntile;
             const int64_t off = i0 * g.h * g.w;
+            bi.gray255 += off;
             kern<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, asmem, st>>>(
                 Li, toned + off, gray_or_null ? gray_or_null + off : nullptr, gi, bi, c.rows_per_chunk, vec);
         });
