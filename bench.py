@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--images", type=int, default=None, help="images per GPU (default: workload's)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="C5: skip the per-GPU size sweep (256x256 .. 8K at fixed total pixels)")
     ap.add_argument("--no-methods", action="store_true",
                     help="skip the per-method side table (paper Table 1 on the GPU + local tone map)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -304,6 +306,11 @@ def main():
     del out, rgb
     torch.cuda.empty_cache()
 
+    sweep = None
+    if wl.name == "C5" and not args.no_sweep:
+        sweep = run_size_sweep(wg, torch, dev, stream, rank)
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, sample = cpu_port_rate(wl, seconds=args.cpu_seconds)
@@ -325,9 +332,47 @@ def main():
         }
         if methods:
             line["methods"] = methods
+        if sweep:
+            line["size_sweep"] = sweep
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_size_sweep(wg, torch, dev, stream, rank, iters: int = 5):
+    """C5's per-GPU size sweep: 256x256 .. 8K uint8 images at fixed total pixels.
+
+    BASELINE.json configs[4]: the same ~4.3 Gpx per GPU cut into images of each
+    size (synth.SIZE_SWEEP), i.i.d. uniform bytes generated on the device; one
+    decolor launch per step over the whole batch, device-timed. Shows the
+    throughput does not depend on the image size (the kernels see a flat
+    pixel stream).
+    """
+    from paper_2108_13656_b200 import synth
+
+    total = max(n * h * w for h, w, n in synth.SIZE_SWEEP)
+    buf = torch.empty(total * 3, dtype=torch.uint8, device=dev)
+    gout = torch.empty(total, dtype=torch.uint8, device=dev)
+    res = {}
+    for h, w, n in synth.SIZE_SWEEP:
+        px = n * h * w
+        rgb = buf[: px * 3].view(n, h, w, 3)
+        synth.fill_uniform_u8(rgb, seed=5, first_image=rank * n)
+        out = gout[:px].view(n, h, w)
+        wg.decolor(rgb, out=out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            wg.decolor(rgb, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        res[f"{w}x{h}"] = {"images": n, "gpix": round(px / 1e9, 3), "gpix_s": round(px / ms / 1e6, 1)}
+    del buf, gout
+    res["note"] = (f"{iters} device-resident passes per size in this order, uint8 i.i.d. input, fixed total pixels "
+                   "per GPU; sw_power_cap engages over the sweep, so later sizes run at lower SM clocks")
+    return res
 
 
 def run_methods(wg, torch, rgb, out, n_img, wl, stream, iters: int = 5):
@@ -340,6 +385,11 @@ def run_methods(wg, torch, rgb, out, n_img, wl, stream, iters: int = 5):
     decolor + local tone map (tonemap_image(mode="local")).
     """
     grid = wg.LocalHistogramGrid.for_image(wl.width, wl.height)
+    # at most ~2.2 Gpx (all of C3; 66 frames of C5): the local tone map's scratch
+    # holds a 4 B/px gray plane and the extractors allocate their outputs
+    n_img = min(n_img, max(1, 2_200_000_000 // wl.pix_per_image))
+    rgb = rgb[:n_img]
+    out = out[:n_img]
     img4 = rgb.view(n_img, wl.height, wl.width, 3)
     scratch = torch.empty(int(wg._lib.load().wg_lhe_scratch_bytes(n_img, wl.height, wl.width, grid.tile_w,
                                                                   grid.tile_h, grid.bins)),
