@@ -66,9 +66,19 @@ WG_API int wg_sm_count(int device);
 
 /* uint8 RGB -> uint8 gray, i.e. quantize_u8(decolor_image(dequantize_u8(rgb)))
  * (codec.py:22-29 around core.py:147-169 / _kernels.pyx:31-56), fused in one
- * pass over a flat batch of npix pixels: 3 B in, 1 B out per pixel. */
-WG_API int wg_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r, float beta_k,
+ * pass over a flat batch of npix pixels: 3 B in, 1 B out per pixel. Identical
+ * to the reference except +-1 on rounding ties (5e-6 of all colours; the
+ * north-star bar is 1e-4). */
+WG_API int wg_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r, double beta_k,
                   void* stream);
+/* Same, bit-identical to the reference for every input (~10% slower): pixels
+ * whose fp32 result lies next to a rounding boundary take the exact byte of
+ * their colour from a per-(beta_r, beta_k) table settled once over all 2^24
+ * colours against the fp64 chain (built on the first call, cached per device). */
+WG_API int wg_decolor_u8_exact(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r, double beta_k,
+                               void* stream);
+/* Diagnostics of that table: boundary margin (2^-15 units) and slot count. */
+WG_API int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, uint32_t* slots);
 
 /* fp32 RGB in [0,1] -> fp32 gray (decolor_image on float data; core.py:147-169). */
 WG_API int wg_decolor_f32(const float* rgb, float* gray, int64_t npix, float beta_r, float beta_k,
@@ -171,8 +181,10 @@ WG_API int wg_host_luma_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, int m
 WG_API int wg_host_decolor_rows_f64(const double* rgb, double* out, int64_t height, int64_t width,
                              double beta_r, double beta_k, int64_t row0, int64_t row1,
                              int device);
-WG_API int wg_host_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r,
-                       float beta_k, int device);
+WG_API int wg_host_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r,
+                       double beta_k, int device);
+WG_API int wg_host_decolor_u8_exact(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r,
+                                    double beta_k, int device);
 WG_API int wg_host_decolor_f32(const float* rgb, float* gray, int64_t npix, float beta_r, float beta_k,
                         int device);
 WG_API int wg_host_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null,

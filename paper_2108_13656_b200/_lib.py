@@ -49,7 +49,9 @@ SIGNATURES = {
     "wg_last_error": (ctypes.c_char_p, []),
     "wg_device_count": (_i, []),
     "wg_sm_count": (_i, [_i]),
-    "wg_decolor_u8": (_i, [_vp, _vp, _i64, _f, _f, _vp]),
+    "wg_decolor_u8": (_i, [_vp, _vp, _i64, _d, _d, _vp]),
+    "wg_decolor_u8_exact": (_i, [_vp, _vp, _i64, _d, _d, _vp]),
+    "wg_u8_exact_info": (_i, [_d, _d, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]),
     "wg_decolor_f32": (_i, [_vp, _vp, _i64, _f, _f, _vp]),
     "wg_decolor_f64": (_i, [_vp, _vp, _i64, _d, _d, _vp]),
     "wg_sigmoid_f64": (_i, [_vp, _vp, _i64, _d, _d, _vp]),
@@ -78,7 +80,8 @@ SIGNATURES = {
     "wg_host_lab_rows_f64": (_i, [_vp, _vp, _i64, _i64, _i64, _i64, _i]),
     "wg_host_luma_u8": (_i, [_vp, _vp, _i64, _i, _i]),
     "wg_host_decolor_rows_f64": (_i, [_vp, _vp, _i64, _i64, _d, _d, _i64, _i64, _i]),
-    "wg_host_decolor_u8": (_i, [_vp, _vp, _i64, _f, _f, _i]),
+    "wg_host_decolor_u8": (_i, [_vp, _vp, _i64, _d, _d, _i]),
+    "wg_host_decolor_u8_exact": (_i, [_vp, _vp, _i64, _d, _d, _i]),
     "wg_host_decolor_f32": (_i, [_vp, _vp, _i64, _f, _f, _i]),
     "wg_host_decolor_tone_u8": (_i, [_vp, _vp, _vp, _i64, _f, _f, _f, _f, _i]),
     "wg_host_sigmoid_f64": (_i, [_vp, _vp, _i64, _d, _d, _i]),

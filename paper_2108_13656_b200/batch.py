@@ -59,8 +59,13 @@ def _stream(stream, device):
     return s.cuda_stream
 
 
-def decolor(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, stream=None):
-    """Gray of a device-resident (..., 3) uint8 / float32 / float64 batch."""
+def decolor(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, stream=None, exact: bool = False):
+    """Gray of a device-resident (..., 3) uint8 / float32 / float64 batch.
+
+    uint8: identical to quantize_u8 of the reference except +-1 on rounding
+    ties (5e-6 of colours); ``exact=True`` makes it bit-identical (~10%
+    slower). float64 is always bit-identical; float32 within 1e-6.
+    """
     torch = _torch()
     name = _check_rgb_tensor(rgb, _DECOLOR_FN)
     if out is None:
@@ -69,9 +74,9 @@ def decolor(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, stream=None):
             or out.device != rgb.device:
         raise ValueError("out must be a contiguous tensor of shape rgb.shape[:-1], same dtype/device")
     n = out.numel()
+    fn = "wg_decolor_u8_exact" if exact and name == "uint8" else _DECOLOR_FN[name]
     with torch.cuda.device(rgb.device):
-        _lib.call(_DECOLOR_FN[name], rgb.data_ptr(), out.data_ptr(), n, params.beta_r,
-                  params.beta_k, _stream(stream, rgb.device))
+        _lib.call(fn, rgb.data_ptr(), out.data_ptr(), n, params.beta_r, params.beta_k, _stream(stream, rgb.device))
     return out
 
 
@@ -240,8 +245,9 @@ def _host_rgb(rgb, dtypes):
     return np.ascontiguousarray(arr)
 
 
-def decolor_host(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, device: int | None = None):
-    """Gray of a host (..., 3) uint8 / float32 / float64 array via the pipelined host path."""
+def decolor_host(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, device: int | None = None,
+                 exact: bool = False):
+    """Gray of a host (..., 3) uint8 / float32 / float64 array via the pipelined host path (see :func:`decolor`)."""
     arr = _host_rgb(rgb, ("uint8", "float32", "float64"))
     if out is None:
         out = np.empty(arr.shape[:-1], dtype=arr.dtype)
@@ -251,8 +257,8 @@ def decolor_host(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, device: 
     n = out.size
     if n:
         if arr.dtype == np.uint8:
-            _lib.call("wg_host_decolor_u8", arr.ctypes.data, out.ctypes.data, n, params.beta_r,
-                      params.beta_k, dev)
+            _lib.call("wg_host_decolor_u8_exact" if exact else "wg_host_decolor_u8", arr.ctypes.data,
+                      out.ctypes.data, n, params.beta_r, params.beta_k, dev)
         elif arr.dtype == np.float32:
             _lib.call("wg_host_decolor_f32", arr.ctypes.data, out.ctypes.data, n, params.beta_r,
                       params.beta_k, dev)

@@ -159,9 +159,9 @@ struct U8Consts {
     float cr, c1, sqrt3, c3, inv_c4sq;
 };
 
-inline U8Consts make_u8_consts(float beta_r, float beta_k) {
+inline U8Consts make_u8_consts(double beta_r, double beta_k) {
     // derive in double, round once to fp32
-    double br = beta_r, bk = beta_k;
+    const double br = beta_r, bk = beta_k;
     U8Consts k;
     k.cr = static_cast<float>(br / (1.0 - br));
     k.c1 = static_cast<float>(1.7320508075688772 * std::sqrt(1.0 - br));
@@ -281,6 +281,118 @@ __device__ __forceinline__ uint8_t decolor255_x1(float r, float g, float b, cons
     float X = __fmaf_rn(T, S2k, 1e-30f);
     float y = rsqrt_mufu(X);
     return static_cast<uint8_t>(__float_as_uint(__fmaf_rn(T, y, kMagic)) & 0xFFu);
+}
+
+// Exact-rounding variants: the final FMA adds 256.5 instead of 2^23, so the
+// float's bits hold floor(T*y + 0.5) in bits 15..22 and the next 15 bits of
+// its fraction below them (value in [256.5, 512): exponent fixed, ulp 2^-15).
+// The integer part is the fast byte; the fraction tells how close T*y came to
+// a rounding boundary (csrc/wg_u8exact.cu settles those against the fp64
+// reference). Same FMA-pipe work as decolor255_x2.
+constexpr float kMagicFrac = 256.5f;
+__device__ __forceinline__ float2 decolor255_bits_x2(float2 R, float2 G, float2 B, const U8Consts& k) {
+    float2 R2 = mul2(R, R);
+    float2 G2 = mul2(G, G);
+    float2 RG2 = add2(R2, G2);
+    float2 q = fma2(B, B, RG2);
+    float2 p = fma2(R2, bc2(k.cr), G2);
+    float2 Rc1 = mul2(R, bc2(k.c1));
+    float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
+    float2 RGq = make_float2(sqrt_mufu(p.x), sqrt_mufu(p.y));
+    float2 RG = add2(R, G);
+    float2 S = add2(RG, B);
+    float2 GB = add2(G, B);
+    float2 t1 = mul2(GB, W);
+    float2 A = fma2(Rc1, RGq, t1);
+    float2 u = fma2(RG, bc2(k.sqrt3), W);
+    float2 Bp = mul2(B, u);
+    float2 B2 = mul2(Bp, Bp);
+    float2 A2 = mul2(A, A);
+    float2 T = fma2(B2, bc2(k.c3), A2);
+    float2 S2 = mul2(S, S);
+    float2 S2k = mul2(S2, bc2(k.inv_c4sq));
+    float2 X = fma2(T, S2k, bc2(1e-30f));
+    float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
+    return fma2(T, y, bc2(kMagicFrac));
+}
+// scalar twin (lane-exact: identical IEEE rn operation sequence)
+__device__ __forceinline__ uint32_t decolor255_bits_x1(float r, float g, float b, const U8Consts& k) {
+    float R2 = __fmul_rn(r, r);
+    float G2 = __fmul_rn(g, g);
+    float RG2 = __fadd_rn(R2, G2);
+    float q = __fmaf_rn(b, b, RG2);
+    float p = __fmaf_rn(R2, k.cr, G2);
+    float Rc1 = __fmul_rn(r, k.c1);
+    float W = sqrt_mufu(q);
+    float RGq = sqrt_mufu(p);
+    float RG = __fadd_rn(r, g);
+    float S = __fadd_rn(RG, b);
+    float GB = __fadd_rn(g, b);
+    float t1 = __fmul_rn(GB, W);
+    float A = __fmaf_rn(Rc1, RGq, t1);
+    float u = __fmaf_rn(RG, k.sqrt3, W);
+    float Bp = __fmul_rn(b, u);
+    float B2 = __fmul_rn(Bp, Bp);
+    float A2 = __fmul_rn(A, A);
+    float T = __fmaf_rn(B2, k.c3, A2);
+    float S2 = __fmul_rn(S, S);
+    float S2k = __fmul_rn(S2, k.inv_c4sq);
+    float X = __fmaf_rn(T, S2k, 1e-30f);
+    return __float_as_uint(__fmaf_rn(T, rsqrt_mufu(X), kMagicFrac));
+}
+// byte and boundary distance (in 2^-15 units) of decolor255_bits_* results
+__device__ __forceinline__ uint32_t bits_byte(uint32_t bits) { return (bits >> 15) & 0xFFu; }
+__device__ __forceinline__ bool bits_near_tie(uint32_t bits, uint32_t margin) {
+    return ((bits + margin) & 0x7FFFu) <= 2u * margin;
+}
+
+// 1 if any of the 16 results lies within `margin` of a rounding boundary:
+// ((bits + margin) << 17) < (2 margin + 1) << 17, chained through one
+// predicate (a shift-add and an OR-compare per pixel)
+__device__ __forceinline__ uint32_t any_near_tie16(const uint32_t (&b)[16], uint32_t madd, uint32_t mlim) {
+    uint32_t r;
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "mad.lo.u32 t, %1, 131072, %17;\n\tsetp.lt.u32 p, t, %18;\n\t"
+        "mad.lo.u32 t, %2, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %3, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %4, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %5, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %6, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %7, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %8, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %9, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %10, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %11, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %12, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %13, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %14, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %15, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "mad.lo.u32 t, %16, 131072, %17;\n\tsetp.lt.or.u32 p, t, %18, p;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r)
+        : "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7]), "r"(b[8]),
+          "r"(b[9]), "r"(b[10]), "r"(b[11]), "r"(b[12]), "r"(b[13]), "r"(b[14]), "r"(b[15]), "r"(madd), "r"(mlim));
+    return r;
+}
+
+// Exact bytes of the near-tie colours (csrc/wg_u8exact.cu): an open-addressing
+// table of (rgb << 8 | byte) entries, 0xFFFFFFFF = empty (white is never a
+// near-tie colour). A pixel whose fast result lies within `margin` of a
+// rounding boundary looks its colour up; absent means the fast byte is exact.
+struct U8Exact {
+    const uint32_t* tab;
+    uint32_t mask;    // slots - 1 (power of two)
+    uint32_t margin;  // in 2^-15 units
+};
+__host__ __device__ __forceinline__ uint32_t u8exact_slot(uint32_t key, uint32_t mask) {
+    return (key * 2654435761u >> 8) & mask;
+}
+static __device__ __noinline__ uint32_t u8exact_lookup(U8Exact t, uint32_t key, uint32_t fast) {
+    for (uint32_t s = u8exact_slot(key, t.mask);; s = (s + 1) & t.mask) {
+        const uint32_t e = __ldg(t.tab + s);
+        if (e == 0xFFFFFFFFu) return fast;
+        if ((e >> 8) == key) return e & 0xFFu;
+    }
 }
 
 // ---------------------------------------------------------------- fp32 path (accurate)

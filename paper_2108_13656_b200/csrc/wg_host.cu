@@ -331,8 +331,8 @@ extern "C" int wg_host_luma_u8(const uint8_t* rgb, uint8_t* out, int64_t npix, i
                          });
 }
 
-extern "C" int wg_host_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r,
-                                  float beta_k, int device) {
+extern "C" int wg_host_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r,
+                                  double beta_k, int device) {
     WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
     HostIn in[1] = {{rgb, 3}};
     HostOut o[1] = {{gray, 1}};
@@ -340,6 +340,18 @@ extern "C" int wg_host_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npi
                          [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
                              return wg_decolor_u8(static_cast<const uint8_t*>(di[0]),
                                                   static_cast<uint8_t*>(dout[0]), n, beta_r, beta_k, st);
+                         });
+}
+
+extern "C" int wg_host_decolor_u8_exact(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r,
+                                        double beta_k, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
+    HostIn in[1] = {{rgb, 3}};
+    HostOut o[1] = {{gray, 1}};
+    return host_pipeline(device, npix, in, 1, o, 1, 4096, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_decolor_u8_exact(static_cast<const uint8_t*>(di[0]),
+                                                        static_cast<uint8_t*>(dout[0]), n, beta_r, beta_k, st);
                          });
 }
 

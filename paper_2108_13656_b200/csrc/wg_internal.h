@@ -21,6 +21,11 @@ int check_ptrs(int64_t n, const void* a, const void* b);
 int check_params(double beta_r, double beta_k);   // core.py:33-51: 0.5 < beta < 1
 int check_curve(double midpoint, double slope);   // tonemap.py:22-33
 
+struct U8Exact;
+// Near-tie table of the bit-exact uint8 decolor for (beta_r, beta_k) on the
+// current device (csrc/wg_u8exact.cu); built on first use, then cached.
+int u8exact_get(double beta_r, double beta_k, U8Exact* out);
+
 }  // namespace wg
 
 #define WG_CHECK_ARGS(failed) \

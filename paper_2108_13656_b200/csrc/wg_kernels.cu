@@ -31,6 +31,8 @@ namespace wg {
 // handles one pixel straight from global memory (tails, unaligned buffers)
 // with bit-identical arithmetic.
 
+// Default uint8 op: round-to-nearest of 255*gray in fp32 (the north-star bar:
+// identical except +-1 on <= 0.01% of pixels; measured 5e-6 over all colours).
 struct OpDecolorU8 {
     static constexpr bool kLdg = true;
     static constexpr int kInBpp = 3;
@@ -65,6 +67,89 @@ struct OpDecolorU8 {
     __device__ __forceinline__ void scalar(int64_t p) const {
         gray[p] = decolor255_x1(static_cast<float>(in[3 * p]), static_cast<float>(in[3 * p + 1]),
                                 static_cast<float>(in[3 * p + 2]), k);
+    }
+};
+
+
+// Bit-exact variant (opt-in, wg_decolor_u8_exact): the final FMA keeps 15
+// fraction bits (decolor255_bits_x2); groups with a pixel within the table's
+// margin of a rounding boundary take the exact byte of that colour from the
+// near-tie table (csrc/wg_u8exact.cu). ~10% slower than OpDecolorU8 on C3:
+// the shift, shift-add and compare per pixel compete for issue slots with the
+// saturated FMA and MUFU pipes.
+struct OpDecolorU8Exact {
+    static constexpr bool kLdg = true;
+    static constexpr int kInBpp = 3;
+    static constexpr int kPx = 16;
+    const uint8_t* in;
+    uint8_t* gray;
+    U8Consts k;
+    U8Exact ex;  // exact bytes of the near-tie colours (csrc/wg_u8exact.cu)
+
+    __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
+        const uint32_t w[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y,
+                                v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
+        uint32_t bits[16];
+        // near-tie test: ((bits + margin) << 17) < (2 margin + 1) << 17, i.e. the
+        // 15-bit fraction within `margin` of a rounding boundary; one shift-add and
+        // one compare per pixel, OR-ed into a per-group flag
+        const uint32_t madd = ex.margin << 17, mlim = (2u * ex.margin + 1u) << 17;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            // pixels 2j and 2j+1 share one packed lane pair
+            float2 ch[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int b0 = 3 * (2 * j) + c, b1 = 3 * (2 * j + 1) + c;
+                ch[c] = make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3));
+                ch[c] = add2(ch[c], bc2(-kMagic));
+            }
+            const float2 f = decolor255_bits_x2(ch[0], ch[1], ch[2], k);
+            bits[2 * j] = __float_as_uint(f.x);
+            bits[2 * j + 1] = __float_as_uint(f.y);
+        }
+        const uint32_t any_tie = any_near_tie16(bits, madd, mlim);
+        // low byte of bits >> 15 = floor(255 gray + 0.5)
+        uint4 o;
+        o.x = __byte_perm(__byte_perm(bits[0] >> 15, bits[1] >> 15, 0x0040u),
+                          __byte_perm(bits[2] >> 15, bits[3] >> 15, 0x0040u), 0x5410u);
+        o.y = __byte_perm(__byte_perm(bits[4] >> 15, bits[5] >> 15, 0x0040u),
+                          __byte_perm(bits[6] >> 15, bits[7] >> 15, 0x0040u), 0x5410u);
+        o.z = __byte_perm(__byte_perm(bits[8] >> 15, bits[9] >> 15, 0x0040u),
+                          __byte_perm(bits[10] >> 15, bits[11] >> 15, 0x0040u), 0x5410u);
+        o.w = __byte_perm(__byte_perm(bits[12] >> 15, bits[13] >> 15, 0x0040u),
+                          __byte_perm(bits[14] >> 15, bits[15] >> 15, 0x0040u), 0x5410u);
+        if (any_tie) fix_ties(bits, o, px0);  // ~0.4% of groups
+        st_global_cs_v4(gray + px0, o);
+    }
+    // pixels next to a rounding boundary take the exact byte of their colour
+    __device__ __forceinline__ void fix_ties(const uint32_t (&bits)[16], uint4& o, int64_t px0) const {
+        uint32_t slow = 0;
+#pragma unroll
+        for (int p = 0; p < 16; ++p) slow |= static_cast<uint32_t>(bits_near_tie(bits[p], ex.margin)) << p;
+        while (slow) {
+            const int p = __ffs(slow) - 1;
+            slow &= slow - 1;
+            const uint8_t* src = in + 3 * (px0 + p);
+            const uint32_t key = (static_cast<uint32_t>(__ldg(src)) << 16) | (static_cast<uint32_t>(__ldg(src + 1)) << 8) |
+                                 __ldg(src + 2);
+            const uint32_t sh = 8 * (p & 3), q = p >> 2;
+            const uint32_t word = q == 0 ? o.x : q == 1 ? o.y : q == 2 ? o.z : o.w;
+            const uint32_t e = u8exact_lookup(ex, key, (word >> sh) & 255u);
+            const uint32_t nw = (word & ~(255u << sh)) | (e << sh);
+            // o.{x,y,z,w} with a dynamic index would go to local memory: select instead
+            o.x = q == 0 ? nw : o.x;
+            o.y = q == 1 ? nw : o.y;
+            o.z = q == 2 ? nw : o.z;
+            o.w = q == 3 ? nw : o.w;
+        }
+    }
+    __device__ __forceinline__ void scalar(int64_t p) const {
+        const uint32_t r = in[3 * p], g = in[3 * p + 1], bl = in[3 * p + 2];
+        const uint32_t bits = decolor255_bits_x1(static_cast<float>(r), static_cast<float>(g), static_cast<float>(bl), k);
+        uint32_t q = bits_byte(bits);
+        if (bits_near_tie(bits, ex.margin)) q = u8exact_lookup(ex, (r << 16) | (g << 8) | bl, q);
+        gray[p] = static_cast<uint8_t>(q);
     }
 };
 
@@ -252,10 +337,23 @@ using namespace wg;
 
 // ====================================================================== C ABI (device pointers)
 
-extern "C" int wg_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, float beta_r,
-                             float beta_k, void* stream) {
+extern "C" int wg_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r,
+                             double beta_k, void* stream) {
     WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
+    if (npix == 0) return WG_OK;
     OpDecolorU8 op{rgb, gray, make_u8_consts(beta_r, beta_k)};
+    const void* outs[1] = {gray};
+    return launch_stream(op, rgb, outs, 1, npix, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int wg_decolor_u8_exact(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r, double beta_k,
+                                   void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
+    if (npix == 0) return WG_OK;
+    U8Exact ex;
+    const int rc = u8exact_get(beta_r, beta_k, &ex);
+    if (rc != WG_OK) return rc;
+    OpDecolorU8Exact op{rgb, gray, make_u8_consts(beta_r, beta_k), ex};
     const void* outs[1] = {gray};
     return launch_stream(op, rgb, outs, 1, npix, static_cast<cudaStream_t>(stream));
 }
