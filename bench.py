@@ -381,8 +381,10 @@ def run_methods(wg, torch, rgb, out, n_img, wl, stream, iters: int = 5):
     The paper's Table 1 compares its method's per-pixel time with the CIE Lab
     lightness baseline; BT.601 ("y") and HSV value ("v") are the reference's
     other extractors (colorspaces.py:87-112), all uint8 -> uint8 and
-    bit-identical to quantize_u8 of the reference. "local" is the fused
-    decolor + local tone map (tonemap_image(mode="local")).
+    bit-identical to quantize_u8 of the reference. "global_tone" is the fused
+    decolor + global sigmoid (tonemap_image(mode="global"), north-star bar)
+    and "local_tone" the fused decolor + local tone map (mode="local",
+    SURVEY 8 f1, bit-identical).
     """
     grid = wg.LocalHistogramGrid.for_image(wl.width, wl.height)
     # at most ~2.2 Gpx (all of C3; 66 frames of C5): the local tone map's scratch
@@ -396,6 +398,7 @@ def run_methods(wg, torch, rgb, out, n_img, wl, stream, iters: int = 5):
                           dtype=torch.uint8, device=rgb.device)
     fns = {
         "ours": lambda: wg.decolor(rgb, out=out),
+        "global_tone": lambda: wg.decolor_tone(rgb),
         "y_bt601": lambda: wg.luma(rgb, "y"),
         "v_hsv": lambda: wg.luma(rgb, "v"),
         "lab_lightness": lambda: wg.luma(rgb, "lab"),

@@ -176,47 +176,6 @@ struct OpDecolorF32 {
     }
 };
 
-// decolor + global sigmoid on uint8 input: toned u8 (+ optional gray u8)
-struct OpToneU8 {
-    static constexpr bool kLdg = false;
-    static constexpr int kInBpp = 3;
-    static constexpr int kPx = 16;
-    const uint8_t* in;
-    uint8_t* toned;
-    uint8_t* gray;  // may be null
-    AccConsts k;
-    float m, slope;
-
-    __device__ __forceinline__ void one(float r, float g, float b, const SigF& s, uint8_t& t,
-                                        uint8_t& q) const {
-        const float inv255 = 1.0f / 255.0f;
-        float l = decolor_acc(__fmul_rn(r, inv255), __fmul_rn(g, inv255), __fmul_rn(b, inv255), k);
-        t = quantize_f32(sigmoid_f(l, s));
-        q = quantize_f32(l);
-    }
-    __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
-        const SigF s = make_sig_f(m, slope);
-        const uint8_t* bytes = reinterpret_cast<const uint8_t*>(&v[0]);
-        uint32_t tw[4] = {0u, 0u, 0u, 0u}, qw[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-        for (int p = 0; p < 16; ++p) {
-            uint8_t t, q;
-            one(bytes[3 * p], bytes[3 * p + 1], bytes[3 * p + 2], s, t, q);
-            tw[p >> 2] |= static_cast<uint32_t>(t) << (8 * (p & 3));
-            qw[p >> 2] |= static_cast<uint32_t>(q) << (8 * (p & 3));
-        }
-        st_global_cs_v4(toned + px0, make_uint4(tw[0], tw[1], tw[2], tw[3]));
-        if (gray) st_global_cs_v4(gray + px0, make_uint4(qw[0], qw[1], qw[2], qw[3]));
-    }
-    __device__ __forceinline__ void scalar(int64_t p) const {
-        const SigF s = make_sig_f(m, slope);
-        uint8_t t, q;
-        one(in[3 * p], in[3 * p + 1], in[3 * p + 2], s, t, q);
-        toned[p] = t;
-        if (gray) gray[p] = q;
-    }
-};
-
 // decolor + global sigmoid (+ reinstate) on fp32 input
 struct OpToneF32 {
     static constexpr bool kLdg = false;
@@ -411,16 +370,6 @@ extern "C" int wg_tonemap_global_f64(const double* rgb, double* l_out, double* r
     tonemap_global_f64_kernel<<<ew_blocks(npix), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         rgb, l_out, rgb_out, npix, beta_r, beta_k, midpoint, slope);
     return check_launch("tonemap_global_f64");
-}
-
-extern "C" int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null,
-                                  int64_t npix, float beta_r, float beta_k, float midpoint,
-                                  float slope, void* stream) {
-    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, toned) || check_params(beta_r, beta_k) ||
-                  check_curve(midpoint, slope));
-    OpToneU8 op{rgb, toned, gray_or_null, make_acc_consts(beta_r, beta_k), midpoint, slope};
-    const void* outs[2] = {toned, gray_or_null};
-    return launch_stream(op, rgb, outs, 2, npix, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int wg_decolor_tone_f32(const float* rgb, float* toned, float* gray_or_null,

@@ -23,7 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mpix", type=int, default=512)
     ap.add_argument("--iters", type=int, default=50)
-    ap.add_argument("--methods", default="ours,y,v,lab,local")
+    ap.add_argument("--methods", default="ours,tone,y,v,lab,local")
     args = ap.parse_args()
     # 4K frames (C3 shape) so the tiled local tone map sees real images
     nimg = max(1, (args.mpix << 20) // (2160 * 3840))
@@ -37,6 +37,7 @@ def main():
     hbm = peaks.get("hbm_gbs", 6545.3)
     fns = {
         "ours": lambda: wg.decolor(rgb, out=out.view(n)),
+        "tone": lambda: wg.decolor_tone(rgb),
         "y": lambda: wg.luma(rgb, "y"),
         "v": lambda: wg.luma(rgb, "v"),
         "lab": lambda: wg.luma(rgb, "lab"),

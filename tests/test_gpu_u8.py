@@ -228,7 +228,8 @@ def test_tone_u8_cube(torch_dev, cube):
 
     torch, dev = torch_dev
     t = torch.from_numpy(cube).to(dev)
-    for m, k in [(0.5, 8.0), (0.3, 12.0), (0.5, 1e-6)]:
+    # k = 200 / 2000: bins with several thresholds (the binary-search fallback); m = 0 / 1: one-sided curves
+    for m, k in [(0.5, 8.0), (0.3, 12.0), (0.5, 1e-6), (0.5, 200.0), (0.6, 2000.0), (0.0, 3.0), (1.0, 3.0)]:
         toned, gray, _ = wg.decolor_tone(t, wg.SigmoidCurve(m, k), return_gray=True)
         want_t, want_g = oracle.tone_u8(cube, midpoint=m, slope=k, threads=oracle.default_threads(),
                                         with_gray=True)
@@ -237,6 +238,8 @@ def test_tone_u8_cube(torch_dev, cube):
         assert mx <= 1 and frac <= U8_MAX_FRAC
         mx, frac = u8_mismatch(gray.cpu().numpy(), want_g)
         assert mx <= 1 and frac <= U8_MAX_FRAC
+        # toned-only launch (the other kernel variant) gives the same bytes
+        assert torch.equal(wg.decolor_tone(t, wg.SigmoidCurve(m, k)), toned)
 
 
 def test_empty_and_errors(torch_dev):
