@@ -87,6 +87,22 @@ __device__ __forceinline__ int lut_bin(float r) {
     return min(max(b, 0), kLutBins - 1);
 }
 
+// 32-bit table entry: count of thresholds below the bin (bits 24..31) and the
+// low 17 bits of the float bits of the one threshold inside it (bits 0..17;
+// 0x20000 = none). All floats of a bin share their bits >> 17, so comparing
+// the low 17 bits of r with it is the float compare r >= threshold. One LDS.32
+// per pixel instead of an LDS.64 (fewer shared-memory wavefronts for these
+// random-bin lookups).
+__device__ __forceinline__ uint32_t lut_entry(int count, float thr) {
+    const uint32_t f = thr == INFINITY ? 0x20000u : (__float_as_uint(thr) & 0x1FFFFu);
+    return (static_cast<uint32_t>(count) << 24) | f;
+}
+__device__ __forceinline__ uint32_t lut_px32(float v, float inv, const uint32_t* s_lut) {
+    const uint32_t rb = __float_as_uint(__fmul_rn(v, inv));
+    const uint32_t e = s_lut[min(max(rb >> 17, 127u << 6), (127u << 6) + kLutBins - 1) - (127u << 6)];
+    return (e >> 24) + ((rb & 0x1FFFFu) >= (e & 0x3FFFFu) ? 1u : 0u);
+}
+
 // ---------------------------------------------------------------- per-pixel tone
 struct ToneU8 {
     float m, hk, t0, inv_den;
@@ -231,11 +247,11 @@ __global__ void __launch_bounds__(kT) hdr_stats_kernel(const float2* __restrict_
         __syncthreads();
         int off = incl - sum;
         for (int w = 0; w < warp; ++w) off += s_wsum[w];
-        float2* lut = luts + static_cast<int64_t>(img) * kLutBins;
+        uint32_t* lut = reinterpret_cast<uint32_t*>(luts) + static_cast<int64_t>(img) * kLutBins;
 #pragma unroll
         for (int j = 0; j < kLutBins / kT; ++j) {
             const int b = tid * (kLutBins / kT) + j;
-            lut[b] = make_float2(s_thr[b], __int_as_float(off + local[j]));
+            lut[b] = lut_entry(off + local[j], s_thr[b]);
         }
         st.lut = conflict ? 0 : 1;
     }
@@ -245,10 +261,45 @@ __global__ void __launch_bounds__(kT) hdr_stats_kernel(const float2* __restrict_
 // ---------------------------------------------------------------- pass 3: tone (image-uniform blocks)
 // One 16-px chunk (4 x 16 B loads, one 16 B store) per thread per iteration;
 // the per-image mode is hoisted out of the loop.
+// Table path for images of a multiple of 4096 px: gray tiles of 16 KiB stream
+// through a 3-stage cp.async.bulk ring; thread t takes float4 t + 256 j
+// (conflict-free LDS.128) and stores 4 coalesced 32-bit words.
+constexpr int kToneTilePx = 4096;
+constexpr int kToneStages = 3;
+constexpr int kToneSmem = kToneStages * kToneTilePx * 4 + kToneStages * 8;
+
 template <class Px>
 __device__ __forceinline__ void tone_loop(const float* __restrict__ g, uint8_t* __restrict__ o, int64_t ppi,
                                           bool discard, Px px) {
-    if ((ppi & 15) == 0) {
+    if (ppi % kToneTilePx == 0) {
+        // 4096-px tiles, thread t takes float4 t + 256 j (coalesced 128-bit loads,
+        // coalesced 32-bit stores), next tile prefetched into registers
+        const int64_t ntiles = ppi / kToneTilePx;
+        const int tid = threadIdx.x;
+        int64_t t = blockIdx.x;
+        float4 nx[4];
+        if (t < ntiles) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) nx[j] = __ldcs(reinterpret_cast<const float4*>(g + t * kToneTilePx) + tid + 256 * j);
+        }
+        for (; t < ntiles; t += gridDim.x) {
+            float4 v[4] = {nx[0], nx[1], nx[2], nx[3]};
+            if (t + gridDim.x < ntiles) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    nx[j] = __ldcs(reinterpret_cast<const float4*>(g + (t + gridDim.x) * kToneTilePx) + tid + 256 * j);
+            }
+            uint32_t* dst = reinterpret_cast<uint32_t*>(o + t * kToneTilePx);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                __stcs(dst + tid + 256 * j, px(v[j].x) | (px(v[j].y) << 8) | (px(v[j].z) << 16) | (px(v[j].w) << 24));
+            // this thread's loads of tile t are consumed: one 128 B gray line per 8 threads' float4s
+            if (discard && (tid & 7) == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) discard_l2_line(g + t * kToneTilePx + 4 * (tid + 256 * j));
+            }
+        }
+    } else if ((ppi & 15) == 0) {
         // register prefetch: chunk ch + step is in flight while chunk ch is toned
         const int64_t nchunks = ppi >> 4;
         const int64_t step = static_cast<int64_t>(gridDim.x) * kT;
@@ -295,12 +346,7 @@ __device__ __forceinline__ uint32_t lut_px(float v, float inv, const float2* s_l
     return static_cast<uint32_t>(__float_as_int(e.y)) + (r >= e.x ? 1u : 0u);
 }
 
-// Table path for images of a multiple of 4096 px: gray tiles of 16 KiB stream
-// through a 3-stage cp.async.bulk ring; thread t takes float4 t + 256 j
-// (conflict-free LDS.128) and stores 4 coalesced 32-bit words.
-constexpr int kToneTilePx = 4096;
-constexpr int kToneStages = 3;
-constexpr int kToneSmem = kToneStages * kToneTilePx * 4 + kToneStages * 8;
+
 
 template <class Px>
 __device__ __forceinline__ void tone_tiles(const float* __restrict__ g, uint8_t* __restrict__ o, int64_t ppi,
@@ -358,17 +404,17 @@ __global__ void __launch_bounds__(kT) hdr_tone_tiled_kernel(const float* __restr
                                                             const float2* __restrict__ luts, float m, float slope,
                                                             bool discard) {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ float2 s_lut[kLutBins];
+    __shared__ uint32_t s_lut[kLutBins];
     const int64_t img = blockIdx.y;
     const HdrStat st = stats[img];
     const float* g = gray + img * ppi;
     uint8_t* o = out + img * ppi;
     if (st.mode == 1 && st.lut) {  // block-uniform
-        const float2* lut = luts + img * kLutBins;
+        const uint32_t* lut = reinterpret_cast<const uint32_t*>(luts) + img * kLutBins;
         for (int q = threadIdx.x; q < kLutBins; q += kT) s_lut[q] = lut[q];
         // (made visible by the __syncthreads inside tone_tiles before first use)
         const float inv = st.inv_gmin;
-        tone_tiles(g, o, ppi, discard, smem, [&](float v) -> uint32_t { return lut_px(v, inv, s_lut); });
+        tone_tiles(g, o, ppi, discard, smem, [&](float v) -> uint32_t { return lut_px32(v, inv, s_lut); });
     } else if (st.mode == 2) {
         tone_tiles(g, o, ppi, discard, smem, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });
     } else {
@@ -381,17 +427,17 @@ __global__ void __launch_bounds__(kT) hdr_tone_kernel(const float* __restrict__ 
                                                       int64_t ppi, const HdrStat* __restrict__ stats,
                                                       const float2* __restrict__ luts, float m, float slope,
                                                       bool discard) {
-    __shared__ float2 s_lut[kLutBins];
+    __shared__ uint32_t s_lut[kLutBins];
     const int64_t img = blockIdx.y;
     const HdrStat st = stats[img];
     const float* g = gray + img * ppi;
     uint8_t* o = out + img * ppi;
     if (st.mode == 1 && st.lut) {
-        const float2* lut = luts + img * kLutBins;
+        const uint32_t* lut = reinterpret_cast<const uint32_t*>(luts) + img * kLutBins;
         for (int q = threadIdx.x; q < kLutBins; q += kT) s_lut[q] = lut[q];
         __syncthreads();
         const float inv = st.inv_gmin;
-        tone_loop(g, o, ppi, discard, [&](float v) -> uint32_t { return lut_px(v, inv, s_lut); });
+        tone_loop(g, o, ppi, discard, [&](float v) -> uint32_t { return lut_px32(v, inv, s_lut); });
     } else if (st.mode == 2) {
         tone_loop(g, o, ppi, discard, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });  // t = 1
     } else {
@@ -842,7 +888,7 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
         // drop the gray lines from L2 only when the group's plane can actually be resident there
         const bool discard = static_cast<size_t>(g) * pix_per_img * sizeof(float) <= (size_t(96) << 20) &&
                              !getenv("WG_HDR_NO_DISCARD");
-        if (pix_per_img % kToneTilePx == 0 && !getenv("WG_HDR_NO_TILED")) {
+        if (pix_per_img % kToneTilePx == 0 && getenv("WG_HDR_TILED")) {
             static int tone_occ[kMaxDevices] = {0};
             if (device >= 0 && device < kMaxDevices && !tone_occ[device]) {
                 cudaFuncSetAttribute(hdr_tone_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kToneSmem);
