@@ -291,8 +291,12 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": committed_traffic(wl.name),
                 "bytes_per_px": wl.bytes_per_px, "peak_source": peak_src,
-                "kernel": "stream_kernel<OpDecolorU8>" if wl.dtype == "uint8" and wl.output == "gray_u8"
-                else ("stream_kernel<OpDecolorF32>" if wl.output == "gray_f32" else "hdr_pass1+hdr_pass2")}
+                # the measured peak is a 1:1 copy; read-dominant streams (3:1 for the fp32
+                # path) can exceed it, so the fraction of the 8 TB/s HBM3e spec is given too
+                "frac_vs_spec_8000": round(achieved / 8000.0, 4),
+                "kernel": "ldg_stream_kernel<OpDecolorU8>" if wl.dtype == "uint8" and wl.output == "gray_u8"
+                else ("ldg_stream_kernel<OpDecolorF32>" if wl.output == "gray_f32"
+                      else "hdr_gray_kernel + hdr_stats_kernel + hdr_tone_kernel")}
 
     # ---- side table (not the metric): the paper's Table 1 comparison on this batch
     methods = None

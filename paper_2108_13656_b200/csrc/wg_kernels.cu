@@ -154,7 +154,7 @@ struct OpDecolorU8Exact {
 };
 
 struct OpDecolorF32 {
-    static constexpr bool kLdg = false;
+    static constexpr bool kLdg = true;
     static constexpr int kInBpp = 12;
     static constexpr int kPx = 4;
     const float* in;
@@ -178,7 +178,7 @@ struct OpDecolorF32 {
 
 // decolor + global sigmoid (+ reinstate) on fp32 input
 struct OpToneF32 {
-    static constexpr bool kLdg = false;
+    static constexpr bool kLdg = true;
     static constexpr int kInBpp = 12;
     static constexpr int kPx = 4;
     const float* in;
