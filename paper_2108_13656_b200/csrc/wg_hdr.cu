@@ -150,11 +150,24 @@ __global__ void __launch_bounds__(kT) hdr_gray_kernel(const float* __restrict__ 
     float* g = gray + static_cast<int64_t>(img) * ppi;
     float lo = INFINITY, hi = 0.0f;
     const bool vec = (ppi & 3) == 0 && (reinterpret_cast<uintptr_t>(rgb) & 15) == 0;
-    if (vec) {  // 4 px per thread: 3 x 16 B in (evict-first), 16 B out
-        for (int64_t q = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x; q < (ppi >> 2);
-             q += static_cast<int64_t>(gridDim.x) * kT) {
+    if (vec) {  // 4 px per thread: 3 x 16 B in (evict-first), 16 B out; next quad prefetched into registers
+        const int64_t nq = ppi >> 2, step = static_cast<int64_t>(gridDim.x) * kT;
+        int64_t q = blockIdx.x * static_cast<int64_t>(kT) + threadIdx.x;
+        float4 n0, n1, n2;
+        if (q < nq) {
             const float4* src = reinterpret_cast<const float4*>(in + 12 * q);
-            const float4 v0 = __ldcs(src), v1 = __ldcs(src + 1), v2 = __ldcs(src + 2);
+            n0 = __ldcs(src);
+            n1 = __ldcs(src + 1);
+            n2 = __ldcs(src + 2);
+        }
+        for (; q < nq; q += step) {
+            const float4 v0 = n0, v1 = n1, v2 = n2;
+            if (q + step < nq) {
+                const float4* src = reinterpret_cast<const float4*>(in + 12 * (q + step));
+                n0 = __ldcs(src);
+                n1 = __ldcs(src + 1);
+                n2 = __ldcs(src + 2);
+            }
             const float2 a = decolor_fast_x2(make_float2(v0.x, v0.w), make_float2(v0.y, v1.x),
                                              make_float2(v0.z, v1.y), k);
             const float2 b = decolor_fast_x2(make_float2(v1.z, v2.y), make_float2(v1.w, v2.z),
