@@ -593,36 +593,11 @@ struct ApplySmem {
     }
 };
 
-template <bool kGray>
-__global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8_t* __restrict__ toned,
-                                                               uint8_t* __restrict__ gray, LheGeom g, LheBufs s,
-                                                               int rows_per_chunk, bool vec) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int64_t img = blockIdx.z;
-    const int ty = blockIdx.y;
-    const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
-    const int64_t y1 = imin64(imin64(y0 + rows_per_chunk, static_cast<int64_t>(ty + 1) * g.th), g.h);
-    if (y0 >= y1) return;
-    // rows of this tile row blend tile rows {ty-1, ty, ty+1} at most
-    const int jbase = max(ty - 1, 0), nload = min(ty + 1, g.ny - 1) - jbase + 1;
-    const int64_t wp = ApplySmem::wpad(g.w);
-    float* cur = reinterpret_cast<float*>(smem);              // [3][nx][nb]: 255 * curve, NaN = identity
-    float* sxf = cur + static_cast<size_t>(3) * g.nx * g.nb;  // [wp]
-    uint32_t* sxo = reinterpret_cast<uint32_t*>(sxf + wp);    // [wp] i0 * nb
-    const int64_t tile0 = img * g.ntile + static_cast<int64_t>(jbase) * g.nx;
-    const int ncur = nload * g.nx * g.nb;
-    for (int i = threadIdx.x; i < ncur; i += blockDim.x) cur[i] = s.curvef[tile0 * g.nb + i];
-    // column x = 16 gc + 4 q + r is stored at ((q * G + gc) * 4 + r), G = wp / 16: the
-    // lanes of a warp (consecutive groups gc) then read consecutive 16-byte vectors
-    const int64_t G = wp / kGrp;
-    for (int64_t x = threadIdx.x; x < wp; x += blockDim.x) {
-        const int64_t xc = imin64(x, g.w - 1);
-        const int64_t gc = x / kGrp, q = (x % kGrp) >> 2, r = x & 3;
-        const int64_t at = (q * G + gc) * 4 + r;
-        sxf[at] = s.xff[xc];
-        sxo[at] = static_cast<uint32_t>(s.xi[xc] * g.nb);
-    }
-    __syncthreads();
+template <bool kGray, bool kIdent>
+__device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict__ toned, uint8_t* __restrict__ gray,
+                                             const LheGeom& g, const LheBufs& s, int64_t y0, int64_t y1, int64_t img,
+                                             int jbase, const float* cur, const float* sxf, const uint32_t* sxo,
+                                             int64_t G, bool vec) {
     const float sf = static_cast<float>(g.strength);
     const int dnb = g.nx > 1 ? g.nb : 0;  // i1 - i0 in curve-table units
     const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
@@ -691,10 +666,12 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
             const int b = L.bin_fast(v, sure);
             const int a00 = r0nb + static_cast<int>(xos[p]) + b, a10 = a00 + drow;
             float c00 = cur[a00], c01 = cur[a00 + dnb], c10 = cur[a10], c11 = cur[a10 + dnb];
-            c00 = c00 != c00 ? v : c00;  // NaN: identity tile (the pixel's own value)
-            c01 = c01 != c01 ? v : c01;
-            c10 = c10 != c10 ? v : c10;
-            c11 = c11 != c11 ? v : c11;
+            if constexpr (kIdent) {
+                c00 = c00 != c00 ? v : c00;  // NaN: identity tile (the pixel's own value)
+                c01 = c01 != c01 ? v : c01;
+                c10 = c10 != c10 ? v : c10;
+                c11 = c11 != c11 ? v : c11;
+            }
             const float wx = wxs[p];
             const float top = __fmaf_rn(wx, __fsub_rn(c01, c00), c00);
             const float bottom = __fmaf_rn(wx, __fsub_rn(c11, c10), c10);
@@ -758,6 +735,44 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
             }
         }
     }
+}
+
+template <bool kGray>
+__global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8_t* __restrict__ toned,
+                                                               uint8_t* __restrict__ gray, LheGeom g, LheBufs s,
+                                                               int rows_per_chunk, bool vec) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int64_t img = blockIdx.z;
+    const int ty = blockIdx.y;
+    const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
+    const int64_t y1 = imin64(imin64(y0 + rows_per_chunk, static_cast<int64_t>(ty + 1) * g.th), g.h);
+    if (y0 >= y1) return;
+    // rows of this tile row blend tile rows {ty-1, ty, ty+1} at most
+    const int jbase = max(ty - 1, 0), nload = min(ty + 1, g.ny - 1) - jbase + 1;
+    const int64_t wp = ApplySmem::wpad(g.w);
+    float* cur = reinterpret_cast<float*>(smem);              // [3][nx][nb]: 255 * curve, NaN = identity
+    float* sxf = cur + static_cast<size_t>(3) * g.nx * g.nb;  // [wp]
+    uint32_t* sxo = reinterpret_cast<uint32_t*>(sxf + wp);    // [wp] i0 * nb
+    const int64_t tile0 = img * g.ntile + static_cast<int64_t>(jbase) * g.nx;
+    const int ncur = nload * g.nx * g.nb;
+    for (int i = threadIdx.x; i < ncur; i += blockDim.x) cur[i] = s.curvef[tile0 * g.nb + i];
+    // column x = 16 gc + 4 q + r is stored at ((q * G + gc) * 4 + r), G = wp / 16: the
+    // lanes of a warp (consecutive groups gc) then read consecutive 16-byte vectors
+    const int64_t G = wp / kGrp;
+    for (int64_t x = threadIdx.x; x < wp; x += blockDim.x) {
+        const int64_t xc = imin64(x, g.w - 1);
+        const int64_t gc = x / kGrp, q = (x % kGrp) >> 2, r = x & 3;
+        const int64_t at = (q * G + gc) * 4 + r;
+        sxf[at] = s.xff[xc];
+        sxo[at] = static_cast<uint32_t>(s.xi[xc] * g.nb);
+    }
+    __syncthreads();
+    // identity tiles (NaN curves) are rare: the per-pixel NaN selects only run in
+    // blocks whose staged curve rows contain one
+    bool any_ident = false;
+    for (int i = threadIdx.x; i < nload * g.nx; i += blockDim.x) any_ident |= cur[i * g.nb] != cur[i * g.nb];
+    if (__syncthreads_or(any_ident)) apply_groups<kGray, true>(L, toned, gray, g, s, y0, y1, img, jbase, cur, sxf, sxo, G, vec);
+    else apply_groups<kGray, false>(L, toned, gray, g, s, y0, y1, img, jbase, cur, sxf, sxo, G, vec);
 }
 
 // ------------------------------------------------------------------ driver
