@@ -700,22 +700,17 @@ __global__ void __launch_bounds__(kT) hdr_fused_kernel(const float* __restrict__
 }
 
 // ---------------------------------------------------------------- host helpers
+// opt-in knobs are read per call (tests switch them within one process)
 bool fused_enabled() {
-    static const bool on = [] {
-        // opt-in (WG_HDR_FUSED=1): measured 157 vs 259 Gpix/s for the grouped
-        // schedule on C4 -- with ~7K px per CTA per image the per-image
-        // grid-wide dependency and table setup cost more than the 8 B/px saved
-        const char* e = getenv("WG_HDR_FUSED");
-        return e && e[0] == '1';
-    }();
-    return on;
+    // opt-in (WG_HDR_FUSED=1): measured 157 vs 259 Gpix/s for the grouped
+    // schedule on C4 -- with ~7K px per CTA per image the per-image
+    // grid-wide dependency and table setup cost more than the 8 B/px saved
+    const char* e = getenv("WG_HDR_FUSED");
+    return e && e[0] == '1';
 }
 size_t l2_budget() {
-    static size_t b = [] {
-        const char* e = getenv("WG_HDR_L2_BUDGET_MB");  // tuning knob (scripts/), default kL2Budget
-        return e ? static_cast<size_t>(atoll(e)) << 20 : kL2Budget;
-    }();
-    return b;
+    const char* e = getenv("WG_HDR_L2_BUDGET_MB");  // tuning knob (scripts/), default kL2Budget
+    return e ? static_cast<size_t>(atoll(e)) << 20 : kL2Budget;
 }
 int group_size(int64_t nimg, int64_t ppi) {
     const int64_t fit = static_cast<int64_t>(l2_budget() / (static_cast<size_t>(ppi) * sizeof(float)));

@@ -262,19 +262,23 @@ def test_hdr_c4_images(torch_dev):
     assert (hist > 0).sum() > 200  # log-range normalisation spreads the levels
 
 
-def test_hdr_tiled_tone_equals_grid_stride(torch_dev, monkeypatch):
-    """Regression: the bulk-copy tone kernel once raced (LDS in flight vs TMA refill)."""
+def test_hdr_schedules_agree(torch_dev, monkeypatch):
+    """The opt-in schedules equal the default bit for bit: the bulk-copy tone ring
+    (WG_HDR_TILED; it once raced: LDS in flight vs TMA refill) and the fused
+    persistent kernel (WG_HDR_FUSED)."""
     import paper_2108_13656_b200 as wg
     from paper_2108_13656_b200 import synth
 
     torch, dev = torch_dev
     rgb = torch.empty((3, 1024, 2048, 3), dtype=torch.float32, device=dev)
     synth.fill_hdr_f32(rgb, seed=9)
-    tiled = [wg.hdr_tonemap(rgb) for _ in range(3)]
-    monkeypatch.setenv("WG_HDR_NO_TILED", "1")
     plain = wg.hdr_tonemap(rgb)
-    for t in tiled:
-        assert torch.equal(t, plain)
+    monkeypatch.setenv("WG_HDR_TILED", "1")
+    for _ in range(3):
+        assert torch.equal(wg.hdr_tonemap(rgb), plain)
+    monkeypatch.delenv("WG_HDR_TILED")
+    monkeypatch.setenv("WG_HDR_FUSED", "1")
+    assert torch.equal(wg.hdr_tonemap(rgb), plain)
 
 
 def test_hdr_shard_invariance(torch_dev):
