@@ -352,12 +352,6 @@ __device__ __forceinline__ void tone_loop(const float* __restrict__ g, uint8_t* 
 }
 
 // table lookup of one pixel; r = 0 (black) falls in bin 0 whose count is 0
-__device__ __forceinline__ uint32_t lut_px(float v, float inv, const float2* s_lut) {
-    const float r = __fmul_rn(v, inv);
-    const uint32_t b = min(max(__float_as_uint(r) >> 17, 127u << 6), (127u << 6) + kLutBins - 1);
-    const float2 e = s_lut[b - (127u << 6)];
-    return static_cast<uint32_t>(__float_as_int(e.y)) + (r >= e.x ? 1u : 0u);
-}
 
 
 
