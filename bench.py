@@ -145,6 +145,17 @@ def cpu_port_rate(workload, seconds: float = 10.0, max_images: int = 4):
     return px / el / 1e9, threads, f"{desc}, repeated for {el:.1f} s ({px / 1e6:.0f} Mpx)"
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_sample(workload, n: int):
     """A bounded sample of the workload's input, generated on the host."""
     import numpy as np
@@ -279,9 +290,12 @@ def main():
         elapsed_ms = sum(a.elapsed_time(b) for a, b in evs)
 
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    per_rank = [elapsed_ms]
     if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    max_ms = float(t.item())
+        allt = torch.zeros(world, dtype=torch.float64, device=dev)
+        torch.distributed.all_gather_into_tensor(allt, t)
+        per_rank = allt.cpu().tolist()
+    max_ms = max(per_rank)
     px_step = n_img * wl.pix_per_image
     value = world * px_step * steps / (max_ms / 1e3) / 1e9
     ms_per_step = max_ms / steps
@@ -318,7 +332,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, sample = cpu_port_rate(wl, seconds=args.cpu_seconds)
-        cpu = {"value": round(v, 4), "unit": "Gpix/s", "cores": cores, "kind": "port", "sample": sample}
+        cpu = {"value": round(v, 4), "unit": "Gpix/s", "cores": cores, "kind": "port", "sample": sample,
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {
@@ -333,7 +348,11 @@ def main():
                        "l2": "inputs larger than L2, no flush" if flush is None else "L2 flushed between steps"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": steps * launches_per_step, "clocks": clk.summary(),
+            # each GPU's own rate next to the aggregate (SURVEY 8 e)
+            "per_gpu_gpix_s": [round(px_step * steps / (ms / 1e3) / 1e9, 2) for ms in per_rank],
         }
+        if wl.name == "C1":  # a single 512^2 image is latency-bound: report the latency (SURVEY 8 d)
+            line["latency_us_per_image"] = round(ms_per_step * 1e3 / n_img, 2)
         if methods:
             line["methods"] = methods
         if sweep:
@@ -497,7 +516,7 @@ def run_reference(args, wl, steps, warmup, world):
                    "images_per_gpu": wl.n_images, "height": wl.height, "width": wl.width,
                    "io": f"{wl.dtype}->{wl.output}"},
         "cpu_baseline": {"value": round(value, 4), "unit": "Gpix/s", "cores": threads, "kind": "port",
-                         "sample": desc + " per step"},
+                         "sample": desc + " per step", "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 4), "unit": "Gpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
