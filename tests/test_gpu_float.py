@@ -293,3 +293,31 @@ def test_hdr_shard_invariance(torch_dev):
     parts = torch.cat([wg.hdr_tonemap(rgb[i:i + 1]) for i in range(6)])
     assert torch.equal(whole, parts)
     assert int(whole[1].max()) == 0
+
+
+def test_plugin_rows_concurrent_threads():
+    """The reference's run_rows calls the plugin from a thread pool on disjoint row ranges
+    (backend.py:65-81); the CUDA plugin must give the same bytes under concurrency."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle
+    from paper_2108_13656_b200 import _kernels_cuda as k
+    from paper_2108_13656_b200.backend import run_rows
+
+    rgb = np.random.default_rng(21).random((257, 301, 3))
+    want = oracle.decolor_f64(rgb, threads=8)
+    for threads in (2, 5, 8):
+        out = np.full(rgb.shape[:2], -1.0)
+        run_rows(rgb.shape[0], threads, lambda r0, r1: k.decolor_rows(rgb, out, 0.55, 0.8, r0, r1))
+        assert out.tobytes() == want.tobytes()
+    # raw thread pool mixing three row kernels on one image
+    outs = {name: np.full(rgb.shape[:2], -1.0) for name in ("decolor", "bt601", "lab")}
+    fns = {"decolor": lambda o, a, b: k.decolor_rows(rgb, o, 0.55, 0.8, a, b),
+           "bt601": lambda o, a, b: k.bt601_rows(rgb, o, a, b),
+           "lab": lambda o, a, b: k.lab_lightness_rows(rgb, o, a, b)}
+    jobs = [(name, r0, min(r0 + 13, 257)) for name in fns for r0 in range(0, 257, 13)]
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        list(ex.map(lambda j: fns[j[0]](outs[j[0]], j[1], j[2]), jobs))
+    assert outs["decolor"].tobytes() == want.tobytes()
+    assert outs["bt601"].tobytes() == oracle.luma_f64(rgb, "y").tobytes()
+    assert np.abs(outs["lab"] - oracle.luma_f64(rgb, "lab")).max() <= 1e-12
