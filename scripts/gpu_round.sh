@@ -3,7 +3,7 @@
 # and a torchrun launch), and the ncu evidence (launch list + one full capture of
 # the hot kernel) for the C3 bench command.
 # Usage (from the repo root, under gpurun):  bash scripts/gpu_round.sh [tag]
-TAG=${1:-r01c}
+TAG=${1:-r01d}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/nvsmi_$TAG.txt 2>&1
