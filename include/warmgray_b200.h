@@ -112,6 +112,14 @@ WG_API int wg_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_o
 WG_API int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null, int64_t npix,
                        float beta_r, float beta_k, float midpoint, float slope, void* stream);
 
+/* Colour output of the global tone map on uint8: rgb_out = quantize_u8 of
+ * tonemap_image(mode="global")'s reinstated RGB (tonemap.py:172-216), toned /
+ * gray optional. Evaluates the reference's fp64 chain per pixel (the ratio
+ * l_out / l_in amplifies fp32 error past the parity bar): FP64-bound. */
+WG_API int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned_or_null,
+                                  uint8_t* gray_or_null, int64_t npix, double beta_r, double beta_k,
+                                  double midpoint, double slope, void* stream);
+
 /* Fused decolor + global tone map on fp32 RGB; gray_or_null gets the
  * untoned gray, rgb_out_or_null the reinstated colour (tonemap.py:172-192). */
 WG_API int wg_decolor_tone_f32(const float* rgb, float* toned, float* gray_or_null,
@@ -190,6 +198,9 @@ WG_API int wg_host_decolor_f32(const float* rgb, float* gray, int64_t npix, floa
 WG_API int wg_host_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null,
                             int64_t npix, float beta_r, float beta_k, float midpoint,
                             float slope, int device);
+WG_API int wg_host_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned_or_null,
+                                       uint8_t* gray_or_null, int64_t npix, double beta_r, double beta_k,
+                                       double midpoint, double slope, int device);
 WG_API int wg_host_sigmoid_f64(const double* lum, double* out, int64_t n, double midpoint, double slope,
                         int device);
 WG_API int wg_host_reinstate_f64(const double* rgb, const double* l_in, const double* l_out,

@@ -43,6 +43,7 @@ _SIGS = {
     "or_reinstate_f64": [_c_dp, _c_dp, _c_dp, _c_dp, _i64],
     "or_tone_u8": [_c_u8p, _c_u8p, _c_u8p, _i64, _d, _d, _d, _d, _i],
     "or_tonemap_global_f64": [_c_dp, _c_dp, _c_dp, _i64, _d, _d, _d, _d],
+    "or_tone_rgb_u8": [_c_u8p, _c_u8p, _c_u8p, _c_u8p, _i64, _d, _d, _d, _d, _i],
     "or_hdr_u8": [_c_fp, _c_u8p, _i64, _i64, _d, _d, _d, _d, _i],
     "or_synth_uniform_u8": [_c_u8p, _i64, _i64, ctypes.c_uint32, _i64],
     "or_synth_voronoi_u8": [_c_u8p, _i64, ctypes.c_int32, ctypes.c_int32, _c_i32p, _c_u8p,
@@ -207,6 +208,17 @@ def tone_u8(rgb: np.ndarray, beta_r=0.55, beta_k=0.8, midpoint=0.5, slope=8.0,
                      _ptr(gray, ctypes.c_uint8) if gray is not None else None,
                      toned.size, beta_r, beta_k, midpoint, slope, threads)
     return (toned, gray) if with_gray else toned
+
+
+def tone_rgb_u8(rgb: np.ndarray, beta_r=0.55, beta_k=0.8, midpoint=0.5, slope=8.0, threads: int = 1):
+    """(rgb_out, toned, gray) u8: quantize_u8 of tonemap_image(mode='global') on dequantize_u8(rgb)."""
+    rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
+    out = np.empty_like(rgb)
+    toned = np.empty(rgb.shape[:-1], dtype=np.uint8)
+    gray = np.empty_like(toned)
+    lib().or_tone_rgb_u8(_ptr(rgb, ctypes.c_uint8), _ptr(out, ctypes.c_uint8), _ptr(toned, ctypes.c_uint8),
+                         _ptr(gray, ctypes.c_uint8), toned.size, beta_r, beta_k, midpoint, slope, threads)
+    return out, toned, gray
 
 
 def tonemap_global_f64(rgb: np.ndarray, beta_r=0.55, beta_k=0.8, midpoint=0.5, slope=8.0):

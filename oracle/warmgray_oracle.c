@@ -355,6 +355,30 @@ OR_API void or_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray, int64_
     run_spans(npix, threads, tone8_span, &c);
 }
 
+/* u8 rgb -> u8 colour tone map: quantize_u8 of tonemap_image(mode="global")'s
+ * (rgb_out, l_out) on dequantize_u8(rgb) (tonemap.py:172-216, codec.py:22-29);
+ * toned / gray may be NULL. */
+typedef struct { const uint8_t* rgb; uint8_t* rgb_out; uint8_t* toned; uint8_t* gray; double br, bk; sig_t s; } tonergb_ctx;
+static void tonergb_span(void* c, int64_t p0, int64_t p1) {
+    tonergb_ctx* x = (tonergb_ctx*)c;
+    for (int64_t i = p0; i < p1; ++i) {
+        double r = dequantize(x->rgb[3 * i]), g = dequantize(x->rgb[3 * i + 1]), b = dequantize(x->rgb[3 * i + 2]);
+        double li = decolor_px(r, g, b, x->br, x->bk);
+        double lo = sig_apply(&x->s, li);
+        double ratio = lo / (li > 1e-6 ? li : 1e-6);
+        x->rgb_out[3 * i] = li == 0.0 ? 0 : quantize(clamp01(r * ratio));
+        x->rgb_out[3 * i + 1] = li == 0.0 ? 0 : quantize(clamp01(g * ratio));
+        x->rgb_out[3 * i + 2] = li == 0.0 ? 0 : quantize(clamp01(b * ratio));
+        if (x->toned) x->toned[i] = quantize(lo);
+        if (x->gray) x->gray[i] = quantize(li);
+    }
+}
+OR_API void or_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned, uint8_t* gray, int64_t npix,
+                           double beta_r, double beta_k, double midpoint, double slope, int threads) {
+    tonergb_ctx c = {rgb, rgb_out, toned, gray, beta_r, beta_k, sig_make(midpoint, slope)};
+    run_spans(npix, threads, tonergb_span, &c);
+}
+
 /* fp64 rgb -> (toned luminance, reinstated rgb): tonemap_image(mode="global")
  * (tonemap.py:195-216) = decolor -> apply_sigmoid -> reinstate_color. */
 OR_API void or_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_out, int64_t npix,

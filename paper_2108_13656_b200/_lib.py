@@ -59,6 +59,8 @@ SIGNATURES = {
     "wg_reinstate_f64": (_i, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "wg_tonemap_global_f64": (_i, [_vp, _vp, _vp, _i64, _d, _d, _d, _d, _vp]),
     "wg_decolor_tone_u8": (_i, [_vp, _vp, _vp, _i64, _f, _f, _f, _f, _vp]),
+    "wg_decolor_tone_rgb_u8": (_i, [_vp, _vp, _vp, _vp, _i64, _d, _d, _d, _d, _vp]),
+    "wg_host_decolor_tone_rgb_u8": (_i, [_vp, _vp, _vp, _vp, _i64, _d, _d, _d, _d, _i]),
     "wg_decolor_tone_f32": (_i, [_vp, _vp, _vp, _vp, _i64, _f, _f, _f, _f, _vp]),
     "wg_quantize_u8_f64": (_i, [_vp, _vp, _i64, _vp]),
     "wg_dequantize_u8_f64": (_i, [_vp, _vp, _i64, _vp]),

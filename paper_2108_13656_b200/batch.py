@@ -84,7 +84,9 @@ def decolor_tone(rgb, curve: SigmoidCurve = SigmoidCurve(), params: DecolorParam
                  return_gray: bool = False, return_rgb: bool = False, stream=None):
     """Fused decolor + global sigmoid on a device batch.
 
-    uint8 -> toned uint8 (and gray uint8 if ``return_gray``);
+    uint8 -> toned uint8 (and gray uint8 if ``return_gray``; with
+    ``return_rgb`` also the reinstated colour image as uint8, i.e.
+    quantize_u8 of tonemap_image(mode="global")[0], via the fp64 chain);
     float32 -> toned float32 (+ gray, + reinstated rgb if requested).
     Returns the toned tensor, or a tuple ``(toned, gray, rgb_out)`` with
     ``None`` for outputs not requested when either flag is set.
@@ -97,9 +99,13 @@ def decolor_tone(rgb, curve: SigmoidCurve = SigmoidCurve(), params: DecolorParam
     rgb_out = None
     with torch.cuda.device(rgb.device):
         st = _stream(stream, rgb.device)
-        if name == "uint8":
-            if return_rgb:
-                raise ValueError("return_rgb is supported for float32 input only")
+        if name == "uint8" and return_rgb:
+            # colour output: the reference's fp64 chain per pixel (wg_decolor_tone_rgb_u8)
+            rgb_out = torch.empty_like(rgb)
+            _lib.call("wg_decolor_tone_rgb_u8", rgb.data_ptr(), rgb_out.data_ptr(), toned.data_ptr(),
+                      gray.data_ptr() if gray is not None else None, toned.numel(), params.beta_r, params.beta_k,
+                      curve.midpoint, curve.slope, st)
+        elif name == "uint8":
             _lib.call("wg_decolor_tone_u8", rgb.data_ptr(), toned.data_ptr(),
                       gray.data_ptr() if gray is not None else None, toned.numel(),
                       params.beta_r, params.beta_k, curve.midpoint, curve.slope, st)
@@ -295,16 +301,27 @@ def decolor_tone_local_host(rgb, grid=None, params: DecolorParams = DEFAULT_PARA
 
 def decolor_tone_host(rgb, curve: SigmoidCurve = SigmoidCurve(),
                       params: DecolorParams = DEFAULT_PARAMS, return_gray: bool = False,
-                      device: int | None = None):
-    """Fused decolor + global sigmoid of a host uint8 (..., 3) array -> toned uint8 (+ gray)."""
+                      device: int | None = None, return_rgb: bool = False):
+    """Fused decolor + global sigmoid of a host uint8 (..., 3) array -> toned uint8 (+ gray).
+
+    With ``return_rgb`` returns ``(toned, gray, rgb_out)`` (gray None unless
+    requested), rgb_out the reinstated colour image as uint8.
+    """
     arr = _host_rgb(rgb, ("uint8",))
     toned = np.empty(arr.shape[:-1], dtype=np.uint8)
     gray = np.empty_like(toned) if return_gray else None
-    if toned.size:
+    rgb_out = np.empty_like(arr) if return_rgb else None
+    dev = get_device() if device is None else device
+    if toned.size and return_rgb:
+        _lib.call("wg_host_decolor_tone_rgb_u8", arr.ctypes.data, rgb_out.ctypes.data, toned.ctypes.data,
+                  gray.ctypes.data if gray is not None else None, toned.size, params.beta_r,
+                  params.beta_k, curve.midpoint, curve.slope, dev)
+    elif toned.size:
         _lib.call("wg_host_decolor_tone_u8", arr.ctypes.data, toned.ctypes.data,
                   gray.ctypes.data if gray is not None else None, toned.size, params.beta_r,
-                  params.beta_k, curve.midpoint, curve.slope,
-                  get_device() if device is None else device)
+                  params.beta_k, curve.midpoint, curve.slope, dev)
+    if return_rgb:
+        return toned, gray, rgb_out
     return (toned, gray) if return_gray else toned
 
 

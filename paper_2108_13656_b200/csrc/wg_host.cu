@@ -383,6 +383,23 @@ extern "C" int wg_host_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8
                          });
 }
 
+extern "C" int wg_host_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned_or_null,
+                                           uint8_t* gray_or_null, int64_t npix, double beta_r, double beta_k,
+                                           double midpoint, double slope, int device) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, rgb_out) || check_params(beta_r, beta_k) ||
+                  check_curve(midpoint, slope));
+    HostIn in[1] = {{rgb, 3}};
+    HostOut o[3] = {{rgb_out, 3}, {toned_or_null, 1}, {gray_or_null, 1}};
+    return host_pipeline(device, npix, in, 1, o, 3, 256, no_scratch,
+                         [&](const void** di, void** dout, void*, int64_t n, cudaStream_t st) {
+                             return wg_decolor_tone_rgb_u8(static_cast<const uint8_t*>(di[0]),
+                                                           static_cast<uint8_t*>(dout[0]),
+                                                           static_cast<uint8_t*>(dout[1]),
+                                                           static_cast<uint8_t*>(dout[2]), n, beta_r, beta_k,
+                                                           midpoint, slope, st);
+                         });
+}
+
 extern "C" int wg_host_sigmoid_f64(const double* lum, double* out, int64_t n, double midpoint,
                                    double slope, int device) {
     WG_CHECK_ARGS(check_npix(n) || check_ptrs(n, lum, out) || check_curve(midpoint, slope));

@@ -18,6 +18,7 @@
 // within the fp32 error of a threshold or a rounding boundary can differ).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -217,10 +218,55 @@ int tone_table(double m, double k, const ToneTable** out, bool* multi) {
     return WG_OK;
 }
 
+// Colour output (tonemap_image(mode="global")'s rgb_out, tonemap.py:172-216):
+// rgb_out_c = quantize_u8(clip(c * l_out / max(l_in, 1e-6))), 0 where l_in == 0.
+// The ratio l_out / l_in amplifies any error of a fast fp32 route into the
+// rounding of every channel (~5e-4 of channels at +-1, above the bar), so this
+// kernel evaluates the reference's fp64 chain per pixel (decolor_f64, logistic
+// with exp, IEEE division): FP64-bound, bit-identical to the oracle.
+__global__ void __launch_bounds__(256) tone_rgb_u8_kernel(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ rgb_out,
+                                                          uint8_t* __restrict__ toned, uint8_t* __restrict__ gray,
+                                                          int64_t npix, double br, double bk, SigD sig) {
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npix;
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double r = deq_byte(rgb[3 * p]), g = deq_byte(rgb[3 * p + 1]), b = deq_byte(rgb[3 * p + 2]);
+        const double li = decolor_f64(r, g, b, br, bk);
+        const double lo = sigmoid_d(li, sig);
+        const double ratio = __ddiv_rn(lo, li > 1e-6 ? li : 1e-6);
+        const bool black = li == 0.0;
+        rgb_out[3 * p] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(r, ratio)));
+        rgb_out[3 * p + 1] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(g, ratio)));
+        rgb_out[3 * p + 2] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(b, ratio)));
+        if (toned) toned[p] = static_cast<uint8_t>(quantize_d(lo));
+        if (gray) gray[p] = static_cast<uint8_t>(quantize_d(li));
+    }
+}
+
 }  // namespace
 }  // namespace wg
 
 using namespace wg;
+
+extern "C" int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned_or_null,
+                                      uint8_t* gray_or_null, int64_t npix, double beta_r, double beta_k,
+                                      double midpoint, double slope, void* stream) {
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, rgb_out) || check_params(beta_r, beta_k) ||
+                  check_curve(midpoint, slope));
+    if (npix == 0) return WG_OK;
+    int device = 0;
+    cudaGetDevice(&device);
+    const unsigned blocks = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>((npix + 255) / 256, 16LL * sm_count(device))));
+    // the curve's constants, as apply_sigmoid forms them (tonemap.py:76-80)
+    SigD sig;
+    sig.m = midpoint;
+    sig.k = slope;
+    sig.lo = 1.0 / (1.0 + std::exp(slope * midpoint));
+    sig.hi = 1.0 / (1.0 + std::exp(-slope * (1.0 - midpoint)));
+    tone_rgb_u8_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(rgb, rgb_out, toned_or_null,
+                                                                             gray_or_null, npix, beta_r, beta_k, sig);
+    return check_launch("tone_rgb_u8");
+}
 
 extern "C" int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null, int64_t npix,
                                   float beta_r, float beta_k, float midpoint, float slope, void* stream) {

@@ -35,6 +35,9 @@ into this repository; only the outputs below are committed:
   metrics.npz/json    _sweep_counts / evaluate / ccpr / ccfr / write_sweep_csv of
                       the reference on seeded image pairs (exhaustive and
                       sampled pair sets, several gray methods)
+  tone_rgb.npz        quantize_u8 of tonemap_image(mode="global") colour and
+                      luminance outputs on uint8 images (default and custom
+                      parameters, black and very dark pixels)
   colorspaces.json    scalar known answers (luma_weighted, hsv_v, rgb_to_lab,
                       lab_lightness, delta_e76) and sha256 of the u8 cube
                       through luminance_image for y / v / lab
@@ -214,7 +217,27 @@ def main() -> None:
     lhe_golden(wg)
     codec_golden(wg)
     metrics_golden(wg)
+    tone_rgb_golden(wg)
     print("golden fixtures written to", HERE)
+
+
+def tone_rgb_golden(wg) -> None:
+    """uint8 colour output of the global tone map: quantize_u8 of tonemap_image(mode="global")."""
+    rng = np.random.default_rng(2112)
+    u8 = rng.integers(0, 256, (2, 40, 56, 3), dtype=np.uint8)
+    u8[0, 0, :8] = 0      # black pixels (l_in == 0 -> 0)
+    u8[1, :4] = 3         # very dark pixels (ratio amplifies)
+    out = {"u8": u8}
+    for tag, curve, params in (("default", wg.SigmoidCurve(), wg.DEFAULT_PARAMS),
+                               ("custom", wg.SigmoidCurve(0.3, 12.0), wg.DecolorParams(0.7, 0.9))):
+        rgb_o, toned = [], []
+        for im in u8:
+            r, lo = wg.tonemap_image(wg.PlanarImage(wg.dequantize_u8(im)), mode="global", params=params, curve=curve)
+            rgb_o.append(wg.quantize_u8(r.data))
+            toned.append(wg.quantize_u8(lo.data))
+        out[f"{tag}_rgb"] = np.stack(rgb_o)
+        out[f"{tag}_toned"] = np.stack(toned)
+    np.savez_compressed(os.path.join(HERE, "tone_rgb.npz"), **out)
 
 
 def metrics_golden(wg) -> None:
@@ -396,6 +419,12 @@ def colorspaces_golden(wg, get_kernels) -> None:
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["tone_rgb"]:
+        sys.path.insert(0, build_reference())
+        import warmgray as _wg
+
+        tone_rgb_golden(_wg)
+        sys.exit(0)
     if sys.argv[1:] == ["metrics"]:
         sys.path.insert(0, build_reference())
         import warmgray as _wg

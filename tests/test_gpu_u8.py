@@ -242,6 +242,35 @@ def test_tone_u8_cube(torch_dev, cube):
         assert torch.equal(wg.decolor_tone(t, wg.SigmoidCurve(m, k)), toned)
 
 
+def test_tone_rgb_u8_golden_and_cube(torch_dev, cube):
+    """Colour output of the global tone map: bit-identical (fp64 chain per pixel)."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+
+    torch, dev = torch_dev
+    g = np.load(os.path.join(GOLDEN, "tone_rgb.npz"))
+    t = torch.from_numpy(g["u8"]).to(dev)
+    for tag, curve, params in (("default", wg.SigmoidCurve(), wg.DEFAULT_PARAMS),
+                               ("custom", wg.SigmoidCurve(0.3, 12.0), wg.DecolorParams(0.7, 0.9))):
+        toned, _, out = wg.decolor_tone(t, curve, params, return_rgb=True)
+        assert np.array_equal(out.cpu().numpy(), g[f"{tag}_rgb"])
+        assert np.array_equal(toned.cpu().numpy(), g[f"{tag}_toned"])
+    t = torch.from_numpy(cube).to(dev)
+    for m, k in [(0.5, 8.0), (0.6, 2000.0), (0.0, 3.0)]:
+        toned, gray, out = wg.decolor_tone(t, wg.SigmoidCurve(m, k), return_gray=True, return_rgb=True)
+        want_o, want_t, want_g = oracle.tone_rgb_u8(cube, midpoint=m, slope=k, threads=oracle.default_threads())
+        n_o = int((out.cpu().numpy() != want_o).sum())
+        n_t = int((toned.cpu().numpy() != want_t).sum())
+        n_g = int((gray.cpu().numpy() != want_g).sum())
+        print(f"tone rgb cube m={m} k={k}: rgb diffs {n_o} toned diffs {n_t} gray diffs {n_g}")
+        assert n_o == n_t == n_g == 0
+    # host-buffer entry point, ragged size
+    h = cube[: 1000003]
+    toned, gray, out = wg.decolor_tone_host(h, return_gray=True, return_rgb=True)
+    want_o, want_t, want_g = oracle.tone_rgb_u8(h)
+    assert np.array_equal(out, want_o) and np.array_equal(toned, want_t) and np.array_equal(gray, want_g)
+
+
 def test_empty_and_errors(torch_dev):
     import paper_2108_13656_b200 as wg
 

@@ -127,6 +127,14 @@ def test_tonemap_global_matches_reference():
     assert np.abs(rgb_out - g["rgb_out2"]).max() <= 1e-15
 
 
+def test_tone_rgb_u8_matches_reference():
+    g = _npz("tone_rgb.npz")
+    out, toned, _ = oracle.tone_rgb_u8(g["u8"])
+    assert np.array_equal(out, g["default_rgb"]) and np.array_equal(toned, g["default_toned"])
+    out, toned, _ = oracle.tone_rgb_u8(g["u8"], 0.7, 0.9, 0.3, 12.0, threads=2)
+    assert np.array_equal(out, g["custom_rgb"]) and np.array_equal(toned, g["custom_toned"])
+
+
 def test_hdr_adapter_matches_reference_operators():
     """The HDR restatement equals decolor_image(x/max) -> log-range -> apply_sigmoid -> quantize_u8."""
     g = _npz("hdr.npz")
