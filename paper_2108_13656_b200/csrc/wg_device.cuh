@@ -481,7 +481,8 @@ __device__ __forceinline__ double decolor_f64(double r, double g, double b, doub
 // as one FMA correction of k * fl(1/255) (checked exhaustively against IEEE
 // division over k = 0..255).
 __device__ __forceinline__ double deq_byte(uint32_t k) {
-    const double inv = 1.0 / 255.0, x = static_cast<double>(k);
+    // (double)k exactly, as 2^52 + k minus 2^52 (a DADD instead of an XU-pipe I2F.F64)
+    const double inv = 1.0 / 255.0, x = __hiloint2double(0x43300000, static_cast<int>(k)) - 4503599627370496.0;
     const double q0 = __dmul_rn(x, inv);
     return __fma_rn(__fma_rn(-q0, 255.0, x), inv, q0);
 }

@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -218,28 +219,342 @@ int tone_table(double m, double k, const ToneTable** out, bool* multi) {
     return WG_OK;
 }
 
-// Colour output (tonemap_image(mode="global")'s rgb_out, tonemap.py:172-216):
-// rgb_out_c = quantize_u8(clip(c * l_out / max(l_in, 1e-6))), 0 where l_in == 0.
-// The ratio l_out / l_in amplifies any error of a fast fp32 route into the
-// rounding of every channel (~5e-4 of channels at +-1, above the bar), so this
-// kernel evaluates the reference's fp64 chain per pixel (decolor_f64, logistic
-// with exp, IEEE division): FP64-bound, bit-identical to the oracle.
+// ---------------------------------------------------------------- colour output
+// tonemap_image(mode="global")'s rgb_out on uint8 (tonemap.py:172-216):
+// rgb_out_c = quantize_u8(clip(c * l_out / max(l_in, 1e-6))), 0 where l_in == 0;
+// toned = quantize_u8(l_out), gray = quantize_u8(l_in).
+//
+// The ratio l_out / l_in amplifies fp32 error into the rounding of every
+// channel, so bit-identity needs the reference's fp64 chain wherever an output
+// byte is in doubt -- and only there. The fast kernel evaluates the chain in
+// packed fp32 (two pixels per f32x2 op) on MUFU approximations, together with
+// a per-pixel bound `rel` on the relative error of the output values. Each
+// byte is settled by two FFMAs, lo = RN(v (1 - rel) + 2^23) and
+// hi = RN(v (1 + rel) + 2^23): if they agree, every value within the bound
+// rounds to the same byte (the low byte of lo). A pixel with any
+// disagreement (sum of hi - lo over its outputs != 0) is queued in shared
+// memory, one queue per warp (pixel index; lanes append at a shuffle prefix
+// sum; the queue holds a whole warp-tile on top of the drain threshold, so it
+// cannot overflow), and the warp drains it through the fp64 chain
+// (tone_rgb_px) once 32 are waiting -- all lanes busy, and no block barrier
+// anywhere in the loop. ~1% of pixels take the fp64 route at the default
+// curve. Bit-identical to the reference by construction.
+//
+// fp32 chain, in the 0..255 domain (decolor is homogeneous of degree 1) and
+// pre-scaled by sqrt(3) (white' = sqrt(3) white etc.), with bytes R, G, B:
+//   white' = sqrt(R^2+G^2+B^2), rg' = sqrt(3 br R^2 + 3 (1-br) G^2),
+//   W' = R rg' + (G+B) white', C' = B (sqrt(3) (R+G) + white'), s = R+G+B
+//   Qn = (bk/3) W'^2 + ((1-bk)/3) C'^2, q = rsqrt(Qn s^2),
+//   L = 255 l_in = Qn q = sqrt(Qn)/s, 1/L = s^2 q   (one MUFU for both)
+//   (warm = W'/(sqrt(3) s), cool = C'/(sqrt(3) s))
+// (black: Qn gets +1e-30 and s is floored at 1, so L = 1e-15 and every
+// output value is 0 without a branch; l_in == 0 only for black with betas in
+// (0.5, 1)). Logistic difference in product form (no cancellation at small k):
+//   N(x) = (sig(k(x-m)) - sig(-km)) / (sig(k(1-m)) - sig(-km))
+//        = sig(t) (1 - e^{-kx}) / (sig(k(1-m)) (1 - e^{-k})),  t = k(x-m)
+//   e^{-kx} = 2^y, y = -kx log2(e); e^{-t} = 2^y e^{km} (one ex2) for k <= 80,
+//   2^{y + km log2 e} (a second ex2) beyond; 1 - 2^y by a degree-6 series in
+//   y for kx < 1/4 (evaluated only by warps that hold such a pixel).
+// Error bound (u = 2^-24; MUFU ex2/rsqrt/sqrt/rcp <= 2.5 u measured
+// exhaustively on the B200 by scripts/mufu_error.cu, budgeted at 4 u each;
+// first-order sums along the chain, budgets rounded up):
+//   rel(L), rel(1/L) <= 14 u (budget 24 u);
+//   rel(e^{-t}) <= 6u + kx (rel(L) + 2u)          (one-ex2 form)
+//              <= 4u + 2 km u + kx (rel(L) + 3u)   (two-ex2 form)
+//   rel(1 - e^{-kx}) <= 42 u;  rel(N) <= omS rel(e^{-t}) + 50 u + ref
+//     with omS = 1 - sig(t) (the logistic's own conditioning) and ref the
+//     reference's fp64 error (1e-13 + 4e-16 / D + 1e-15 k, D = hi - lo);
+//   rgb v_c = R N 255 / L: rel(N) + rel(1/L) + 2u (+2u for the scale
+//     constants) + the reference's absolute y - lo error folded in relative
+//     form (v >= 0.4 where it matters: 1.1e-10 / (0.4 D)); the toned value
+//     255 N shares the rgb scales (a wider margin than it needs).
+// A wide margin is never wrong, only slower (more pairs take the fp64 chain).
+// Curves with k < 1e-3 or k > 1e4 run the fp64 kernel for every pixel.
+struct ToneRgbF {
+    float br3, br13, bk3, bk13;  // 3 br, 3 (1-br), bk/3, (1-bk)/3
+    float nak;      // -k log2(e) / 255: y = L nak, e^{-kx} = 2^y
+    float ekm;      // e^{km} (one-ex2 form)
+    float tc;       // k m log2(e): e^{-t} = 2^{y + tc} (two-ex2 form)
+    float ycut;     // -0.25 log2(e): the series below |y| < |ycut| (kx < 1/4)
+    float cn255;    // 255 / (sig(k(1-m)) (1 - e^{-k}))
+    float cA, cC, cD;  // rel(N) <= omS (L cA + cC) + cD
+    float relRgb;      // rel(v_rgb) = rel(N) + relRgb (toned uses the same)
+    float glo, ghi;    // gray scales 1 -/+ rel(L)
+};
+
+__device__ __forceinline__ float ex2_mufu(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_mufu(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float2 sqrt2_mufu(float2 x) { return make_float2(sqrt_mufu(x.x), sqrt_mufu(x.y)); }
+__device__ __forceinline__ float2 rsqrt2_mufu(float2 x) { return make_float2(rsqrt_mufu(x.x), rsqrt_mufu(x.y)); }
+__device__ __forceinline__ float2 rcp2_mufu(float2 x) { return make_float2(rcp_mufu(x.x), rcp_mufu(x.y)); }
+__device__ __forceinline__ float2 ex22_mufu(float2 x) { return make_float2(ex2_mufu(x.x), ex2_mufu(x.y)); }
+// the low bytes of a, b, c, d as one word
+__device__ __forceinline__ uint32_t pack4(float a, float b, float c, float d) {
+    return __byte_perm(__byte_perm(__float_as_uint(a), __float_as_uint(b), 0x0040u),
+                       __byte_perm(__float_as_uint(c), __float_as_uint(d), 0x0040u), 0x5410u);
+}
+// hi - lo as integers: 0 when both round to the same byte, else the count of crossed boundaries
+__device__ __forceinline__ void crossed(float2 lo, float2 hi, uint32_t& x0, uint32_t& x1) {
+    x0 += __float_as_uint(hi.x) - __float_as_uint(lo.x);
+    x1 += __float_as_uint(hi.y) - __float_as_uint(lo.y);
+}
+
+// the reference's fp64 chain for one pixel (also the unaligned / tail path)
+static __device__ __noinline__ void tone_rgb_px(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ rgb_out,
+                                                uint8_t* __restrict__ toned, uint8_t* __restrict__ gray, int64_t p,
+                                                double br, double bk, double m, double k, double lo, double hi) {
+    SigD sig;
+    sig.m = m;
+    sig.k = k;
+    sig.lo = lo;
+    sig.hi = hi;
+    const double r = deq_byte(rgb[3 * p]), g = deq_byte(rgb[3 * p + 1]), b = deq_byte(rgb[3 * p + 2]);
+    const double li = decolor_f64(r, g, b, br, bk);
+    const double lout = sigmoid_d(li, sig);
+    const double ratio = __ddiv_rn(lout, li > 1e-6 ? li : 1e-6);
+    const bool black = li == 0.0;
+    rgb_out[3 * p] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(r, ratio)));
+    rgb_out[3 * p + 1] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(g, ratio)));
+    rgb_out[3 * p + 2] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(b, ratio)));
+    if (toned) toned[p] = static_cast<uint8_t>(quantize_d(lout));
+    if (gray) gray[p] = static_cast<uint8_t>(quantize_d(li));
+}
+
 __global__ void __launch_bounds__(256) tone_rgb_u8_kernel(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ rgb_out,
                                                           uint8_t* __restrict__ toned, uint8_t* __restrict__ gray,
                                                           int64_t npix, double br, double bk, SigD sig) {
     for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npix;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double r = deq_byte(rgb[3 * p]), g = deq_byte(rgb[3 * p + 1]), b = deq_byte(rgb[3 * p + 2]);
-        const double li = decolor_f64(r, g, b, br, bk);
-        const double lo = sigmoid_d(li, sig);
-        const double ratio = __ddiv_rn(lo, li > 1e-6 ? li : 1e-6);
-        const bool black = li == 0.0;
-        rgb_out[3 * p] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(r, ratio)));
-        rgb_out[3 * p + 1] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(g, ratio)));
-        rgb_out[3 * p + 2] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(b, ratio)));
-        if (toned) toned[p] = static_cast<uint8_t>(quantize_d(lo));
-        if (gray) gray[p] = static_cast<uint8_t>(quantize_d(li));
+         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        tone_rgb_px(rgb, rgb_out, toned, gray, p, br, bk, sig.m, sig.k, sig.lo, sig.hi);
+}
+
+constexpr int kRgbPx = 16;                            // pixels per thread per tile (48 input bytes)
+constexpr int kRgbTile = 256 * kRgbPx;                // 4096 pixels per tile
+constexpr int kQueueDrain = 32;                       // a warp drains once a warp's worth is queued
+constexpr int kQueueCap = kQueueDrain + 32 * kRgbPx;  // < kQueueDrain carried + one tile of the warp
+
+// One pixel pair through the fp32 chain: settled bytes (lo values) and each
+// pixel's crossed-boundary count (0: all its bytes settled).
+struct PairOut {
+    float2 r, g, b, t, y;
+    uint32_t crossed0, crossed1;
+};
+template <bool kTwoEx2, bool kToned, bool kGray>
+__device__ __forceinline__ PairOut tone_rgb_pair(float2 R, float2 G, float2 B, const ToneRgbF& c) {
+    const float2 M2 = bc2(kMagic), one2 = bc2(1.0f);
+    // decolor
+    const float2 R2 = mul2(R, R), G2 = mul2(G, G);
+    const float2 white = sqrt2_mufu(fma2(B, B, add2(R2, G2)));
+    const float2 rg = sqrt2_mufu(fma2(R2, bc2(c.br3), mul2(G2, bc2(c.br13))));
+    const float2 RG = add2(R, G);
+    const float2 s = add2(RG, B);
+    const float2 W = fma2(R, rg, mul2(add2(G, B), white));
+    const float2 C = mul2(B, fma2(RG, bc2(1.7320508075688772f), white));
+    const float2 Qn = fma2(mul2(W, bc2(c.bk3)), W, fma2(mul2(C, bc2(c.bk13)), C, bc2(1e-30f)));
+    const float2 s1 = make_float2(fmaxf(s.x, 1.0f), fmaxf(s.y, 1.0f));
+    const float2 ss = mul2(s1, s1);                     // exact (s <= 765)
+    const float2 q = rsqrt2_mufu(mul2(Qn, ss));         // 1 / (s sqrt(Qn))
+    const float2 L = mul2(Qn, q);                       // sqrt(Qn) / s
+    const float2 invL = mul2(ss, q);                    // s / sqrt(Qn)
+    // logistic difference
+    const float2 y = mul2(L, bc2(c.nak));  // -kx log2(e)
+    const float2 E = ex22_mufu(y);
+    const float2 eT = kTwoEx2 ? ex22_mufu(add2(y, bc2(c.tc))) : mul2(E, bc2(c.ekm));
+    const float2 sg = rcp2_mufu(add2(eT, one2));
+    float2 omS = mul2(eT, sg);
+    if constexpr (kTwoEx2) omS = make_float2(fminf(omS.x, 1.0f), fminf(omS.y, 1.0f));  // inf * 0
+    float2 omE = fma2(E, bc2(-1.0f), one2);
+    if (__any_sync(0xFFFFFFFFu, fminf(y.x, y.y) > c.ycut)) {
+        // 1 - 2^y = sum_n -(y ln2)^n / n!, n = 1..6
+        constexpr float l1 = 0.6931471805599453f, l2 = 0.2402265069591007f, l3 = 0.0555041086648216f,
+                        l4 = 0.0096181291076285f, l5 = 0.0013333558146428f, l6 = 0.0001540353039338f;
+        const float2 ser =
+            mul2(y, fma2(y, fma2(y, fma2(y, fma2(y, fma2(y, bc2(-l6), bc2(-l5)), bc2(-l4)), bc2(-l3)), bc2(-l2)),
+                         bc2(-l1)));
+        omE.x = y.x > c.ycut ? ser.x : omE.x;
+        omE.y = y.y > c.ycut ? ser.y : omE.y;
     }
+    const float2 N255 = mul2(mul2(sg, omE), bc2(c.cn255));
+    // error bound -> one scale pair for the rgb and toned values
+    const float2 relC = fma2(omS, fma2(L, bc2(c.cA), bc2(c.cC)), bc2(c.cD + c.relRgb));
+    const float2 cl = fma2(relC, bc2(-1.0f), one2), ch = add2(relC, one2);
+    // outputs
+    const float2 rs = mul2(N255, invL);
+    const float2 vR = mul2(R, rs), vG = mul2(G, rs), vB = mul2(B, rs);
+    const float2 vr = make_float2(fminf(vR.x, 255.0f), fminf(vR.y, 255.0f));
+    const float2 vg = make_float2(fminf(vG.x, 255.0f), fminf(vG.y, 255.0f));
+    const float2 vb = make_float2(fminf(vB.x, 255.0f), fminf(vB.y, 255.0f));
+    PairOut o;
+    o.r = fma2(vr, cl, M2);
+    o.g = fma2(vg, cl, M2);
+    o.b = fma2(vb, cl, M2);
+    uint32_t x0 = 0, x1 = 0;
+    crossed(o.r, fma2(vr, ch, M2), x0, x1);
+    crossed(o.g, fma2(vg, ch, M2), x0, x1);
+    crossed(o.b, fma2(vb, ch, M2), x0, x1);
+    if constexpr (kToned) {
+        o.t = fma2(N255, cl, M2);
+        crossed(o.t, fma2(N255, ch, M2), x0, x1);
+    }
+    if constexpr (kGray) {
+        o.y = fma2(L, bc2(c.glo), M2);
+        crossed(o.y, fma2(L, bc2(c.ghi), M2), x0, x1);
+    }
+    o.crossed0 = x0;
+    o.crossed1 = x1;
+    return o;
+}
+
+template <bool kTwoEx2, bool kToned, bool kGray>
+__global__ void __launch_bounds__(256, 3)
+    tone_rgb_fast_kernel(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ rgb_out,
+                         uint8_t* __restrict__ toned, uint8_t* __restrict__ gray, int64_t ntiles, int64_t npix,
+                         ToneRgbF c, double br, double bk, SigD sig) {
+    __shared__ int64_t queues[8][kQueueCap];  // one per warp: appends and drains need only __syncwarp
+    const int tid = threadIdx.x, lane = tid & 31;
+    int64_t* queue = queues[tid >> 5];
+    int qn = 0;  // warp-uniform queue length
+    const int64_t stride = gridDim.x;
+    int64_t t = blockIdx.x;
+    uint4 v[3];
+    if (t < ntiles) {
+        const uint4* p = reinterpret_cast<const uint4*>(rgb + t * (kRgbTile * 3)) + tid * 3;
+        v[0] = __ldcs(p);
+        v[1] = __ldcs(p + 1);
+        v[2] = __ldcs(p + 2);
+    }
+    for (; t < ntiles; t += stride) {
+        uint4 nx[3] = {v[0], v[1], v[2]};
+        if (t + stride < ntiles) {
+            const uint4* q = reinterpret_cast<const uint4*>(rgb + (t + stride) * (kRgbTile * 3)) + tid * 3;
+            nx[0] = __ldcs(q);
+            nx[1] = __ldcs(q + 1);
+            nx[2] = __ldcs(q + 2);
+        }
+        const uint32_t w[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y,
+                                v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
+        uint32_t o[12], ot[4], og[4];
+        uint32_t mask = 0;  // bit i: pixel i needs the fp64 chain
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            // pixels 4q..4q+3 = words 3q..3q+2: R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3
+            const uint32_t w0 = w[3 * q], w1 = w[3 * q + 1], w2 = w[3 * q + 2];
+            const float2 mM = bc2(-kMagic);
+            const float2 RA = add2(make_float2(byte_biased(w0, 0), byte_biased(w0, 3)), mM);
+            const float2 GA = add2(make_float2(byte_biased(w0, 1), byte_biased(w1, 0)), mM);
+            const float2 BA = add2(make_float2(byte_biased(w0, 2), byte_biased(w1, 1)), mM);
+            const float2 RB = add2(make_float2(byte_biased(w1, 2), byte_biased(w2, 1)), mM);
+            const float2 GB = add2(make_float2(byte_biased(w1, 3), byte_biased(w2, 2)), mM);
+            const float2 BB = add2(make_float2(byte_biased(w2, 0), byte_biased(w2, 3)), mM);
+            const PairOut a = tone_rgb_pair<kTwoEx2, kToned, kGray>(RA, GA, BA, c);
+            const PairOut b = tone_rgb_pair<kTwoEx2, kToned, kGray>(RB, GB, BB, c);
+            o[3 * q] = pack4(a.r.x, a.g.x, a.b.x, a.r.y);
+            o[3 * q + 1] = pack4(a.g.y, a.b.y, b.r.x, b.g.x);
+            o[3 * q + 2] = pack4(b.b.x, b.r.y, b.g.y, b.b.y);
+            if constexpr (kToned) ot[q] = pack4(a.t.x, a.t.y, b.t.x, b.t.y);
+            if constexpr (kGray) og[q] = pack4(a.y.x, a.y.y, b.y.x, b.y.y);
+            mask |= (a.crossed0 ? 1u : 0u) << (4 * q);
+            mask |= (a.crossed1 ? 1u : 0u) << (4 * q + 1);
+            mask |= (b.crossed0 ? 1u : 0u) << (4 * q + 2);
+            mask |= (b.crossed1 ? 1u : 0u) << (4 * q + 3);
+        }
+        const int64_t p0 = t * kRgbTile + static_cast<int64_t>(tid) * kRgbPx;
+        uint4* orgb = reinterpret_cast<uint4*>(rgb_out + p0 * 3);
+        __stcs(orgb, make_uint4(o[0], o[1], o[2], o[3]));
+        __stcs(orgb + 1, make_uint4(o[4], o[5], o[6], o[7]));
+        __stcs(orgb + 2, make_uint4(o[8], o[9], o[10], o[11]));
+        if constexpr (kToned) __stcs(reinterpret_cast<uint4*>(toned + p0), make_uint4(ot[0], ot[1], ot[2], ot[3]));
+        if constexpr (kGray) __stcs(reinterpret_cast<uint4*>(gray + p0), make_uint4(og[0], og[1], og[2], og[3]));
+        if (__any_sync(0xFFFFFFFFu, mask != 0u)) {
+            // exclusive prefix of the lanes' pixel counts -> each lane's slots
+            const int cnt = __popc(mask);
+            int pre = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+                if (lane >= d) pre += x;
+            }
+            int slot = qn + pre - cnt;
+            for (uint32_t mm = mask; mm; mm &= mm - 1) queue[slot++] = p0 + (__ffs(mm) - 1);
+            qn += __shfl_sync(0xFFFFFFFFu, pre, 31);
+            __syncwarp();  // appends and this tile's provisional stores before the drain
+            if (qn >= kQueueDrain) {
+                for (int j = lane; j < qn; j += 32)
+                    tone_rgb_px(rgb, rgb_out, toned, gray, queue[j], br, bk, sig.m, sig.k, sig.lo, sig.hi);
+                qn = 0;
+                __syncwarp();  // queue reads before the next appends
+            }
+        }
+        v[0] = nx[0];
+        v[1] = nx[1];
+        v[2] = nx[2];
+    }
+    for (int j = lane; j < qn; j += 32)
+        tone_rgb_px(rgb, rgb_out, toned, gray, queue[j], br, bk, sig.m, sig.k, sig.lo, sig.hi);
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t p = ntiles * kRgbTile + tid; p < npix; p += 256)
+            tone_rgb_px(rgb, rgb_out, toned, gray, p, br, bk, sig.m, sig.k, sig.lo, sig.hi);
+    }
+}
+
+// fp32 constants and error budget of the fast kernel; false if the curve is
+// outside its range (then the fp64 kernel runs every pixel)
+bool make_tone_rgb_consts(double br, double bk, double m, double k, ToneRgbF* c, bool* two_ex2) {
+    const double u = std::ldexp(1.0, -24), log2e = 1.4426950408889634;
+    if (!(k >= 1e-3 && k <= 1e4)) return false;
+    const double sig1 = 1.0 / (1.0 + std::exp(-k * (1.0 - m)));  // sig(k(1-m))
+    const double D = sig1 - 1.0 / (1.0 + std::exp(k * m));       // hi - lo as the reference forms it
+    const double cn = 1.0 / (sig1 * -std::expm1(-k));
+    if (!(D > 0.0) || !std::isfinite(cn)) return false;
+    *two_ex2 = k > 80.0;
+    const double relL = 24 * u;
+    const double ref = 1e-13 + 4e-16 / D + 1e-15 * k;
+    c->br3 = static_cast<float>(3.0 * br);
+    c->br13 = static_cast<float>(3.0 * (1.0 - br));
+    c->bk3 = static_cast<float>(bk / 3.0);
+    c->bk13 = static_cast<float>((1.0 - bk) / 3.0);
+    c->nak = static_cast<float>(-k * log2e / 255.0);
+    c->ekm = *two_ex2 ? 0.0f : static_cast<float>(std::exp(k * m));
+    c->tc = static_cast<float>(k * m * log2e);
+    c->ycut = static_cast<float>(-0.25 * log2e);
+    c->cn255 = static_cast<float>(255.0 * cn);
+    const double cA = k / 255.0 * (relL + 3 * u);
+    const double cC = *two_ex2 ? 4 * u + 2 * k * m * u : 6 * u;
+    const double cD = 64 * u + ref;
+    const double relRgb = 22 * u + 2 * u + 1.1e-10 / (0.4 * D);
+    c->cA = static_cast<float>(cA);
+    c->cC = static_cast<float>(cC);
+    c->cD = static_cast<float>(cD);
+    c->relRgb = static_cast<float>(relRgb);
+    c->glo = static_cast<float>(1.0 - (relL + 2 * u));
+    c->ghi = static_cast<float>(1.0 + (relL + 2 * u));
+    return true;
+}
+
+template <bool kTwoEx2>
+void launch_tone_rgb_fast(unsigned grid, cudaStream_t st, const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned,
+                          uint8_t* gray, int64_t ntiles, int64_t npix, const ToneRgbF& c, double br, double bk,
+                          const SigD& sig) {
+    if (toned && gray)
+        tone_rgb_fast_kernel<kTwoEx2, true, true><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles, npix, c,
+                                                                        br, bk, sig);
+    else if (toned)
+        tone_rgb_fast_kernel<kTwoEx2, true, false><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles, npix, c,
+                                                                         br, bk, sig);
+    else if (gray)
+        tone_rgb_fast_kernel<kTwoEx2, false, true><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles, npix, c,
+                                                                         br, bk, sig);
+    else
+        tone_rgb_fast_kernel<kTwoEx2, false, false><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles, npix,
+                                                                          c, br, bk, sig);
 }
 
 }  // namespace
@@ -255,16 +570,32 @@ extern "C" int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint
     if (npix == 0) return WG_OK;
     int device = 0;
     cudaGetDevice(&device);
-    const unsigned blocks = static_cast<unsigned>(
-        std::max<int64_t>(1, std::min<int64_t>((npix + 255) / 256, 16LL * sm_count(device))));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     // the curve's constants, as apply_sigmoid forms them (tonemap.py:76-80)
     SigD sig;
     sig.m = midpoint;
     sig.k = slope;
     sig.lo = 1.0 / (1.0 + std::exp(slope * midpoint));
     sig.hi = 1.0 / (1.0 + std::exp(-slope * (1.0 - midpoint)));
-    tone_rgb_u8_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(rgb, rgb_out, toned_or_null,
-                                                                             gray_or_null, npix, beta_r, beta_k, sig);
+    ToneRgbF c;
+    bool two_ex2 = false;
+    const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const bool aligned = al(rgb) && al(rgb_out) && (!toned_or_null || al(toned_or_null)) &&
+                         (!gray_or_null || al(gray_or_null));
+    const int64_t ntiles = npix / kRgbTile;
+    if (aligned && ntiles > 0 && make_tone_rgb_consts(beta_r, beta_k, midpoint, slope, &c, &two_ex2)) {
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ntiles, 3LL * sm_count(device)));
+        if (two_ex2)
+            launch_tone_rgb_fast<true>(grid, st, rgb, rgb_out, toned_or_null, gray_or_null, ntiles, npix, c, beta_r,
+                                       beta_k, sig);
+        else
+            launch_tone_rgb_fast<false>(grid, st, rgb, rgb_out, toned_or_null, gray_or_null, ntiles, npix, c, beta_r,
+                                        beta_k, sig);
+        return check_launch("tone_rgb_fast");
+    }
+    const unsigned blocks = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>((npix + 255) / 256, 16LL * sm_count(device))));
+    tone_rgb_u8_kernel<<<blocks, 256, 0, st>>>(rgb, rgb_out, toned_or_null, gray_or_null, npix, beta_r, beta_k, sig);
     return check_launch("tone_rgb_u8");
 }
 

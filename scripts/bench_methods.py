@@ -1,7 +1,8 @@
 """Device-resident per-method throughput (the paper's Table 1 comparison on B200).
 
 Times wg_decolor_u8 ("ours") against the baseline extractors (wg_luma_u8:
-y / v / lab) on the same uint8 batch already in HBM, CUDA events on the
+y / v / lab), the tone maps and the colour tone map (tone_rgb: 3 B in,
+3 B rgb + 1 B toned out per pixel) on the same uint8 batch already in HBM, CUDA events on the
 launching stream, inputs larger than L2. Prints one JSON line per method.
 
     python scripts/bench_methods.py [--mpix 512] [--iters 50]
@@ -38,6 +39,7 @@ def main():
     fns = {
         "ours": lambda: wg.decolor(rgb, out=out.view(n)),
         "tone": lambda: wg.decolor_tone(rgb),
+        "tone_rgb": lambda: wg.decolor_tone(rgb, return_rgb=True),
         "y": lambda: wg.luma(rgb, "y"),
         "v": lambda: wg.luma(rgb, "v"),
         "lab": lambda: wg.luma(rgb, "lab"),
@@ -55,7 +57,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.iters
-        gbps = 4 * n / ms / 1e6
+        gbps = (7 if name == "tone_rgb" else 4) * n / ms / 1e6  # algorithmic bytes per pixel
         print(json.dumps({"method": name, "npix": n, "ms": round(ms, 4), "gpix_s": round(n / ms / 1e6, 1),
                           "per_pixel_ps": round(ms * 1e9 / n, 3), "gbps": round(gbps, 1),
                           "frac_hbm": round(gbps / hbm, 3)}))

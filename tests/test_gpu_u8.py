@@ -256,16 +256,31 @@ def test_tone_rgb_u8_golden_and_cube(torch_dev, cube):
         assert np.array_equal(out.cpu().numpy(), g[f"{tag}_rgb"])
         assert np.array_equal(toned.cpu().numpy(), g[f"{tag}_toned"])
     t = torch.from_numpy(cube).to(dev)
-    for m, k in [(0.5, 8.0), (0.6, 2000.0), (0.0, 3.0)]:
-        toned, gray, out = wg.decolor_tone(t, wg.SigmoidCurve(m, k), return_gray=True, return_rgb=True)
-        want_o, want_t, want_g = oracle.tone_rgb_u8(cube, midpoint=m, slope=k, threads=oracle.default_threads())
+    # fp32 fast kernel + fp64 queue (1e-6 <= k <= 1e4): default, steep, flat, one-sided curves,
+    # custom betas; k = 2e4 runs the all-fp64 kernel
+    cases = [(0.5, 8.0, 0.55, 0.8), (0.3, 12.0, 0.7, 0.9), (0.6, 2000.0, 0.55, 0.8), (0.0, 3.0, 0.55, 0.8),
+             (1.0, 3.0, 0.51, 0.99), (0.5, 1e-6, 0.55, 0.8), (0.5, 200.0, 0.95, 0.6), (0.4, 2e4, 0.55, 0.8)]
+    for m, k, br, bk in cases:
+        toned, gray, out = wg.decolor_tone(t, wg.SigmoidCurve(m, k), wg.DecolorParams(br, bk), return_gray=True,
+                                           return_rgb=True)
+        want_o, want_t, want_g = oracle.tone_rgb_u8(cube, br, bk, m, k, threads=oracle.default_threads())
         n_o = int((out.cpu().numpy() != want_o).sum())
         n_t = int((toned.cpu().numpy() != want_t).sum())
         n_g = int((gray.cpu().numpy() != want_g).sum())
-        print(f"tone rgb cube m={m} k={k}: rgb diffs {n_o} toned diffs {n_t} gray diffs {n_g}")
+        print(f"tone rgb cube m={m} k={k} betas {br}/{bk}: rgb diffs {n_o} toned diffs {n_t} gray diffs {n_g}")
         assert n_o == n_t == n_g == 0
+    # toned-only request through the same kernel (gray pointer null)
+    toned2, _, out2 = wg.decolor_tone(t, return_rgb=True)
+    want_o, want_t, _ = oracle.tone_rgb_u8(cube, threads=oracle.default_threads())
+    assert np.array_equal(out2.cpu().numpy(), want_o) and np.array_equal(toned2.cpu().numpy(), want_t)
+    # unaligned device buffers (the all-fp64 kernel) and a ragged tail
+    raw = torch.from_numpy(cube.reshape(-1)[: 5000 * 3 + 1].copy()).to(dev)
+    sub = raw[1: 1 + 5000 * 3].view(5000, 3)
+    toned3, _, out3 = wg.decolor_tone(sub, return_rgb=True)
+    want_o, want_t, _ = oracle.tone_rgb_u8(cube.reshape(-1)[1: 1 + 5000 * 3].reshape(5000, 3))
+    assert np.array_equal(out3.cpu().numpy(), want_o) and np.array_equal(toned3.cpu().numpy(), want_t)
     # host-buffer entry point, ragged size
-    h = cube[: 1000003]
+    h = cube.reshape(-1, 3)[: 1000003]
     toned, gray, out = wg.decolor_tone_host(h, return_gray=True, return_rgb=True)
     want_o, want_t, want_g = oracle.tone_rgb_u8(h)
     assert np.array_equal(out, want_o) and np.array_equal(toned, want_t) and np.array_equal(gray, want_g)
