@@ -255,19 +255,24 @@ int tone_table(double m, double k, const ToneTable** out, bool* multi) {
 //   e^{-kx} = 2^y, y = -kx log2(e); e^{-t} = 2^y e^{km} (one ex2) for k <= 80,
 //   2^{y + km log2 e} (a second ex2) beyond; 1 - 2^y by a degree-6 series in
 //   y for kx < 1/4 (evaluated only by warps that hold such a pixel).
-// Error bound (u = 2^-24; MUFU ex2/rsqrt/sqrt/rcp <= 2.5 u measured
-// exhaustively on the B200 by scripts/mufu_error.cu, budgeted at 4 u each;
-// first-order sums along the chain, budgets rounded up):
-//   rel(L), rel(1/L) <= 14 u (budget 24 u);
-//   rel(e^{-t}) <= 6u + kx (rel(L) + 2u)          (one-ex2 form)
-//              <= 4u + 2 km u + kx (rel(L) + 3u)   (two-ex2 form)
-//   rel(1 - e^{-kx}) <= 42 u;  rel(N) <= omS rel(e^{-t}) + 50 u + ref
-//     with omS = 1 - sig(t) (the logistic's own conditioning) and ref the
-//     reference's fp64 error (1e-13 + 4e-16 / D + 1e-15 k, D = hi - lo);
+// Error bound (u = 2^-24; MUFU ex2/rsqrt/sqrt/rcp <= 2.45 u measured
+// exhaustively on the B200 by scripts/mufu_error.cu, budgeted at e = 3 u each;
+// first-order sums along the chain, each budget rounded up):
+//   white' 3u, rg' 4.5u, W' 5.5u, C' 5u, Qn 14u (bytes, R^2+G^2+B^2 and s^2
+//   exact); L = Qn rsqrt(Qn s^2) and 1/L: Qn enters as delta/2 -> 11.5 u
+//   (budget relL = 13 u);
+//   rel(e^{-t}) <= 5u + kx (relL + 2u)            (one-ex2 form)
+//              <= 3u + 2 km u + kx (relL + 3u)    (two-ex2 form)
+//   rel(1 - e^{-kx}) <= 3.52 e + relL + 3u (1 - E, kx >= 1/4) or
+//     relL + 9u (series) -> 28 u;
+//   rel(N) <= omS rel(e^{-t}) + 4u (1 + e^{-t}, rcp) + 28u + 3u (products,
+//     cn255) + ref, omS = 1 - sig(t) (the logistic's own conditioning), ref
+//     the reference's fp64 error (1e-13 + 4e-16 / D + 1e-15 k, D = hi - lo);
 //   rgb v_c = R N 255 / L: rel(N) + rel(1/L) + 2u (+2u for the scale
-//     constants) + the reference's absolute y - lo error folded in relative
-//     form (v >= 0.4 where it matters: 1.1e-10 / (0.4 D)); the toned value
-//     255 N shares the rgb scales (a wider margin than it needs).
+//     constants) -> relRgb 17 u, + the reference's absolute y - lo error
+//     folded in relative form (v >= 0.4 where it matters: 1.1e-10 / (0.4 D));
+//     the toned value 255 N shares the rgb scales (a wider margin than it
+//     needs).
 // A wide margin is never wrong, only slower (more pairs take the fp64 chain).
 // Curves with k < 1e-3 or k > 1e4 run the fp64 kernel for every pixel.
 struct ToneRgbF {
@@ -515,7 +520,7 @@ bool make_tone_rgb_consts(double br, double bk, double m, double k, ToneRgbF* c,
     const double cn = 1.0 / (sig1 * -std::expm1(-k));
     if (!(D > 0.0) || !std::isfinite(cn)) return false;
     *two_ex2 = k > 80.0;
-    const double relL = 24 * u;
+    const double relL = 13 * u;
     const double ref = 1e-13 + 4e-16 / D + 1e-15 * k;
     c->br3 = static_cast<float>(3.0 * br);
     c->br13 = static_cast<float>(3.0 * (1.0 - br));
@@ -527,15 +532,22 @@ bool make_tone_rgb_consts(double br, double bk, double m, double k, ToneRgbF* c,
     c->ycut = static_cast<float>(-0.25 * log2e);
     c->cn255 = static_cast<float>(255.0 * cn);
     const double cA = k / 255.0 * (relL + 3 * u);
-    const double cC = *two_ex2 ? 4 * u + 2 * k * m * u : 6 * u;
-    const double cD = 64 * u + ref;
-    const double relRgb = 22 * u + 2 * u + 1.1e-10 / (0.4 * D);
-    c->cA = static_cast<float>(cA);
-    c->cC = static_cast<float>(cC);
-    c->cD = static_cast<float>(cD);
-    c->relRgb = static_cast<float>(relRgb);
-    c->glo = static_cast<float>(1.0 - (relL + 2 * u));
-    c->ghi = static_cast<float>(1.0 + (relL + 2 * u));
+    const double cC = *two_ex2 ? 3 * u + 2 * k * m * u : 5 * u;
+    const double cD = 36 * u + ref;
+    const double relRgb = 17 * u + 1.1e-10 / (0.4 * D);
+    // test knob: WG_TONE_RGB_MARGIN_SCALE in (0, 1] shrinks every margin, so the
+    // GPU tests can show the bound holds with headroom (bit-identical at 0.5)
+    double sc = 1.0;
+    if (const char* e = std::getenv("WG_TONE_RGB_MARGIN_SCALE")) {
+        const double v = std::atof(e);
+        if (v > 0.0 && v <= 1.0) sc = v;
+    }
+    c->cA = static_cast<float>(sc * cA);
+    c->cC = static_cast<float>(sc * cC);
+    c->cD = static_cast<float>(sc * cD);
+    c->relRgb = static_cast<float>(sc * relRgb);
+    c->glo = static_cast<float>(1.0 - sc * (relL + 2 * u));
+    c->ghi = static_cast<float>(1.0 + sc * (relL + 2 * u));
     return true;
 }
 

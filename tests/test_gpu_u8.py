@@ -286,6 +286,25 @@ def test_tone_rgb_u8_golden_and_cube(torch_dev, cube):
     assert np.array_equal(out, want_o) and np.array_equal(toned, want_t) and np.array_equal(gray, want_g)
 
 
+def test_tone_rgb_u8_bound_headroom(torch_dev, cube, monkeypatch):
+    """The fast kernel's error bound with every margin halved still settles
+    only correct bytes over all 2^24 colours: the first-order budget has at
+    least 2x headroom on the realised fp32 errors (csrc/wg_tone.cu)."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+
+    torch, dev = torch_dev
+    monkeypatch.setenv("WG_TONE_RGB_MARGIN_SCALE", "0.5")
+    t = torch.from_numpy(cube).to(dev)
+    for m, k, br, bk in [(0.5, 8.0, 0.55, 0.8), (0.3, 12.0, 0.7, 0.9), (0.6, 200.0, 0.9, 0.6)]:
+        toned, gray, out = wg.decolor_tone(t, wg.SigmoidCurve(m, k), wg.DecolorParams(br, bk), return_gray=True,
+                                           return_rgb=True)
+        want_o, want_t, want_g = oracle.tone_rgb_u8(cube, br, bk, m, k, threads=oracle.default_threads())
+        n = [int((a.cpu().numpy() != b).sum()) for a, b in ((out, want_o), (toned, want_t), (gray, want_g))]
+        print(f"tone rgb half margins m={m} k={k}: diffs {n}")
+        assert n == [0, 0, 0]
+
+
 def test_empty_and_errors(torch_dev):
     import paper_2108_13656_b200 as wg
 
