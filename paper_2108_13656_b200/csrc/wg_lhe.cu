@@ -52,9 +52,10 @@ constexpr float kGray255Margin = 255.0f * kGrayMargin;  // the same in the 0..25
 // (bins of the uint8 route need margin_t = kGrayMargin * nb < 0.5, i.e. nb < 500000)
 constexpr int kGrp = 16;                                // pixels per thread group (48 input bytes)
 // quantization margin in the x = 255 v + 0.5 domain. Error budget of the uint8
-// route's fp32 x: gray estimate <= 255 * 2.4e-7 = 6.1e-5, fp32 curves (255
-// domain) <= 7.6e-6, fp32 blend fractions <= 2 * 255 * 6e-8, the six roundings
-// of the blend <= 6e-5: < 1.6e-4, so 4e-4 leaves 2.5x headroom.
+// route's fp32 x: gray estimate <= 255 * 2.4e-7 = 6.1e-5 (+ 1.5e-5 when the
+// plane stores it with ulp 2^-15, kPacked), fp32 curves (255 domain) <= 7.6e-6,
+// fp32 blend fractions <= 2 * 255 * 6e-8, the six roundings of the blend
+// <= 6e-5: < 1.8e-4, so 4e-4 leaves 2.2x headroom.
 constexpr float kQuantMargin = 4e-4f;
 constexpr size_t kHistSmemCap = 96 * 1024;
 constexpr size_t kApplySmemCap = 200 * 1024;
@@ -480,10 +481,53 @@ struct U8Lhe {
     }
 };
 
+// Per-warp queue of the rare pixels that need the reference's fp64 chain
+// (entry = group index * 16 + pixel): lanes append their flagged pixels at a
+// shuffle prefix sum and the warp drains the queue through `fix` 32 at a time
+// (all lanes busy) instead of each flagged lane running the long fp64 chain
+// while its warp waits. Capacity: < 32 carried + one group per lane.
+constexpr int kWq = 32 + 32 * kGrp;
+constexpr size_t kWqBytes = static_cast<size_t>(kBlock / 32) * kWq * 4;
+template <class F>
+__device__ __forceinline__ void wq_push(uint32_t* q, int& qn, uint32_t mask, uint32_t gi, F&& fix) {
+    if (!__any_sync(0xFFFFFFFFu, mask != 0u)) return;
+    const int lane = threadIdx.x & 31;
+    const int cnt = __popc(mask);
+    int pre = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int x = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+        if (lane >= d) pre += x;
+    }
+    int slot = qn + pre - cnt;
+    for (uint32_t mm = mask; mm; mm &= mm - 1) q[slot++] = gi * kGrp + static_cast<uint32_t>(__ffs(mm) - 1);
+    qn += __shfl_sync(0xFFFFFFFFu, pre, 31);
+    __syncwarp();  // appends (and the callers' provisional stores) before the drain
+    if (qn >= 32) {
+        for (int j = lane; j < qn; j += 32) fix(q[j]);
+        qn = 0;
+        __syncwarp();  // queue reads before the next appends
+    }
+}
+template <class F>
+__device__ __forceinline__ void wq_flush(const uint32_t* q, int qn, F&& fix) {
+    __syncwarp();
+    for (int j = static_cast<int>(threadIdx.x & 31); j < qn; j += 32) fix(q[j]);
+}
+
+// kPacked (nb <= 512): the plane word carries the pixel's exact bin next to the
+// estimate, bin << 23 | the 23 fraction bits of 256 + g255 (ulp 2^-15), so the
+// apply pass neither recomputes the bin nor re-tests its edges; else the plane
+// holds the fp32 estimate.
+__device__ __forceinline__ uint32_t plane_word(float g255, int bin) {
+    return (__float_as_uint(__fadd_rn(g255, 256.0f)) & 0x7FFFFFu) | (static_cast<uint32_t>(bin) << 23);
+}
+
+template <bool kPacked>
 __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
                                                               float* __restrict__ gplane, int rows_per_chunk,
                                                               bool vec) {
-    extern __shared__ uint32_t sh[];  // [nx * nb] + one dummy cell
+    extern __shared__ uint32_t sh[];  // [nx * nb] + one dummy cell, then the warp queues
     const int64_t img = blockIdx.z;
     const int ty = blockIdx.y;
     const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
@@ -491,6 +535,8 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
     if (y0 >= y1) return;
     const int cells = g.nx * g.nb;
     for (int i = threadIdx.x; i <= cells; i += blockDim.x) sh[i] = 0;
+    uint32_t* wq = sh + cells + 1 + (threadIdx.x >> 5) * kWq;
+    int qn = 0;
     __syncthreads();
     const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
     const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
@@ -501,15 +547,34 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
         n = static_cast<int>(imin64(kGrp, g.w - x0));
         p0 = row0 + static_cast<int64_t>(gy) * g.w + x0;
     };
-    uint32_t gi = threadIdx.x;
+    // the reference's fp64 bin for a pixel next to a bin edge (queued, rare)
+    const auto fix = [&](uint32_t e) {
+        int x0, n;
+        int64_t p0;
+        group_at(e / kGrp, x0, n, p0);
+        const int p = static_cast<int>(e % kGrp);
+        uint32_t cr, cg, cb;
+        L.src.load(p0 + p, cr, cg, cb);
+        const int b = bin_d(L.src.gray_d(cr, cg, cb), g.nb);
+        atomicAdd(&sh[((x0 + p) / g.tw) * g.nb + b], 1u);
+        if constexpr (kPacked) {  // the exact bin into the plane word (after the warp's stores)
+            uint32_t* wp = reinterpret_cast<uint32_t*>(gplane) + p0 + p;
+            *wp = (*wp & 0x7FFFFFu) | (static_cast<uint32_t>(b) << 23);
+        }
+    };
+    const uint32_t lane = threadIdx.x & 31u;
     U8Group nxt;
     int x0n = 0, nn = 0;
     int64_t p0n = 0;
-    if (gi < ngroups) {
-        group_at(gi, x0n, nn, p0n);
+    if (threadIdx.x < ngroups) {
+        group_at(threadIdx.x, x0n, nn, p0n);
         nxt.load(L.src.rgb, p0n, nn, vec);
     }
-    for (; gi < ngroups; gi += blockDim.x) {
+    // warp-uniform trip count (the queue uses warp collectives)
+    for (uint32_t gb = threadIdx.x - lane; gb < ngroups; gb += blockDim.x) {
+        const uint32_t gi = gb + lane;
+        uint32_t slow = 0;
+        if (gi < ngroups) {
         const U8Group grp = nxt;
         const int x0 = x0n, n = nn;
         const int64_t p0 = p0n;
@@ -517,21 +582,11 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
             group_at(gi + blockDim.x, x0n, nn, p0n);
             nxt.load(L.src.rgb, p0n, nn, vec);
         }
-        uint32_t slow = 0;
         int tx = x0 / g.tw, next = (tx + 1) * g.tw;
         if (n == kGrp) {
             float g255[kGrp];
             grp.gray255(L.k8, g255);
-            // keep the estimate for the apply pass (4 B/px instead of recomputing the gray)
-            if (vec) {
-#pragma unroll
-                for (int q = 0; q < kGrp / 4; ++q)
-                    reinterpret_cast<float4*>(gplane + p0)[q] =
-                        make_float4(g255[4 * q], g255[4 * q + 1], g255[4 * q + 2], g255[4 * q + 3]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < kGrp; ++q) gplane[p0 + q] = g255[q];
-            }
+            uint32_t words[kGrp];
             // runs of equal cells are merged before the shared-memory atomic; the
             // first flush goes to the dummy cell
             int run_cell = cells;
@@ -542,7 +597,10 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
                 tx += step;
                 next += step ? g.tw : 0;
                 bool sure;
-                const int cell = tx * g.nb + L.bin_fast(g255[p], sure);
+                const int b = L.bin_fast(g255[p], sure);
+                const int cell = tx * g.nb + b;
+                if constexpr (kPacked) words[p] = plane_word(g255[p], b);  // unsure bins are patched below
+                else words[p] = __float_as_uint(g255[p]);
                 slow |= static_cast<uint32_t>(!sure) << p;
                 const bool same = cell == run_cell;
                 if (sure && !same) atomicAdd(&sh[run_cell], run);
@@ -550,6 +608,17 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
                 run_cell = sure ? cell : run_cell;
             }
             atomicAdd(&sh[run_cell], run);
+            // keep the estimate for the apply pass (4 B/px instead of recomputing the gray)
+            uint32_t* wplane = reinterpret_cast<uint32_t*>(gplane);
+            if (vec) {
+#pragma unroll
+                for (int q = 0; q < kGrp / 4; ++q)
+                    reinterpret_cast<uint4*>(wplane + p0)[q] =
+                        make_uint4(words[4 * q], words[4 * q + 1], words[4 * q + 2], words[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < kGrp; ++q) wplane[p0 + q] = words[q];
+            }
         } else {  // row tail of a width that is not a multiple of 16
 #pragma unroll 1
             for (int p = 0; p < n; ++p) {
@@ -561,21 +630,18 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
                 L.src.load(p0 + p, cr, cg, cb);
                 const float g255 = decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
                                                    static_cast<float>(cb), L.k8);
-                gplane[p0 + p] = g255;
                 bool sure;
                 const int b = L.bin_fast(g255, sure);
+                if constexpr (kPacked) reinterpret_cast<uint32_t*>(gplane)[p0 + p] = plane_word(g255, b);
+                else gplane[p0 + p] = g255;
                 if (sure) atomicAdd(&sh[tx * g.nb + b], 1u);
                 else slow |= 1u << p;
             }
         }
-        while (slow) {  // rare: the reference's fp64 bin for pixels next to an edge
-            const int p = __ffs(slow) - 1;
-            slow &= slow - 1;
-            uint32_t cr, cg, cb;
-            L.src.load(p0 + p, cr, cg, cb);
-            atomicAdd(&sh[((x0 + p) / g.tw) * g.nb + bin_d(L.src.gray_d(cr, cg, cb), g.nb)], 1u);
         }
+        wq_push(wq, qn, slow, gi, fix);  // rare: pixels next to a bin edge
     }
+    wq_flush(wq, qn, fix);
     __syncthreads();
     uint32_t* gh = hist + (img * g.ntile + static_cast<int64_t>(ty) * g.nx) * g.nb;
     for (int i = threadIdx.x; i < cells; i += blockDim.x)
@@ -585,19 +651,19 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
 // shared-memory layout of the apply kernel: curves of <= 3 tile rows, then per
 // column the blend fraction (fp32) and the left tile's curve offset i0 * nb
 // (u32), padded to a multiple of 16 columns so a group reads its 16 entries as
-// 128-bit vectors
+// 128-bit vectors, then the per-warp fp64 queues
 struct ApplySmem {
     static __host__ __device__ int64_t wpad(int64_t w) { return (w + kGrp - 1) / kGrp * kGrp; }
     static __host__ __device__ size_t bytes(int nx, int nb, int64_t w) {
-        return static_cast<size_t>(3) * nx * nb * 4 + static_cast<size_t>(wpad(w)) * 8 + 16;
+        return static_cast<size_t>(3) * nx * nb * 4 + static_cast<size_t>(wpad(w)) * 8 + 16 + kWqBytes;
     }
 };
 
-template <bool kGray, bool kIdent>
+template <bool kGray, bool kIdent, bool kPacked>
 __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict__ toned, uint8_t* __restrict__ gray,
                                              const LheGeom& g, const LheBufs& s, int64_t y0, int64_t y1, int64_t img,
                                              int jbase, const float* cur, const float* sxf, const uint32_t* sxo,
-                                             int64_t G, bool vec) {
+                                             int64_t G, bool vec, uint32_t* wq) {
     const float sf = static_cast<float>(g.strength);
     const int dnb = g.nx > 1 ? g.nb : 0;  // i1 - i0 in curve-table units
     const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
@@ -620,9 +686,38 @@ __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict
             for (int q = 0; q < kGrp / 4; ++q) e[q] = make_float4(t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
         }
     };
+    // the reference's fp64 chain for a pixel within the quantization margin
+    // (queued, rare): overwrites the provisional bytes the warp stored
+    const auto fix = [&](uint32_t e) {
+        const uint32_t gi = e / kGrp, gy = gi / gpr;
+        const int p = static_cast<int>(e % kGrp);
+        const int64_t y = y0 + gy;
+        const int x = static_cast<int>(gi - gy * gpr) * kGrp + p;
+        const int64_t pp = (img * g.h + y) * g.w + x;
+        const int j0 = s.yi[y], j1 = g.ny > 1 ? j0 + 1 : 0;
+        uint32_t cr, cg, cb;
+        L.src.load(pp, cr, cg, cb);
+        const double vd = L.src.gray_d(cr, cg, cb);
+        const int b = bin_d(vd, g.nb);
+        const int i0 = s.xi[x], i1 = g.nx > 1 ? i0 + 1 : 0;
+        const int64_t t00 = img * g.ntile + static_cast<int64_t>(j0) * g.nx + i0, t01 = t00 - i0 + i1;
+        const int64_t t10 = img * g.ntile + static_cast<int64_t>(j1) * g.nx + i0, t11 = t10 - i0 + i1;
+        const double c00 = s.ident[t00] ? vd : s.curve[t00 * g.nb + b];
+        const double c01 = s.ident[t01] ? vd : s.curve[t01 * g.nb + b];
+        const double c10 = s.ident[t10] ? vd : s.curve[t10 * g.nb + b];
+        const double c11 = s.ident[t11] ? vd : s.curve[t11 * g.nb + b];
+        toned[pp] = static_cast<uint8_t>(quantize_d(blend_d(vd, c00, c01, c10, c11, s.xf[x], s.yf[y], g.strength)));
+        if constexpr (kGray) gray[pp] = static_cast<uint8_t>(quantize_d(vd));
+    };
+    const uint32_t lane = threadIdx.x & 31u;
+    int qn = 0;
     float4 nxt[kGrp / 4];
     if (threadIdx.x < ngroups) load_est(threadIdx.x, nxt);
-    for (uint32_t gi = threadIdx.x; gi < ngroups; gi += blockDim.x) {
+    // warp-uniform trip count (the queue uses warp collectives)
+    for (uint32_t gb = threadIdx.x - lane; gb < ngroups; gb += blockDim.x) {
+        const uint32_t gi = gb + lane;
+        uint32_t slow = 0;
+        if (gi < ngroups) {
         const uint32_t gy = gi / gpr;
         const int64_t y = y0 + gy;
         const int x0 = static_cast<int>(gi - gy * gpr) * kGrp;
@@ -658,12 +753,20 @@ __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict
             xos[4 * q + 3] = o.w;
         }
         uint32_t ot[4] = {0u, 0u, 0u, 0u}, og[4] = {0u, 0u, 0u, 0u};
-        uint32_t slow = 0;
 #pragma unroll
         for (int p = 0; p < kGrp; ++p) {
-            const float v = g255[p];  // everything below is in the 0..255 domain
+            float v;  // everything below is in the 0..255 domain
             bool sure;
-            const int b = L.bin_fast(v, sure);
+            int b;
+            if constexpr (kPacked) {  // estimate (ulp 2^-15) and exact bin from the hist pass
+                const uint32_t wd = __float_as_uint(g255[p]);
+                v = __fsub_rn(__uint_as_float((wd & 0x7FFFFFu) | 0x43800000u), 256.0f);
+                b = static_cast<int>(wd >> 23);
+                sure = true;
+            } else {
+                v = g255[p];
+                b = L.bin_fast(v, sure);
+            }
             const int a00 = r0nb + static_cast<int>(xos[p]) + b, a10 = a00 + drow;
             float c00 = cur[a00], c01 = cur[a00 + dnb], c10 = cur[a10], c11 = cur[a10 + dnb];
             if constexpr (kIdent) {
@@ -691,37 +794,6 @@ __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict
             }
             slow |= static_cast<uint32_t>(!sure && p < n) << p;
         }
-        while (slow) {  // rare: redo the flagged pixels through the reference's fp64 chain
-            const int p = __ffs(slow) - 1;
-            slow &= slow - 1;
-            const int64_t pp = p0 + p;
-            uint32_t cr, cg, cb;
-            L.src.load(pp, cr, cg, cb);
-            const double vd = L.src.gray_d(cr, cg, cb);
-            const int b = bin_d(vd, g.nb);
-            const int x = x0 + p;
-            const int i0 = s.xi[x], i1 = g.nx > 1 ? i0 + 1 : 0;
-            const int64_t t00 = img * g.ntile + static_cast<int64_t>(j0) * g.nx + i0, t01 = t00 - i0 + i1;
-            const int64_t t10 = img * g.ntile + static_cast<int64_t>(j1) * g.nx + i0, t11 = t10 - i0 + i1;
-            const double c00 = s.ident[t00] ? vd : s.curve[t00 * g.nb + b];
-            const double c01 = s.ident[t01] ? vd : s.curve[t01 * g.nb + b];
-            const double c10 = s.ident[t10] ? vd : s.curve[t10 * g.nb + b];
-            const double c11 = s.ident[t11] ? vd : s.curve[t11 * g.nb + b];
-            const uint32_t qt = quantize_d(blend_d(vd, c00, c01, c10, c11, s.xf[x], s.yf[y], g.strength));
-            const uint32_t qg = quantize_d(vd), sh = 8 * (p & 3), m = ~(255u << sh);
-            const int k = p >> 2;
-            // o[k] with a dynamic k would go to local memory: select instead
-            ot[0] = k == 0 ? (ot[0] & m) | (qt << sh) : ot[0];
-            ot[1] = k == 1 ? (ot[1] & m) | (qt << sh) : ot[1];
-            ot[2] = k == 2 ? (ot[2] & m) | (qt << sh) : ot[2];
-            ot[3] = k == 3 ? (ot[3] & m) | (qt << sh) : ot[3];
-            if constexpr (kGray) {
-                og[0] = k == 0 ? (og[0] & m) | (qg << sh) : og[0];
-                og[1] = k == 1 ? (og[1] & m) | (qg << sh) : og[1];
-                og[2] = k == 2 ? (og[2] & m) | (qg << sh) : og[2];
-                og[3] = k == 3 ? (og[3] & m) | (qg << sh) : og[3];
-            }
-        }
         if (vec && n == kGrp) {
             st_global_cs_v4(toned + p0, make_uint4(ot[0], ot[1], ot[2], ot[3]));
             if constexpr (kGray) st_global_cs_v4(gray + p0, make_uint4(og[0], og[1], og[2], og[3]));
@@ -734,10 +806,13 @@ __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict
                 }
             }
         }
+        }
+        wq_push(wq, qn, slow, gi, fix);
     }
+    wq_flush(wq, qn, fix);
 }
 
-template <bool kGray>
+template <bool kGray, bool kPacked>
 __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8_t* __restrict__ toned,
                                                                uint8_t* __restrict__ gray, LheGeom g, LheBufs s,
                                                                int rows_per_chunk, bool vec) {
@@ -753,6 +828,7 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
     float* cur = reinterpret_cast<float*>(smem);              // [3][nx][nb]: 255 * curve, NaN = identity
     float* sxf = cur + static_cast<size_t>(3) * g.nx * g.nb;  // [wp]
     uint32_t* sxo = reinterpret_cast<uint32_t*>(sxf + wp);    // [wp] i0 * nb
+    uint32_t* wq = sxo + wp + 4 + (threadIdx.x >> 5) * kWq;     // per-warp queues (after 16 B of slack)
     const int64_t tile0 = img * g.ntile + static_cast<int64_t>(jbase) * g.nx;
     const int ncur = nload * g.nx * g.nb;
     for (int i = threadIdx.x; i < ncur; i += blockDim.x) cur[i] = s.curvef[tile0 * g.nb + i];
@@ -771,8 +847,10 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
     // blocks whose staged curve rows contain one
     bool any_ident = false;
     for (int i = threadIdx.x; i < nload * g.nx; i += blockDim.x) any_ident |= cur[i * g.nb] != cur[i * g.nb];
-    if (__syncthreads_or(any_ident)) apply_groups<kGray, true>(L, toned, gray, g, s, y0, y1, img, jbase, cur, sxf, sxo, G, vec);
-    else apply_groups<kGray, false>(L, toned, gray, g, s, y0, y1, img, jbase, cur, sxf, sxo, G, vec);
+    if (__syncthreads_or(any_ident))
+        apply_groups<kGray, true, kPacked>(L, toned, gray, g, s, y0, y1, img, jbase, cur, sxf, sxo, G, vec, wq);
+    else
+        apply_groups<kGray, false, kPacked>(L, toned, gray, g, s, y0, y1, img, jbase, cur, sxf, sxo, G, vec, wq);
 }
 
 // ------------------------------------------------------------------ driver
@@ -949,19 +1027,20 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     rc = lhe_begin(g, b, st);
     if (rc != WG_OK) return rc;
     const Chunking c = chunking(g);
-    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4;  // + the dummy cell
+    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4 + kWqBytes;  // + the dummy cell, warp queues
     const size_t asmem = ApplySmem::bytes(g.nx, g.nb, g.w);
     // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact); the
     // group apply reads the gray plane the group hist writes, so both or neither
     const bool group_ok = bins <= 65536 && hsmem <= kHistSmemCap && asmem <= kApplySmemCap;
+    const bool packed = bins <= 512;  // the plane word carries the bin (9 bits)
     if (group_ok) {
+        auto hk = packed ? lhe_hist_u8g_kernel<true> : lhe_hist_u8g_kernel<false>;
         if (hsmem > 48 * 1024)
-            cudaFuncSetAttribute(lhe_hist_u8g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(hsmem));
+            cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hsmem));
         per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
             U8Lhe Li = L;
             Li.src.advance(i0 * g.h * g.w);
-            lhe_hist_u8g_kernel<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, hsmem, st>>>(
+            hk<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, hsmem, st>>>(
                 Li, gi, b.hist + i0 * g.ntile * g.nb, b.gray255 + i0 * g.h * g.w, c.rows_per_chunk, vec);
         });
     } else {
@@ -969,7 +1048,8 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     }
     lhe_curves(g, b, st);
     if (group_ok) {
-        auto kern = gray_or_null ? lhe_apply_u8g_kernel<true> : lhe_apply_u8g_kernel<false>;
+        auto kern = gray_or_null ? (packed ? lhe_apply_u8g_kernel<true, true> : lhe_apply_u8g_kernel<true, false>)
+                                 : (packed ? lhe_apply_u8g_kernel<false, true> : lhe_apply_u8g_kernel<false, false>);
         if (asmem > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(asmem));
         per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
