@@ -3,7 +3,7 @@
 # and a torchrun launch), and the ncu evidence (launch list + one full capture of
 # the hot kernel) for the C3 bench command.
 # Usage (from the repo root, under gpurun):  bash scripts/gpu_round.sh [tag]
-TAG=${1:-r01d}
+TAG=${1:-r01e}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/nvsmi_$TAG.txt 2>&1
@@ -25,3 +25,7 @@ echo "ncu_launches=$?"
 $B > $OUT/ncu_plain2_$TAG.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 3 -c 1 -o $OUT/prof_c3_$TAG $B > $OUT/ncu_full_$TAG.log 2>&1
 echo "ncu_full=$?"
+T="python scripts/bench_methods.py --mpix 512 --iters 3 --methods tone_rgb,local"
+$T > $OUT/methods_plain_$TAG.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:"tone_rgb_fast|lhe_(hist|apply)_u8g" -s 3 -c 3 -o $OUT/prof_tone_lhe_$TAG $T > $OUT/ncu_tone_lhe_$TAG.log 2>&1
+echo "ncu_tone_lhe=$?"
