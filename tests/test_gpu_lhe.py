@@ -139,7 +139,9 @@ def test_u8_golden_bit_identical(golden):
 
 
 @pytest.mark.parametrize("shape,grid", [((2, 1080, 1920), None), ((3, 97, 131), (17, 13, 64, 0.9)),
-                                        ((1, 64, 48), (1, 1, 256, 1.0)), ((4, 33, 35), (5, 7, 1000, 0.3))])
+                                        ((1, 64, 48), (1, 1, 256, 1.0)), ((4, 33, 35), (5, 7, 1000, 0.3)),
+                                        # nb = 512: largest bin count the plane word carries; 513: fp32 plane
+                                        ((2, 50, 70), (9, 11, 512, 0.8)), ((2, 50, 70), (9, 11, 513, 0.8))])
 def test_u8_batch_vs_oracle(shape, grid):
     import torch
 
