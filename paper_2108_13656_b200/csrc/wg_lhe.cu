@@ -1031,7 +1031,9 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     const size_t asmem = ApplySmem::bytes(g.nx, g.nb, g.w);
     // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact); the
     // group apply reads the gray plane the group hist writes, so both or neither
-    const bool group_ok = bins <= 65536 && hsmem <= kHistSmemCap && asmem <= kApplySmemCap;
+    // (the per-warp queue entries are group * 16 + pixel within one row chunk: < 2^32)
+    const bool group_ok = bins <= 65536 && hsmem <= kHistSmemCap && asmem <= kApplySmemCap &&
+                          static_cast<int64_t>(c.rows_per_chunk) * ApplySmem::wpad(g.w) < (int64_t(1) << 32);
     const bool packed = bins <= 512;  // the plane word carries the bin (9 bits)
     if (group_ok) {
         auto hk = packed ? lhe_hist_u8g_kernel<true> : lhe_hist_u8g_kernel<false>;
