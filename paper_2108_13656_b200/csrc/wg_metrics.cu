@@ -20,6 +20,8 @@
 // Pair sets: all n(n-1)/2 unordered pairs (triangular grid of 256 x 256 pixel
 // tiles, the j tile staged in shared memory), or an explicit (i, j) list -- the
 // reference's seeded sample, drawn on the host with its own NumPy generator.
+// With the integer thresholds 1..ntau of TAU_SWEEP the exhaustive kernel
+// counts in fp32 with a proven margin and an fp64 recheck (metric_all_pairs_int_kernel).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -76,15 +78,18 @@ __device__ __forceinline__ double dot3d(double a0, double a1, double a2, double 
 }
 
 __global__ void metric_prep_kernel(const double* __restrict__ rgb, const double* __restrict__ gray,
-                                   double4* __restrict__ labg, int64_t n) {
+                                   double4* __restrict__ labg, float4* __restrict__ lab32, int64_t n) {
     for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < n;
          p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double lr = lin_d(rgb[3 * p]), lg = lin_d(rgb[3 * p + 1]), lb = lin_d(rgb[3 * p + 2]);
         const double fx = labf_d(__ddiv_rn(dot3d(MX0, MX1, MX2, lr, lg, lb), WHITE_X));
         const double fy = labf_d(dot3d(MY0, MY1, MY2, lr, lg, lb));
         const double fz = labf_d(__ddiv_rn(dot3d(MZ0, MZ1, MZ2, lr, lg, lb), WHITE_Z));
-        labg[p] = make_double4(__dsub_rn(__dmul_rn(116.0, fy), 16.0), __dmul_rn(500.0, __dsub_rn(fx, fy)),
-                               __dmul_rn(200.0, __dsub_rn(fy, fz)), __dmul_rn(gray[p], 100.0));
+        const double4 v = make_double4(__dsub_rn(__dmul_rn(116.0, fy), 16.0), __dmul_rn(500.0, __dsub_rn(fx, fy)),
+                                       __dmul_rn(200.0, __dsub_rn(fy, fz)), __dmul_rn(gray[p], 100.0));
+        labg[p] = v;
+        lab32[p] = make_float4(__double2float_rn(v.x), __double2float_rn(v.y), __double2float_rn(v.z),
+                               __double2float_rn(v.w));
     }
 }
 
@@ -102,8 +107,9 @@ struct WarpHist {
     uint32_t full = 0;  // the saturated bin (kc = kg = ntau), counted in a register
     int full_bin;
     __device__ __forceinline__ void add(int bin) {
-        if (bin == full_bin) ++full;
-        else atomicAdd(&h[bin], 1u);
+        const bool f = bin == full_bin;
+        full += f;
+        if (!f) atomicAdd(&h[bin], 1u);
     }
 };
 
@@ -146,6 +152,114 @@ __global__ void __launch_bounds__(kTile) metric_all_pairs_kernel(const double4* 
         for (int jj = jstart; jj < jn; ++jj) wh.add(pair_bin(a, tile[jj], ts, tg, stride));
     }
     flush_hist(sh, wh, nbins, hist);
+}
+
+// Integer thresholds tau = 1..ntau (TAU_SWEEP): kc = #{k <= ntau : delta_e >= k} =
+// min(floor(delta_e), ntau) and kg likewise from gray_diff, evaluated in fp32
+// (one MUFU sqrt) from fp32 copies of lab / 100 g. Rigorous margins against
+// the reference's fp64 values: each lab component (|.| <= 128) rounds by
+// <= 128 u, so |d32 - D| <= 256 u + u|D| and |sqrt(s32) - |D|| <= 2 sqrt(3)
+// 1.53e-5 + 5u|D| + 3e-10 / |D|, plus 2.5 u r for sqrt.approx: <= 6.1e-5 for
+// r <= 16 (the reference's own fl(sqrt) is within 1e-15); gray_diff (|.| <=
+// 100) <= 200 u + u gd <= 1.3e-5. A pair whose fp32 value lies within 8e-5
+// (colour) / 2e-5 (gray) of a threshold takes the reference's fp64 route
+// (pair_bin); every other count is decided exactly.
+constexpr float kMarginDe = 8e-5f, kMarginGd = 2e-5f;
+// count of the integer thresholds 1..ntau a value reaches, for two values in
+// packed f32x2: each clamped to [1/2, ntau + 1/2] (neither end is a
+// threshold, both floor into [0, ntau]); near when within `margin` of an integer
+__device__ __forceinline__ void int_count2(float2 v, float margin, float vmax, uint32_t& k0, uint32_t& k1,
+                                           bool& near0, bool& near1) {
+    const float2 c = make_float2(fminf(fmaxf(v.x, 0.5f), vmax), fminf(fmaxf(v.y, 0.5f), vmax));
+    const float2 f = add2_rz(c, bc2(8388608.0f));  // 2^23 + floor(c)
+    const float2 e = add2(fma2(add2(f, bc2(-8388608.0f)), bc2(-1.0f), c), bc2(-0.5f));  // frac - 1/2
+    near0 = near0 || fabsf(e.x) > 0.5f - margin;
+    near1 = near1 || fabsf(e.y) > 0.5f - margin;
+    k0 = __float_as_uint(f.x) & 0x7FFFFFu;
+    k1 = __float_as_uint(f.y) & 0x7FFFFFu;
+}
+
+// shared-memory histogram increment without the compiler's warp-aggregation
+// scaffolding: a predicated red.shared
+__device__ __forceinline__ void red_shared_inc(uint32_t* p, bool pred) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n @q red.shared.add.u32 [%0], 1;\n}" ::"r"(
+                     smem_addr(p)),
+                 "r"(static_cast<uint32_t>(pred))
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(kTile) metric_all_pairs_int_kernel(const float4* __restrict__ lab32,
+                                                                     const double4* __restrict__ labg, int64_t n,
+                                                                     Thresholds th, float vmax,
+                                                                     unsigned long long* hist) {
+    const int64_t ti = blockIdx.y, tj = blockIdx.x;
+    if (tj < ti) return;  // triangle: tile pairs (ti <= tj)
+    // the j tile as structure of arrays: one 64-bit shared load per component
+    // fetches two j (a warp-wide broadcast, no bank conflicts)
+    __shared__ __align__(16) float soa[4][kTile];
+    __shared__ uint32_t sh[(kTile / 32) * kBins];
+    __shared__ double ts[16], tg[16];
+    const int ntau = th.ntau, stride = ntau + 1, nbins = stride * stride;
+    for (int b = threadIdx.x; b < (kTile / 32) * kBins; b += blockDim.x) sh[b] = 0;
+    if (threadIdx.x < 16) {
+        ts[threadIdx.x] = th.s[threadIdx.x];
+        tg[threadIdx.x] = th.g[threadIdx.x];
+    }
+    const int64_t j0 = tj * kTile;
+    const int jn = static_cast<int>(imin64(kTile, n - j0));
+    if (static_cast<int>(threadIdx.x) < jn) {
+        const float4 v = lab32[j0 + threadIdx.x];
+        soa[0][threadIdx.x] = v.x;
+        soa[1][threadIdx.x] = v.y;
+        soa[2][threadIdx.x] = v.z;
+        soa[3][threadIdx.x] = v.w;
+    }
+    __syncthreads();
+    uint32_t* wh = sh + (threadIdx.x / 32) * kBins;
+    const int full_bin = ntau * stride + ntau;
+    uint32_t full = 0;  // the saturated bin, counted in a register
+    const int64_t i = ti * kTile + threadIdx.x;
+    const bool active = i < n;
+    const float4 a = active ? lab32[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const auto add = [&](int bin, bool valid) {
+        const bool f = bin == full_bin;
+        full += (f && valid) ? 1u : 0u;
+        red_shared_inc(wh + bin, valid && !f);
+    };
+    const auto exact = [&](int jj) { return pair_bin(labg[i], labg[j0 + jj], ts, tg, stride); };
+    // pairs (k, k + 1) over a block-uniform range; each element masked by this
+    // lane's lower bound (diagonal tile: j > i only) and the tile end
+    const int lo = ti == tj ? static_cast<int>(threadIdx.x) + 1 : 0;
+    const float2 ax = bc2(a.x), ay = bc2(a.y), az = bc2(a.z), aw = bc2(a.w);
+#pragma unroll 2
+    for (int k = 0; k < jn; k += 2) {
+        const bool v0 = active && k >= lo, v1 = active && k + 1 >= lo && k + 1 < jn;
+        const float2 d0 = fma2(*reinterpret_cast<const float2*>(&soa[0][k]), bc2(-1.0f), ax);  // a - b, one rounding
+        const float2 d1 = fma2(*reinterpret_cast<const float2*>(&soa[1][k]), bc2(-1.0f), ay);
+        const float2 d2 = fma2(*reinterpret_cast<const float2*>(&soa[2][k]), bc2(-1.0f), az);
+        const float2 gd = fma2(*reinterpret_cast<const float2*>(&soa[3][k]), bc2(-1.0f), aw);
+        const float2 s2 = fma2(d2, d2, fma2(d1, d1, mul2(d0, d0)));
+        const float2 de = make_float2(sqrt_mufu(s2.x), sqrt_mufu(s2.y));
+        bool n0 = false, n1 = false;
+        uint32_t kc0, kc1, kg0, kg1;
+        int_count2(de, kMarginDe, vmax, kc0, kc1, n0, n1);
+        int_count2(make_float2(fabsf(gd.x), fabsf(gd.y)), kMarginGd, vmax, kg0, kg1, n0, n1);
+        int b0 = static_cast<int>(kc0) * stride + static_cast<int>(kg0);
+        int b1 = static_cast<int>(kc1) * stride + static_cast<int>(kg1);
+        n0 = n0 && v0;
+        n1 = n1 && v1;
+        if (__any_sync(0xFFFFFFFFu, n0 || n1)) {  // rare: the reference's fp64 route
+            if (n0) b0 = exact(k);
+            if (n1) b1 = exact(k + 1);
+        }
+        add(b0, v0);
+        add(b1, v1);
+    }
+    WarpHist w;
+    w.h = wh;
+    w.full = full;
+    w.full_bin = full_bin;
+    flush_hist(sh, w, nbins, hist);
 }
 
 __global__ void __launch_bounds__(kTile) metric_pairs_kernel(const double4* __restrict__ labg,
@@ -201,6 +315,13 @@ int make_thresholds(const double* taus, int ntau, Thresholds* th) {
     return WG_OK;
 }
 
+// taus == 1, 2, ..., ntau (TAU_SWEEP and its prefixes): the fp32 integer-count kernel applies
+bool integer_taus(const double* taus, int ntau) {
+    for (int k = 0; k < ntau; ++k)
+        if (taus[k] != static_cast<double>(k + 1)) return false;
+    return true;
+}
+
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
@@ -209,7 +330,10 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 using namespace wg;
 
 extern "C" size_t wg_metric_scratch_bytes(int64_t npix) {
-    return npix < 0 ? 0 : align256(static_cast<size_t>(npix) * sizeof(double4)) + 256;
+    // fp64 (L*, a*, b*, 100 g) per pixel, then its fp32 copy
+    return npix < 0 ? 0
+                    : align256(static_cast<size_t>(npix) * sizeof(double4)) +
+                          align256(static_cast<size_t>(npix) * sizeof(float4)) + 256;
 }
 
 extern "C" int wg_metric_hist_f64(const double* rgb, const double* gray, int64_t npix, const double* taus, int ntau,
@@ -229,11 +353,13 @@ extern "C" int wg_metric_hist_f64(const double* rgb, const double* gray, int64_t
     if (e != cudaSuccess) return set_error(static_cast<int>(e), "metric: memset: %s", cudaGetErrorString(e));
     if (npix < 2) return WG_OK;
     double4* labg = static_cast<double4*>(scratch);
+    float4* lab32 = reinterpret_cast<float4*>(static_cast<uint8_t*>(scratch) +
+                                              align256(static_cast<size_t>(npix) * sizeof(double4)));
     int device = 0;
     cudaGetDevice(&device);
     const unsigned prep_blocks =
         static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((npix + 255) / 256, 16LL * sm_count(device))));
-    metric_prep_kernel<<<prep_blocks, 256, 0, st>>>(rgb, gray, labg, npix);
+    metric_prep_kernel<<<prep_blocks, 256, 0, st>>>(rgb, gray, labg, lab32, npix);
     if (pair_i) {
         if (npairs) {
             const unsigned blocks = static_cast<unsigned>(
@@ -243,8 +369,12 @@ extern "C" int wg_metric_hist_f64(const double* rgb, const double* gray, int64_t
     } else {
         const int64_t nt = (npix + kTile - 1) / kTile;
         if (nt > 65535) return set_error(WG_EINVAL, "exhaustive pairs support up to %d pixels", 65535 * kTile);
-        metric_all_pairs_kernel<<<dim3(static_cast<unsigned>(nt), static_cast<unsigned>(nt)), kTile, 0, st>>>(
-            labg, npix, th, hist);
+        const dim3 grid(static_cast<unsigned>(nt), static_cast<unsigned>(nt));
+        if (integer_taus(taus, ntau))
+            metric_all_pairs_int_kernel<<<grid, kTile, 0, st>>>(lab32, labg, npix, th,
+                                                                 static_cast<float>(ntau) + 0.5f, hist);
+        else
+            metric_all_pairs_kernel<<<grid, kTile, 0, st>>>(labg, npix, th, hist);
     }
     return check_launch("metric pair counts");
 }

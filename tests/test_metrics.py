@@ -135,6 +135,31 @@ def test_counts_vs_oracle(shape, cfg):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("case", ["random_256", "gray_hundredths", "flat_colours"])
+def test_integer_tau_kernel_vs_oracle(case):
+    """TAU_SWEEP (1..15) exhaustive: the fp32 integer-count kernel with its fp64
+    recheck near thresholds gives the oracle's exact counts, including gray
+    differences within 1e-13 of an integer (gray = k / 100) and repeated
+    colours (delta_e exactly 0)."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(11)
+    if case == "random_256":
+        rgb = rng.integers(0, 256, (256, 256, 3)).astype(np.float64) / 255.0
+        gray = wg.luminance_image(wg.PlanarImage(rgb)).data
+    elif case == "gray_hundredths":
+        rgb = rng.integers(0, 256, (64, 64, 3)).astype(np.float64) / 255.0
+        gray = (rng.integers(0, 101, (64, 64)) / 100.0).astype(np.float64)
+    else:
+        pal = rng.integers(0, 256, (6, 3)).astype(np.float64) / 255.0
+        rgb = pal[rng.integers(0, 6, (48, 80))]
+        gray = wg.luminance_image(wg.PlanarImage(rgb)).data
+    got = m.sweep_counts(wg.PlanarImage(rgb), wg.PlanarImage(gray), m.TAU_SWEEP, EXHAUSTIVE)
+    want = oracle.metric_counts(rgb, gray, list(m.TAU_SWEEP), None, threads=oracle.default_threads())
+    np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.gpu
 def test_reference_properties(rng):
     v = rng.random((6, 6))
     color = wg.PlanarImage(np.repeat(v[:, :, None], 3, axis=2))
