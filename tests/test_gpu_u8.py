@@ -286,6 +286,41 @@ def test_tone_rgb_u8_golden_and_cube(torch_dev, cube):
     assert np.array_equal(out, want_o) and np.array_equal(toned, want_t) and np.array_equal(gray, want_g)
 
 
+def test_tone_rgb_u8_voronoi_frames(torch_dev):
+    """C3-shape Voronoi frames (200 flat cells each): a cell whose colour is
+    near a rounding tie sends thousands of consecutive pixels through the warp
+    queues at once -- bytes still identical to the oracle."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+    from paper_2108_13656_b200 import synth
+
+    torch, dev = torch_dev
+    rgb = torch.empty((2, 2160, 3840, 3), dtype=torch.uint8, device=dev)
+    synth.fill_voronoi_u8(rgb, seed=0, first_image=7)
+    host = rgb.cpu().numpy()
+    for m, k in [(0.5, 8.0), (0.45, 30.0)]:
+        toned, gray, out = wg.decolor_tone(rgb, wg.SigmoidCurve(m, k), return_gray=True, return_rgb=True)
+        want_o, want_t, want_g = oracle.tone_rgb_u8(host, midpoint=m, slope=k, threads=oracle.default_threads())
+        assert np.array_equal(out.cpu().numpy(), want_o)
+        assert np.array_equal(toned.cpu().numpy(), want_t) and np.array_equal(gray.cpu().numpy(), want_g)
+    # a frame of the colour whose exact rgb value lies closest to a rounding
+    # boundary (fp64 chain in NumPy): every pixel of it is queued
+    cols = np.random.default_rng(4).integers(1, 256, (200_000, 3), dtype=np.uint8)
+    c = cols.astype(np.float64) / 255.0
+    li = oracle.decolor_f64(c)
+    lo_, hi_ = 1.0 / (1.0 + np.exp(8.0 * 0.5)), 1.0 / (1.0 + np.exp(-8.0 * 0.5))
+    lout = np.clip((1.0 / (1.0 + np.exp(-8.0 * (li - 0.5))) - lo_) / (hi_ - lo_), 0.0, 1.0)
+    v = np.clip(c * (lout / li)[:, None], 0.0, 1.0) * 255.0
+    dist = np.abs(v - np.floor(v) - 0.5).min(axis=1)
+    pick = cols[int(np.argmin(dist))]
+    print(f"nearest-tie colour {pick.tolist()} at {dist.min():.2e} from a boundary")
+    flat = torch.empty((1, 512, 4096, 3), dtype=torch.uint8, device=dev)
+    flat[:] = torch.from_numpy(pick).to(dev)
+    _, _, fo = wg.decolor_tone(flat, return_rgb=True)
+    want, _, _ = oracle.tone_rgb_u8(pick[None])
+    assert (fo.view(-1, 3).cpu().numpy() == want[0]).all()
+
+
 def test_tone_rgb_u8_bound_headroom(torch_dev, cube, monkeypatch):
     """The fast kernel's error bound with every margin halved still settles
     only correct bytes over all 2^24 colours: the first-order budget has at
