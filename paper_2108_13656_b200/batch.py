@@ -326,12 +326,20 @@ def decolor_tone_host(rgb, curve: SigmoidCurve = SigmoidCurve(),
 
 
 def hdr_tonemap_host(rgb, params: DecolorParams = DEFAULT_PARAMS,
-                     curve: SigmoidCurve = SigmoidCurve(), device: int | None = None):
-    """HDR adapter on a host (N, H, W, 3) float32 batch -> (N, H, W) uint8."""
+                     curve: SigmoidCurve = SigmoidCurve(), device: int | None = None, out=None):
+    """HDR adapter on a host (N, H, W, 3) float32 batch -> (N, H, W) uint8.
+
+    ``out`` (optional, C-contiguous uint8 of shape rgb.shape[:-1]): pass a
+    pinned buffer to keep the device -> host copies asynchronous (a pageable
+    destination serialises the copy pipeline).
+    """
     arr = _host_rgb(rgb, ("float32",))
     if arr.ndim < 2:
         raise ValueError("hdr_tonemap_host expects a batch (N, ..., 3)")
-    out = np.empty(arr.shape[:-1], dtype=np.uint8)
+    if out is None:
+        out = np.empty(arr.shape[:-1], dtype=np.uint8)
+    elif out.shape != arr.shape[:-1] or out.dtype != np.uint8 or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError("out must be C-contiguous uint8 with shape rgb.shape[:-1]")
     n = arr.shape[0]
     ppi = out.size // n if n else 0
     if out.size:
