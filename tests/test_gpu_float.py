@@ -243,6 +243,14 @@ def test_hdr_golden():
     print(f"hdr golden: max {mx} frac {frac:.3e}")
     assert mx <= 1 and frac <= 2e-3  # 2304 px: one tie allowed
     assert (got[2] == got[2].flat[0]).all()  # constant image stays constant
+    # caller-provided (pinned) destination: same bytes; wrong shape / dtype rejected
+    import torch
+
+    pinned = torch.empty(got.shape, dtype=torch.uint8, pin_memory=True).numpy()
+    assert wg.hdr_tonemap_host(g["rgb"], out=pinned) is pinned
+    np.testing.assert_array_equal(pinned, got)
+    with pytest.raises(ValueError):
+        wg.hdr_tonemap_host(g["rgb"], out=np.empty(got.shape, dtype=np.float32))
 
 
 def test_hdr_c4_images(torch_dev):
