@@ -151,18 +151,22 @@ def _empty_batch(shape, pinned: bool) -> np.ndarray:
     return np.empty(shape, dtype=np.uint8)
 
 
-def read_pnm_batch(paths, threads: int | None = None, pinned: bool = True) -> np.ndarray:
+def read_pnm_batch(paths, threads: int | None = None, pinned: bool = True, out=None) -> np.ndarray:
     """Read same-size binary PGM/PPM files into one uint8 batch (N, H, W[, 3]).
 
     The batch lives in pinned host memory by default (the device path copies
-    it with DMA); one host thread per file up to ``threads``.
+    it with DMA), or in ``out`` (C-contiguous uint8 of the batch's shape) when
+    given; one host thread per file up to ``threads``.
     """
     paths = [os.fspath(p) for p in paths]
     if not paths:
         raise ValueError("read_pnm_batch needs at least one path")
     h, w, c = pnm_info(paths[0])
     shape = (len(paths), h, w, 3) if c == 3 else (len(paths), h, w)
-    out = _empty_batch(shape, pinned)
+    if out is None:
+        out = _empty_batch(shape, pinned)
+    elif out.shape != shape or out.dtype != np.uint8 or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"out must be C-contiguous uint8 of shape {shape}")
     _lib.check(_lib.load().wg_pnm_read_batch(_paths(paths), len(paths), out.ctypes.data, w, h, c,
                                              _threads(threads)), "wg_pnm_read_batch")
     return out
@@ -190,7 +194,9 @@ def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=N
     quantize_u8 of the reference's fp64 chain for "local" and within the
     north-star bound (+-1 on <= 0.01% of pixels) for "gray" / "global".
     Same-size binary PPM inputs go through the native batch reader in groups
-    of ``batch``; outputs are written as PGM. Returns the number of files.
+    of ``batch``; outputs are written as PGM. Reading batch i + 1, the device
+    pass of batch i and writing batch i - 1 overlap (pinned double buffers).
+    Returns the number of files.
     """
     from . import batch as _batch
     from .core import DEFAULT_PARAMS
@@ -202,15 +208,46 @@ def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=N
     params = params or DEFAULT_PARAMS
     if mode not in ("gray", "global", "local"):
         raise ValueError(f"unknown mode {mode!r} (use 'gray', 'global' or 'local')")
-    for k in range(0, len(src_paths), batch):
-        rgb = read_pnm_batch(src_paths[k:k + batch], threads=threads)
-        if rgb.ndim != 4:
-            raise CodecError(f"{src_paths[k]}: decolor_files needs rgb (P6) inputs")
-        if mode == "gray":
-            out = _batch.decolor_host(rgb, params, device=device)
-        elif mode == "global":
-            out = _batch.decolor_tone_host(rgb, curve or SigmoidCurve(), params, device=device)
-        else:
-            out = _batch.decolor_tone_local_host(rgb, grid, params, device=device)
-        write_pnm_batch(dst_paths[k:k + batch], out, threads=threads)
+    groups = [(src_paths[k:k + batch], dst_paths[k:k + batch]) for k in range(0, len(src_paths), batch)]
+    # Three-stage pipeline over the batches: the native reader fills pinned
+    # buffer (i + 1) % 2 and the native writer drains output buffer (i - 1) % 2
+    # on two worker threads (the C calls release the GIL) while this thread
+    # runs batch i through the device.
+    bufs = {}
+
+    def buf(slot, kind, shape):
+        b = bufs.get((slot, kind))
+        if b is None or b.shape != shape:
+            b = bufs[(slot, kind)] = _empty_batch(shape, True)
+        return b
+
+    def read(i):
+        paths = groups[i][0]
+        h, w, c = pnm_info(paths[0])
+        shape = (len(paths), h, w, 3) if c == 3 else (len(paths), h, w)
+        return read_pnm_batch(paths, threads=threads, out=buf(i % 2, "in", shape))
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=2) as pool:
+        nxt = pool.submit(read, 0) if groups else None
+        writes = [None, None]
+        for i in range(len(groups)):
+            rgb = nxt.result()
+            if rgb.ndim != 4:
+                raise CodecError(f"{groups[i][0][0]}: decolor_files needs rgb (P6) inputs")
+            if i + 1 < len(groups):
+                nxt = pool.submit(read, i + 1)  # its input slot's last reader (batch i - 1) is done
+            if writes[i % 2] is not None:
+                writes[i % 2].result()  # output slot free again
+            if mode == "gray":
+                out = _batch.decolor_host(rgb, params, out=buf(i % 2, "out", rgb.shape[:-1]), device=device)
+            elif mode == "global":
+                out = _batch.decolor_tone_host(rgb, curve or SigmoidCurve(), params, device=device)
+            else:
+                out = _batch.decolor_tone_local_host(rgb, grid, params, device=device)
+            writes[i % 2] = pool.submit(write_pnm_batch, groups[i][1], out, threads)
+        for f in writes:
+            if f is not None:
+                f.result()
     return len(src_paths)
