@@ -285,13 +285,23 @@ def luma_host(rgb, method: str = "y", device: int | None = None):
     return out
 
 
+def _host_out(out, shape):
+    """A caller's destination array (pinned keeps the copies asynchronous) or a new one."""
+    if out is None:
+        return np.empty(shape, dtype=np.uint8)
+    if out.shape != tuple(shape) or out.dtype != np.uint8 or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"out must be C-contiguous uint8 of shape {tuple(shape)}")
+    return out
+
+
 def decolor_tone_local_host(rgb, grid=None, params: DecolorParams = DEFAULT_PARAMS, return_gray: bool = False,
-                            device: int | None = None):
-    """:func:`decolor_tone_local` on a host uint8 (N, H, W, 3) / (H, W, 3) array (pipelined per image)."""
+                            device: int | None = None, out=None):
+    """:func:`decolor_tone_local` on a host uint8 (N, H, W, 3) / (H, W, 3) array (pipelined per image);
+    ``out``: optional destination for the toned batch."""
     arr = _host_rgb(rgb, ("uint8",))
     n, h, w = _nhw(arr.shape)
     g = _grid_for(h, w, grid)
-    toned = np.empty(arr.shape[:-1], dtype=np.uint8)
+    toned = _host_out(out, arr.shape[:-1])
     gray = np.empty_like(toned) if return_gray else None
     _lib.call("wg_host_decolor_tone_local_u8", arr.ctypes.data, toned.ctypes.data,
               gray.ctypes.data if gray is not None else None, n, h, w, params.beta_r, params.beta_k,
@@ -301,14 +311,15 @@ def decolor_tone_local_host(rgb, grid=None, params: DecolorParams = DEFAULT_PARA
 
 def decolor_tone_host(rgb, curve: SigmoidCurve = SigmoidCurve(),
                       params: DecolorParams = DEFAULT_PARAMS, return_gray: bool = False,
-                      device: int | None = None, return_rgb: bool = False):
+                      device: int | None = None, return_rgb: bool = False, out=None):
     """Fused decolor + global sigmoid of a host uint8 (..., 3) array -> toned uint8 (+ gray).
 
     With ``return_rgb`` returns ``(toned, gray, rgb_out)`` (gray None unless
-    requested), rgb_out the reinstated colour image as uint8.
+    requested), rgb_out the reinstated colour image as uint8. ``out``:
+    optional destination for the toned array.
     """
     arr = _host_rgb(rgb, ("uint8",))
-    toned = np.empty(arr.shape[:-1], dtype=np.uint8)
+    toned = _host_out(out, arr.shape[:-1])
     gray = np.empty_like(toned) if return_gray else None
     rgb_out = np.empty_like(arr) if return_rgb else None
     dev = get_device() if device is None else device

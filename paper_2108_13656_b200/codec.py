@@ -240,12 +240,13 @@ def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=N
                 nxt = pool.submit(read, i + 1)  # its input slot's last reader (batch i - 1) is done
             if writes[i % 2] is not None:
                 writes[i % 2].result()  # output slot free again
+            dst = buf(i % 2, "out", rgb.shape[:-1])
             if mode == "gray":
-                out = _batch.decolor_host(rgb, params, out=buf(i % 2, "out", rgb.shape[:-1]), device=device)
+                out = _batch.decolor_host(rgb, params, out=dst, device=device)
             elif mode == "global":
-                out = _batch.decolor_tone_host(rgb, curve or SigmoidCurve(), params, device=device)
+                out = _batch.decolor_tone_host(rgb, curve or SigmoidCurve(), params, device=device, out=dst)
             else:
-                out = _batch.decolor_tone_local_host(rgb, grid, params, device=device)
+                out = _batch.decolor_tone_local_host(rgb, grid, params, device=device, out=dst)
             writes[i % 2] = pool.submit(write_pnm_batch, groups[i][1], out, threads)
         for f in writes:
             if f is not None:
