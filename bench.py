@@ -15,18 +15,22 @@ Keys beyond the base contract:
                 duration from CUDA events on the launching stream, against
                 MEASURED_PEAKS.json hbm_gbs; traffic = ncu dram bytes / launch
                 from profiles/ when a capture for this workload is committed.
-  cpu_baseline  the CPU oracle port (oracle/warmgray_oracle.c, scalar fp64,
-                the reference's arithmetic) on all host cores, rank 0 at N=1,
-                over a bounded sample of the same workload.
+  cpu_baseline  the reference's own CPU path on all host cores, rank 0 at N=1,
+                over a bounded sample of the same workload: its _kernels.pyx
+                compiled into oracle/_ref by oracle/build_ref.py, driven as
+                decolor_image / dequantize_u8 / quantize_u8 do (kind
+                "reference", plus kernel_only_gpix_s); the oracle port
+                (oracle/warmgray_oracle.c, bit-identical) where that is not
+                built or for the HDR adapter, which the reference lacks.
   e2e           the same metric through the public host-array API
                 (paper_2108_13656_b200.decolor_host -> wg_host_decolor_u8):
                 pinned host input -> H2D -> kernel -> D2H every step.
   clocks        NVML SM clock / throttle reasons sampled during the timed region.
 
---impl reference: the reference's CPU implementation of the path, i.e. the
-oracle port (the reference's Cython kernel cannot travel to the GPU box; the
-port is bit-identical to it, tests/test_oracle_golden.py) on every host core,
-timed on the same workload/metric; rank 0 only.
+--impl reference: the same reference CPU path (kind "reference" when
+oracle/_ref is built -- it travels to the GPU box with the snapshot --, else
+the bit-identical oracle port) on every host core, timed on the same
+workload/metric; rank 0 only.
 """
 
 from __future__ import annotations
@@ -121,18 +125,76 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------------ CPU legs (oracle port)
-def cpu_port_rate(workload, seconds: float = 10.0, max_images: int = 4):
-    """Gpix/s of the oracle port (fp64 scalar, the reference's arithmetic) on all host cores."""
+# ------------------------------------------------------------------ CPU legs
+def reference_fns(workload, threads: int):
+    """The reference's own CPU path for this workload, when its compiled kernels
+    are present (oracle/_ref, built from /root/reference by oracle/build_ref.py):
+    returns (end-to-end fn, kernel-only fn, label) or None.
+
+    End to end is what the reference's public API does for the metric: codec.py's
+    dequantize_u8 (u8 workloads), PlanarImage's validation (core.py:69-80),
+    core.decolor_image -- _kernels.decolor_rows over contiguous row chunks on a
+    thread pool of `threads` workers created per call (backend.run_rows) -- the
+    validation of the result, and quantize_u8 (or the fp32 cast). Kernel only
+    is decolor_rows over the same row chunks on pre-converted fp64 input.
+    The HDR adapter (C4) has no reference implementation: None.
+    """
     import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
 
-    from oracle import oracle
+    from oracle import build_ref
 
-    threads = oracle.default_threads()
-    rgb, desc = cpu_sample(workload, max_images)
-    fn = {"gray_u8": lambda x: oracle.decolor_u8(x, threads=threads),
-          "gray_f32": lambda x: oracle.decolor_f32in(x, threads=threads),
-          "hdr_u8": lambda x: oracle.hdr_u8(x, threads=threads)}[workload.output]
+    if workload.output not in ("gray_u8", "gray_f32"):
+        return None
+    try:
+        k = build_ref.load()
+    except ImportError:
+        return None
+
+    def validate(a):  # PlanarImage.__init__
+        if a.size and (not np.isfinite(a).all() or a.min() < 0.0 or a.max() > 1.0):
+            raise ValueError("image samples must lie in [0, 1]")
+
+    def run_rows(f, out):  # backend.run_rows: contiguous chunks, one pool per call
+        h = f.shape[0]
+        workers = max(1, min(threads, h))
+        chunk = -(-h // workers)
+        spans = [(r0, min(r0 + chunk, h)) for r0 in range(0, h, chunk)]
+        with ThreadPoolExecutor(max_workers=len(spans)) as pool:
+            list(pool.map(lambda sp: k.decolor_rows(f, out, 0.55, 0.8, sp[0], sp[1]), spans))
+
+    def decolor_image(f):
+        out = np.empty(f.shape[:2], dtype=np.float64)
+        run_rows(f, out)
+        validate(out)  # the returned PlanarImage
+        return out
+
+    if workload.output == "gray_u8":
+        def e2e(batch):
+            for img in batch:
+                f = img.astype(np.float64) / 255.0  # dequantize_u8
+                validate(f)
+                np.floor(np.clip(decolor_image(f), 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)  # quantize_u8
+    else:
+        def e2e(batch):
+            for img in batch:
+                f = np.ascontiguousarray(img, dtype=np.float64)
+                validate(f)
+                decolor_image(f).astype(np.float32)
+    cache = {}
+
+    def kernel(batch):
+        f = cache.get(id(batch))
+        if f is None:
+            f = cache[id(batch)] = [np.ascontiguousarray(img, dtype=np.float64) / (255.0 if img.dtype == np.uint8 else 1.0)
+                                    for img in batch]
+        for x in f:
+            run_rows(x, np.empty(x.shape[:2], dtype=np.float64))
+    return e2e, kernel, ("the reference's _kernels.pyx compiled by oracle/build_ref.py (cython + gcc -O3 as "
+                         "setup.py), driven as decolor_image / dequantize_u8 / quantize_u8 do")
+
+
+def _rate(fn, rgb, seconds):
     fn(rgb[:1])  # warm-up
     px = 0
     t0 = time.perf_counter()
@@ -142,7 +204,29 @@ def cpu_port_rate(workload, seconds: float = 10.0, max_images: int = 4):
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    return px / el / 1e9, threads, f"{desc}, repeated for {el:.1f} s ({px / 1e6:.0f} Mpx)"
+    return px / el / 1e9, el, px
+
+
+def cpu_port_rate(workload, seconds: float = 10.0, max_images: int = 4):
+    """Gpix/s of the reference's CPU path on all host cores: its compiled kernels
+    (oracle/_ref) when built, else the oracle port (fp64 scalar, bit-identical).
+    Returns (rate, threads, sample description, kind, extra)."""
+    from oracle import oracle
+
+    threads = oracle.default_threads()
+    rgb, desc = cpu_sample(workload, max_images)
+    ref = reference_fns(workload, threads)
+    if ref is not None:
+        e2e, kernel, label = ref
+        rate, el, px = _rate(e2e, rgb, seconds)
+        krate, _, _ = _rate(kernel, rgb, min(seconds, 5.0))
+        return (rate, threads, f"{desc}, repeated for {el:.1f} s ({px / 1e6:.0f} Mpx); {label}", "reference",
+                {"kernel_only_gpix_s": round(krate, 4)})
+    fn = {"gray_u8": lambda x: oracle.decolor_u8(x, threads=threads),
+          "gray_f32": lambda x: oracle.decolor_f32in(x, threads=threads),
+          "hdr_u8": lambda x: oracle.hdr_u8(x, threads=threads)}[workload.output]
+    rate, el, px = _rate(fn, rgb, seconds)
+    return rate, threads, f"{desc}, repeated for {el:.1f} s ({px / 1e6:.0f} Mpx)", "port", {}
 
 
 def cpu_model() -> str:
@@ -331,9 +415,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, cores, sample = cpu_port_rate(wl, seconds=args.cpu_seconds)
-        cpu = {"value": round(v, 4), "unit": "Gpix/s", "cores": cores, "kind": "port", "sample": sample,
-               "cpu_model": cpu_model()}
+        v, cores, sample, kind, extra = cpu_port_rate(wl, seconds=args.cpu_seconds)
+        cpu = {"value": round(v, 4), "unit": "Gpix/s", "cores": cores, "kind": kind, "sample": sample,
+               "cpu_model": cpu_model(), **extra}
 
     if rank == 0:
         line = {
@@ -493,16 +577,38 @@ def committed_traffic(workload: str):
 
 
 def run_reference(args, wl, steps, warmup, world):
-    """--impl reference: the reference's CPU path (oracle port, all host cores) on this workload."""
+    """--impl reference: the reference's CPU path on this workload, all host cores --
+    its own compiled kernels (oracle/_ref) driven as its public API does when
+    built, else the oracle port."""
+    import numpy as np
+
     from oracle import oracle
 
     threads = oracle.default_threads()
     rgb, desc = cpu_sample(wl, 1)
-    fn = {"gray_u8": lambda x: oracle.decolor_u8(x, threads=threads),
-          "gray_f32": lambda x: oracle.decolor_f32in(x, threads=threads),
-          "hdr_u8": lambda x: oracle.hdr_u8(x, threads=threads)}[wl.output]
+    ref = reference_fns(wl, threads)
+    kind, extra = "port", {}
+    if ref is not None:
+        fn, kernel, label = ref
+        kind = "reference"
+        krate, _, _ = _rate(kernel, rgb, 3.0)
+        extra = {"kernel_only_gpix_s": round(krate, 4)}
+        desc = f"{desc}; {label}"
+    else:
+        fn = {"gray_u8": lambda x: oracle.decolor_u8(x, threads=threads),
+              "gray_f32": lambda x: oracle.decolor_f32in(x, threads=threads),
+              "hdr_u8": lambda x: oracle.hdr_u8(x, threads=threads)}[wl.output]
     for _ in range(min(warmup, 3)):
         fn(rgb)
+    # bound the whole run to ~150 s: a step over more than that share of the
+    # image runs on its leading rows instead (same per-pixel work)
+    t1 = time.perf_counter()
+    fn(rgb)
+    per_step = time.perf_counter() - t1
+    if per_step * steps > 150.0:
+        rows = max(1, int(rgb.shape[1] * 150.0 / (per_step * steps)))
+        rgb = np.ascontiguousarray(rgb[:, :rows])
+        desc = f"{desc}; rows 0..{rows - 1} of each image so {steps} steps fit in ~150 s"
     t0 = time.perf_counter()
     for _ in range(steps):
         fn(rgb)
@@ -517,8 +623,8 @@ def run_reference(args, wl, steps, warmup, world):
         "config": {"workload": f"{wl.name}: 1 x {wl.width}x{wl.height} RGB {wl.dtype} -> {wl.output} per step (bounded sample)",
                    "images_per_gpu": wl.n_images, "height": wl.height, "width": wl.width,
                    "io": f"{wl.dtype}->{wl.output}"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "Gpix/s", "cores": threads, "kind": "port",
-                         "sample": desc + " per step", "cpu_model": cpu_model()},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Gpix/s", "cores": threads, "kind": kind,
+                         "sample": desc + " per step", "cpu_model": cpu_model(), **extra},
         "e2e": {"value": round(value, 4), "unit": "Gpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))

@@ -172,3 +172,37 @@ def test_synth_generators_restatement():
     # a pixel sitting on seed 0 belongs to cell 0 (distance 0, lowest index wins ties)
     x, y = xy[0, 0]
     assert np.abs(v[0, y, x].astype(int) - col[0, 0].astype(int)).max() <= 4
+
+
+def _ref_kernels():
+    from oracle import build_ref
+
+    try:
+        return build_ref.load()
+    except ImportError:
+        pytest.skip("oracle/_ref (the reference's compiled kernels) not built")
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_oracle_equals_compiled_reference(seed):
+    """Pin the oracle against the reference's own _kernels.pyx compiled by
+    oracle/build_ref.py: every row kernel, bit for bit, on random images with
+    black / white / grey pixels."""
+    k = _ref_kernels()
+    rng = np.random.default_rng(seed)
+    img = rng.random((41, 67, 3))
+    img[0, :5] = 0.0
+    img[1, :5] = 1.0
+    img[2, :5] = img[2, :5, :1]
+    h, w = img.shape[:2]
+    out = np.empty((h, w))
+    k.decolor_rows(img, out, 0.55, 0.8, 0, h)
+    assert np.array_equal(out, oracle.decolor_f64(img))
+    k.decolor_rows(img, out, 0.7, 0.9, 0, h)
+    assert np.array_equal(out, oracle.decolor_f64(img, 0.7, 0.9))
+    for name, method in (("bt601_rows", "y"), ("hsv_value_rows", "v"), ("lab_lightness_rows", "lab")):
+        getattr(k, name)(img, out, 0, h)
+        assert np.array_equal(out, oracle.luma_f64(img, method)), name
+    lab = np.empty((h, w, 3))
+    k.lab_rows(img, lab, 0, h)
+    assert np.array_equal(lab, oracle.lab_f64(img))
