@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -792,7 +793,7 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
     const Theta theta = make_theta(midpoint, slope);
     const int sms = sm_count(device);
     const bool tiled = (pix_per_img % 1024) == 0 && (reinterpret_cast<uintptr_t>(rgb) & 15) == 0;
-    static int fused_occ[kMaxDevices] = {0};
+    static std::atomic<int> fused_occ[kMaxDevices];  // idempotent lazy cache
     if (tiled && fused_enabled() && device >= 0 && device < kMaxDevices) {
         if (!fused_occ[device]) {
             int coop = 0;
@@ -891,14 +892,14 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
         const bool discard = static_cast<size_t>(g) * pix_per_img * sizeof(float) <= (size_t(96) << 20) &&
                              !getenv("WG_HDR_NO_DISCARD");
         if (pix_per_img % kToneTilePx == 0 && getenv("WG_HDR_TILED")) {
-            static int tone_occ[kMaxDevices] = {0};
+            static std::atomic<int> tone_occ[kMaxDevices];  // idempotent lazy cache
             if (device >= 0 && device < kMaxDevices && !tone_occ[device]) {
                 cudaFuncSetAttribute(hdr_tone_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kToneSmem);
                 int occ = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hdr_tone_tiled_kernel, kT, kToneSmem);
                 tone_occ[device] = std::max(occ, 1);
             }
-            const int occ = device >= 0 && device < kMaxDevices ? tone_occ[device] : 1;
+            const int occ = device >= 0 && device < kMaxDevices ? tone_occ[device].load() : 1;
             const int64_t ntiles = pix_per_img / kToneTilePx;
             const int64_t bt2 = std::max<int64_t>(1, std::min<int64_t>(ntiles, (static_cast<int64_t>(occ) * sms + g - 1) / g));
             hdr_tone_tiled_kernel<<<dim3(static_cast<unsigned>(bt2), static_cast<unsigned>(g)), kT, kToneSmem, sb>>>(

@@ -11,6 +11,8 @@
 // grown on demand (the device-buffer manager), guarded by a per-device mutex.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -51,17 +53,18 @@ static int cuda_fail(cudaError_t e, const char* what) {
 }
 
 int sm_count(int device) {
-    static int cache[kMaxDevices] = {0};
+    // idempotent lazy cache; relaxed atomics keep concurrent first calls race-free
+    static std::atomic<int> cache[kMaxDevices];
     if (device < 0 || device >= kMaxDevices) return 148;
-    if (!cache[device]) {
+    if (!cache[device].load(std::memory_order_relaxed)) {
         int n = 0;
         if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0) {
             cudaGetLastError();
             n = 148;
         }
-        cache[device] = n;
+        cache[device].store(n, std::memory_order_relaxed);
     }
-    return cache[device];
+    return cache[device].load(std::memory_order_relaxed);
 }
 
 int check_npix(int64_t n) {

@@ -2,6 +2,8 @@
 // libwarmgray_b200.so (error reporting, argument checks, device info).
 #pragma once
 
+#include <mutex>
+
 #include <cstdint>
 
 namespace wg {
@@ -24,7 +26,8 @@ int check_curve(double midpoint, double slope);   // tonemap.py:22-33
 struct U8Exact;
 // Near-tie table of the bit-exact uint8 decolor for (beta_r, beta_k) on the
 // current device (csrc/wg_u8exact.cu); built on first use, then cached.
-int u8exact_get(double beta_r, double beta_k, U8Exact* out);
+// `hold` returns locked; keep it until the kernel using the table is enqueued.
+int u8exact_get(double beta_r, double beta_k, U8Exact* out, std::unique_lock<std::mutex>* hold);
 
 }  // namespace wg
 

@@ -13,6 +13,8 @@
 // :195-216 (tonemap_image global), codec.py:22-29 (quantize / dequantize).
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -310,7 +312,8 @@ extern "C" int wg_decolor_u8_exact(const uint8_t* rgb, uint8_t* gray, int64_t np
     WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, gray) || check_params(beta_r, beta_k));
     if (npix == 0) return WG_OK;
     U8Exact ex;
-    const int rc = u8exact_get(beta_r, beta_k, &ex);
+    std::unique_lock<std::mutex> hold;  // keeps the cached table alive until the launch is enqueued
+    const int rc = u8exact_get(beta_r, beta_k, &ex, &hold);
     if (rc != WG_OK) return rc;
     OpDecolorU8Exact op{rgb, gray, make_u8_consts(beta_r, beta_k), ex};
     const void* outs[1] = {gray};

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <type_traits>
 
@@ -156,20 +157,22 @@ __global__ void __launch_bounds__(kThreads) scalar_kernel(Op op, int64_t npix) {
 // ------------------------------------------------------------------ launch helpers
 template <class Op>
 static int stream_grid(int device) {
-    static int occ_cache[kMaxDevices] = {0};
-    static int attr_set[kMaxDevices] = {0};
-    if (!attr_set[device]) {
+    // idempotent lazy caches; relaxed atomics keep concurrent first calls race-free
+    static std::atomic<int> occ_cache[kMaxDevices];
+    static std::atomic<int> attr_set[kMaxDevices];
+    if (!attr_set[device].load(std::memory_order_relaxed)) {
         cudaFuncSetAttribute(stream_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSmemBytes);
-        attr_set[device] = 1;
+        attr_set[device].store(1, std::memory_order_relaxed);
     }
-    if (!occ_cache[device]) {
-        int occ = 0;
+    int occ = occ_cache[device].load(std::memory_order_relaxed);
+    if (!occ) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_kernel<Op>, kThreads,
                                                       kSmemBytes);
-        occ_cache[device] = std::max(occ, 1);
+        occ = std::max(occ, 1);
+        occ_cache[device].store(occ, std::memory_order_relaxed);
     }
-    return occ_cache[device] * sm_count(device);
+    return occ * sm_count(device);
 }
 
 template <class Op>

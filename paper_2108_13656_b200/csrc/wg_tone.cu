@@ -190,11 +190,14 @@ Entry g_cache[kMaxDevices][kCache];
 int g_next[kMaxDevices];
 std::mutex g_mu;
 
-int tone_table(double m, double k, const ToneTable** out, bool* multi) {
+// The table stays valid while *hold is locked: the caller enqueues its kernel
+// before releasing it, so an eviction by another thread (cudaFree, which waits
+// for the device's queued work) cannot free a table a pending launch uses.
+int tone_table(double m, double k, const ToneTable** out, bool* multi, std::unique_lock<std::mutex>* hold) {
     int device = 0;
     cudaGetDevice(&device);
     if (device < 0 || device >= kMaxDevices) return set_error(WG_ENODEV, "device ordinal out of range");
-    std::lock_guard<std::mutex> lock(g_mu);
+    *hold = std::unique_lock<std::mutex>(g_mu);
     for (Entry& e : g_cache[device])
         if (e.used && e.m == m && e.k == k) {
             *out = e.dev;
@@ -618,7 +621,8 @@ extern "C" int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* g
     if (npix == 0) return WG_OK;
     const ToneTable* tab = nullptr;
     bool multi = false;
-    const int rc = tone_table(midpoint, slope, &tab, &multi);
+    std::unique_lock<std::mutex> hold;  // keeps the cached table alive until the launch is enqueued
+    const int rc = tone_table(midpoint, slope, &tab, &multi, &hold);
     if (rc != WG_OK) return rc;
     const U8Consts k = make_u8_consts(beta_r, beta_k);
     const void* outs[2] = {toned, gray_or_null};

@@ -124,11 +124,14 @@ int build(int device, double br, double bk, U8Exact* out) {
 }  // namespace
 
 // The table for (beta_r, beta_k) on the current device, built on first use.
-int u8exact_get(double beta_r, double beta_k, U8Exact* out) {
+// *hold stays locked: the caller enqueues its kernel before releasing it, so an
+// eviction by another thread (cudaFree waits for queued work) cannot free a
+// table that a pending launch uses.
+int u8exact_get(double beta_r, double beta_k, U8Exact* out, std::unique_lock<std::mutex>* hold) {
     int device = 0;
     cudaGetDevice(&device);
     if (device < 0 || device >= kMaxDevices) return set_error(WG_ENODEV, "device ordinal out of range");
-    std::lock_guard<std::mutex> lock(g_mu);
+    *hold = std::unique_lock<std::mutex>(g_mu);
     for (Entry& en : g_cache[device])
         if (en.used && en.br == beta_r && en.bk == beta_k) {
             *out = en.t;
@@ -156,7 +159,8 @@ using namespace wg;
 extern "C" int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, uint32_t* slots) {
     WG_CHECK_ARGS(check_params(beta_r, beta_k));
     U8Exact t;
-    const int rc = u8exact_get(beta_r, beta_k, &t);
+    std::unique_lock<std::mutex> hold;
+    const int rc = u8exact_get(beta_r, beta_k, &t, &hold);
     if (rc != WG_OK) return rc;
     if (margin) *margin = t.margin;
     if (slots) *slots = t.mask + 1;

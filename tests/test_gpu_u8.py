@@ -340,6 +340,44 @@ def test_tone_rgb_u8_bound_headroom(torch_dev, cube, monkeypatch):
         assert n == [0, 0, 0]
 
 
+def test_table_caches_under_concurrent_eviction(torch_dev):
+    """Threads on their own streams cycle through more tone curves (cache of 8)
+    and exact-u8 parameter pairs (cache of 4) than the per-device caches hold:
+    a table stays alive until the launch that uses it is enqueued, so every
+    result equals the single-threaded one."""
+    import threading
+
+    import paper_2108_13656_b200 as wg
+
+    torch, dev = torch_dev
+    rgb = torch.randint(0, 256, (64, 1024, 3), dtype=torch.uint8, device=dev)
+    curves = [wg.SigmoidCurve(0.3 + 0.02 * i, 4.0 + i) for i in range(12)]
+    pairs = [wg.DecolorParams(0.55 + 0.03 * i, 0.8 - 0.02 * i) for i in range(6)]
+    want_t = [wg.decolor_tone(rgb, c) for c in curves]
+    want_e = [wg.decolor(rgb, p, exact=True) for p in pairs]
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(seed):
+        s = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(s):
+            for it in range(8):
+                i = (seed * 5 + it) % len(curves)
+                j = (seed * 3 + it) % len(pairs)
+                t = wg.decolor_tone(rgb, curves[i], stream=s)
+                e = wg.decolor(rgb, pairs[j], exact=True, stream=s)
+                s.synchronize()
+                if not torch.equal(t, want_t[i]) or not torch.equal(e, want_e[j]):
+                    errors.append((seed, it))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors
+
+
 def test_empty_and_errors(torch_dev):
     import paper_2108_13656_b200 as wg
 
