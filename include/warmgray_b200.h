@@ -112,10 +112,12 @@ WG_API int wg_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_o
 WG_API int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null, int64_t npix,
                        float beta_r, float beta_k, float midpoint, float slope, void* stream);
 
-/* Colour output of the global tone map on uint8: rgb_out = quantize_u8 of
- * tonemap_image(mode="global")'s reinstated RGB (tonemap.py:172-216), toned /
- * gray optional. Evaluates the reference's fp64 chain per pixel (the ratio
- * l_out / l_in amplifies fp32 error past the parity bar): FP64-bound. */
+/* Exact global tone map on uint8, bit-identical to the reference: rgb_out =
+ * quantize_u8 of tonemap_image(mode="global")'s reinstated RGB
+ * (tonemap.py:172-216), toned = quantize_u8 of its l_out, gray = quantize_u8
+ * of l_in; each output may be null (at least one requested). fp32 with a
+ * rigorous per-pixel error bound; pixels in doubt take the reference's fp64
+ * chain. */
 WG_API int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned_or_null,
                                   uint8_t* gray_or_null, int64_t npix, double beta_r, double beta_k,
                                   double midpoint, double slope, void* stream);

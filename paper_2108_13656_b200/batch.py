@@ -81,12 +81,15 @@ def decolor(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, stream=None, 
 
 
 def decolor_tone(rgb, curve: SigmoidCurve = SigmoidCurve(), params: DecolorParams = DEFAULT_PARAMS,
-                 return_gray: bool = False, return_rgb: bool = False, stream=None):
+                 return_gray: bool = False, return_rgb: bool = False, stream=None, exact: bool = False):
     """Fused decolor + global sigmoid on a device batch.
 
     uint8 -> toned uint8 (and gray uint8 if ``return_gray``; with
     ``return_rgb`` also the reinstated colour image as uint8, i.e.
-    quantize_u8 of tonemap_image(mode="global")[0], via the fp64 chain);
+    quantize_u8 of tonemap_image(mode="global")[0]). The default uint8 route
+    meets the north-star bar (+-1 on <= 0.01% of pixels); ``exact=True`` (and
+    every ``return_rgb`` call) is bit-identical to the reference (fp32 with a
+    rigorous error bound, the fp64 chain for pixels in doubt).
     float32 -> toned float32 (+ gray, + reinstated rgb if requested).
     Returns the toned tensor, or a tuple ``(toned, gray, rgb_out)`` with
     ``None`` for outputs not requested when either flag is set.
@@ -99,12 +102,12 @@ def decolor_tone(rgb, curve: SigmoidCurve = SigmoidCurve(), params: DecolorParam
     rgb_out = None
     with torch.cuda.device(rgb.device):
         st = _stream(stream, rgb.device)
-        if name == "uint8" and return_rgb:
-            # colour output: the reference's fp64 chain per pixel (wg_decolor_tone_rgb_u8)
-            rgb_out = torch.empty_like(rgb)
-            _lib.call("wg_decolor_tone_rgb_u8", rgb.data_ptr(), rgb_out.data_ptr(), toned.data_ptr(),
-                      gray.data_ptr() if gray is not None else None, toned.numel(), params.beta_r, params.beta_k,
-                      curve.midpoint, curve.slope, st)
+        if name == "uint8" and (return_rgb or exact):
+            # bit-identical route (wg_decolor_tone_rgb_u8; the colour image only when asked)
+            rgb_out = torch.empty_like(rgb) if return_rgb else None
+            _lib.call("wg_decolor_tone_rgb_u8", rgb.data_ptr(), rgb_out.data_ptr() if rgb_out is not None else None,
+                      toned.data_ptr(), gray.data_ptr() if gray is not None else None, toned.numel(), params.beta_r,
+                      params.beta_k, curve.midpoint, curve.slope, st)
         elif name == "uint8":
             _lib.call("wg_decolor_tone_u8", rgb.data_ptr(), toned.data_ptr(),
                       gray.data_ptr() if gray is not None else None, toned.numel(),
@@ -311,20 +314,22 @@ def decolor_tone_local_host(rgb, grid=None, params: DecolorParams = DEFAULT_PARA
 
 def decolor_tone_host(rgb, curve: SigmoidCurve = SigmoidCurve(),
                       params: DecolorParams = DEFAULT_PARAMS, return_gray: bool = False,
-                      device: int | None = None, return_rgb: bool = False, out=None):
+                      device: int | None = None, return_rgb: bool = False, out=None, exact: bool = False):
     """Fused decolor + global sigmoid of a host uint8 (..., 3) array -> toned uint8 (+ gray).
 
     With ``return_rgb`` returns ``(toned, gray, rgb_out)`` (gray None unless
     requested), rgb_out the reinstated colour image as uint8. ``out``:
-    optional destination for the toned array.
+    optional destination for the toned array. ``exact``: bit-identical toned
+    (and gray) bytes, as with ``return_rgb``.
     """
     arr = _host_rgb(rgb, ("uint8",))
     toned = _host_out(out, arr.shape[:-1])
     gray = np.empty_like(toned) if return_gray else None
     rgb_out = np.empty_like(arr) if return_rgb else None
     dev = get_device() if device is None else device
-    if toned.size and return_rgb:
-        _lib.call("wg_host_decolor_tone_rgb_u8", arr.ctypes.data, rgb_out.ctypes.data, toned.ctypes.data,
+    if toned.size and (return_rgb or exact):  # bit-identical route
+        _lib.call("wg_host_decolor_tone_rgb_u8", arr.ctypes.data,
+                  rgb_out.ctypes.data if rgb_out is not None else None, toned.ctypes.data,
                   gray.ctypes.data if gray is not None else None, toned.size, params.beta_r,
                   params.beta_k, curve.midpoint, curve.slope, dev)
     elif toned.size:

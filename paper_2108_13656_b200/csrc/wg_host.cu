@@ -389,8 +389,10 @@ extern "C" int wg_host_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8
 extern "C" int wg_host_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned_or_null,
                                            uint8_t* gray_or_null, int64_t npix, double beta_r, double beta_k,
                                            double midpoint, double slope, int device) {
-    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, rgb_out) || check_params(beta_r, beta_k) ||
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, rgb) || check_params(beta_r, beta_k) ||
                   check_curve(midpoint, slope));
+    if (npix > 0 && !rgb_out && !toned_or_null && !gray_or_null)
+        return set_error(WG_EINVAL, "decolor_tone_rgb_u8: no output requested");
     HostIn in[1] = {{rgb, 3}};
     HostOut o[3] = {{rgb_out, 3}, {toned_or_null, 1}, {gray_or_null, 1}};
     return host_pipeline(device, npix, in, 1, o, 3, 256, no_scratch,

@@ -286,7 +286,8 @@ struct ToneRgbF {
     float ycut;     // -0.25 log2(e): the series below |y| < |ycut| (kx < 1/4)
     float cn255;    // 255 / (sig(k(1-m)) (1 - e^{-k}))
     float cA, cC, cD;  // rel(N) <= omS (L cA + cC) + cD
-    float relRgb;      // rel(v_rgb) = rel(N) + relRgb (toned uses the same)
+    float relRgb;      // rel(v_rgb) = rel(N) + relRgb (toned shares it when rgb is produced)
+    float relT;        // rel(v_toned) = rel(N) + relT when only toned / gray are produced
     float glo, ghi;    // gray scales 1 -/+ rel(L)
 };
 
@@ -329,9 +330,11 @@ static __device__ __noinline__ void tone_rgb_px(const uint8_t* __restrict__ rgb,
     const double lout = sigmoid_d(li, sig);
     const double ratio = __ddiv_rn(lout, li > 1e-6 ? li : 1e-6);
     const bool black = li == 0.0;
-    rgb_out[3 * p] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(r, ratio)));
-    rgb_out[3 * p + 1] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(g, ratio)));
-    rgb_out[3 * p + 2] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(b, ratio)));
+    if (rgb_out) {
+        rgb_out[3 * p] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(r, ratio)));
+        rgb_out[3 * p + 1] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(g, ratio)));
+        rgb_out[3 * p + 2] = black ? 0 : static_cast<uint8_t>(quantize_d(__dmul_rn(b, ratio)));
+    }
     if (toned) toned[p] = static_cast<uint8_t>(quantize_d(lout));
     if (gray) gray[p] = static_cast<uint8_t>(quantize_d(li));
 }
@@ -355,7 +358,7 @@ struct PairOut {
     float2 r, g, b, t, y;
     uint32_t crossed0, crossed1;
 };
-template <bool kTwoEx2, bool kToned, bool kGray>
+template <bool kTwoEx2, bool kRgb, bool kToned, bool kGray>
 __device__ __forceinline__ PairOut tone_rgb_pair(float2 R, float2 G, float2 B, const ToneRgbF& c) {
     const float2 M2 = bc2(kMagic), one2 = bc2(1.0f);
     // decolor
@@ -392,22 +395,24 @@ __device__ __forceinline__ PairOut tone_rgb_pair(float2 R, float2 G, float2 B, c
     }
     const float2 N255 = mul2(mul2(sg, omE), bc2(c.cn255));
     // error bound -> one scale pair for the rgb and toned values
-    const float2 relC = fma2(omS, fma2(L, bc2(c.cA), bc2(c.cC)), bc2(c.cD + c.relRgb));
+    const float2 relC = fma2(omS, fma2(L, bc2(c.cA), bc2(c.cC)), bc2(c.cD + (kRgb ? c.relRgb : c.relT)));
     const float2 cl = fma2(relC, bc2(-1.0f), one2), ch = add2(relC, one2);
     // outputs
-    const float2 rs = mul2(N255, invL);
-    const float2 vR = mul2(R, rs), vG = mul2(G, rs), vB = mul2(B, rs);
-    const float2 vr = make_float2(fminf(vR.x, 255.0f), fminf(vR.y, 255.0f));
-    const float2 vg = make_float2(fminf(vG.x, 255.0f), fminf(vG.y, 255.0f));
-    const float2 vb = make_float2(fminf(vB.x, 255.0f), fminf(vB.y, 255.0f));
     PairOut o;
-    o.r = fma2(vr, cl, M2);
-    o.g = fma2(vg, cl, M2);
-    o.b = fma2(vb, cl, M2);
     uint32_t x0 = 0, x1 = 0;
-    crossed(o.r, fma2(vr, ch, M2), x0, x1);
-    crossed(o.g, fma2(vg, ch, M2), x0, x1);
-    crossed(o.b, fma2(vb, ch, M2), x0, x1);
+    if constexpr (kRgb) {
+        const float2 rs = mul2(N255, invL);
+        const float2 vR = mul2(R, rs), vG = mul2(G, rs), vB = mul2(B, rs);
+        const float2 vr = make_float2(fminf(vR.x, 255.0f), fminf(vR.y, 255.0f));
+        const float2 vg = make_float2(fminf(vG.x, 255.0f), fminf(vG.y, 255.0f));
+        const float2 vb = make_float2(fminf(vB.x, 255.0f), fminf(vB.y, 255.0f));
+        o.r = fma2(vr, cl, M2);
+        o.g = fma2(vg, cl, M2);
+        o.b = fma2(vb, cl, M2);
+        crossed(o.r, fma2(vr, ch, M2), x0, x1);
+        crossed(o.g, fma2(vg, ch, M2), x0, x1);
+        crossed(o.b, fma2(vb, ch, M2), x0, x1);
+    }
     if constexpr (kToned) {
         o.t = fma2(N255, cl, M2);
         crossed(o.t, fma2(N255, ch, M2), x0, x1);
@@ -421,7 +426,7 @@ __device__ __forceinline__ PairOut tone_rgb_pair(float2 R, float2 G, float2 B, c
     return o;
 }
 
-template <bool kTwoEx2, bool kToned, bool kGray>
+template <bool kTwoEx2, bool kRgb, bool kToned, bool kGray>
 __global__ void __launch_bounds__(256, 3)
     tone_rgb_fast_kernel(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ rgb_out,
                          uint8_t* __restrict__ toned, uint8_t* __restrict__ gray, int64_t ntiles, int64_t npix,
@@ -462,11 +467,13 @@ __global__ void __launch_bounds__(256, 3)
             const float2 RB = add2(make_float2(byte_biased(w1, 2), byte_biased(w2, 1)), mM);
             const float2 GB = add2(make_float2(byte_biased(w1, 3), byte_biased(w2, 2)), mM);
             const float2 BB = add2(make_float2(byte_biased(w2, 0), byte_biased(w2, 3)), mM);
-            const PairOut a = tone_rgb_pair<kTwoEx2, kToned, kGray>(RA, GA, BA, c);
-            const PairOut b = tone_rgb_pair<kTwoEx2, kToned, kGray>(RB, GB, BB, c);
-            o[3 * q] = pack4(a.r.x, a.g.x, a.b.x, a.r.y);
-            o[3 * q + 1] = pack4(a.g.y, a.b.y, b.r.x, b.g.x);
-            o[3 * q + 2] = pack4(b.b.x, b.r.y, b.g.y, b.b.y);
+            const PairOut a = tone_rgb_pair<kTwoEx2, kRgb, kToned, kGray>(RA, GA, BA, c);
+            const PairOut b = tone_rgb_pair<kTwoEx2, kRgb, kToned, kGray>(RB, GB, BB, c);
+            if constexpr (kRgb) {
+                o[3 * q] = pack4(a.r.x, a.g.x, a.b.x, a.r.y);
+                o[3 * q + 1] = pack4(a.g.y, a.b.y, b.r.x, b.g.x);
+                o[3 * q + 2] = pack4(b.b.x, b.r.y, b.g.y, b.b.y);
+            }
             if constexpr (kToned) ot[q] = pack4(a.t.x, a.t.y, b.t.x, b.t.y);
             if constexpr (kGray) og[q] = pack4(a.y.x, a.y.y, b.y.x, b.y.y);
             mask |= (a.crossed0 ? 1u : 0u) << (4 * q);
@@ -475,10 +482,12 @@ __global__ void __launch_bounds__(256, 3)
             mask |= (b.crossed1 ? 1u : 0u) << (4 * q + 3);
         }
         const int64_t p0 = t * kRgbTile + static_cast<int64_t>(tid) * kRgbPx;
-        uint4* orgb = reinterpret_cast<uint4*>(rgb_out + p0 * 3);
-        __stcs(orgb, make_uint4(o[0], o[1], o[2], o[3]));
-        __stcs(orgb + 1, make_uint4(o[4], o[5], o[6], o[7]));
-        __stcs(orgb + 2, make_uint4(o[8], o[9], o[10], o[11]));
+        if constexpr (kRgb) {
+            uint4* orgb = reinterpret_cast<uint4*>(rgb_out + p0 * 3);
+            __stcs(orgb, make_uint4(o[0], o[1], o[2], o[3]));
+            __stcs(orgb + 1, make_uint4(o[4], o[5], o[6], o[7]));
+            __stcs(orgb + 2, make_uint4(o[8], o[9], o[10], o[11]));
+        }
         if constexpr (kToned) __stcs(reinterpret_cast<uint4*>(toned + p0), make_uint4(ot[0], ot[1], ot[2], ot[3]));
         if constexpr (kGray) __stcs(reinterpret_cast<uint4*>(gray + p0), make_uint4(og[0], og[1], og[2], og[3]));
         if (__any_sync(0xFFFFFFFFu, mask != 0u)) {
@@ -549,27 +558,28 @@ bool make_tone_rgb_consts(double br, double bk, double m, double k, ToneRgbF* c,
     c->cC = static_cast<float>(sc * cC);
     c->cD = static_cast<float>(sc * cD);
     c->relRgb = static_cast<float>(sc * relRgb);
+    c->relT = static_cast<float>(sc * 3 * u);  // cn255 and the scale constants
     c->glo = static_cast<float>(1.0 - sc * (relL + 2 * u));
     c->ghi = static_cast<float>(1.0 + sc * (relL + 2 * u));
     return true;
 }
 
-template <bool kTwoEx2>
+template <bool kTwoEx2, bool kRgb>
 void launch_tone_rgb_fast(unsigned grid, cudaStream_t st, const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned,
                           uint8_t* gray, int64_t ntiles, int64_t npix, const ToneRgbF& c, double br, double bk,
                           const SigD& sig) {
     if (toned && gray)
-        tone_rgb_fast_kernel<kTwoEx2, true, true><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles, npix, c,
-                                                                        br, bk, sig);
+        tone_rgb_fast_kernel<kTwoEx2, kRgb, true, true><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles,
+                                                                              npix, c, br, bk, sig);
     else if (toned)
-        tone_rgb_fast_kernel<kTwoEx2, true, false><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles, npix, c,
-                                                                         br, bk, sig);
+        tone_rgb_fast_kernel<kTwoEx2, kRgb, true, false><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles,
+                                                                               npix, c, br, bk, sig);
     else if (gray)
-        tone_rgb_fast_kernel<kTwoEx2, false, true><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles, npix, c,
-                                                                         br, bk, sig);
+        tone_rgb_fast_kernel<kTwoEx2, kRgb, false, true><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles,
+                                                                               npix, c, br, bk, sig);
     else
-        tone_rgb_fast_kernel<kTwoEx2, false, false><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles, npix,
-                                                                          c, br, bk, sig);
+        tone_rgb_fast_kernel<kTwoEx2, kRgb, false, false><<<grid, 256, 0, st>>>(rgb, rgb_out, toned, gray, ntiles,
+                                                                                npix, c, br, bk, sig);
 }
 
 }  // namespace
@@ -580,8 +590,10 @@ using namespace wg;
 extern "C" int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint8_t* toned_or_null,
                                       uint8_t* gray_or_null, int64_t npix, double beta_r, double beta_k,
                                       double midpoint, double slope, void* stream) {
-    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, rgb_out) || check_params(beta_r, beta_k) ||
+    WG_CHECK_ARGS(check_npix(npix) || check_ptrs(npix, rgb, rgb) || check_params(beta_r, beta_k) ||
                   check_curve(midpoint, slope));
+    if (npix > 0 && !rgb_out && !toned_or_null && !gray_or_null)
+        return set_error(WG_EINVAL, "decolor_tone_rgb_u8: no output requested");
     if (npix == 0) return WG_OK;
     int device = 0;
     cudaGetDevice(&device);
@@ -595,17 +607,14 @@ extern "C" int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint
     ToneRgbF c;
     bool two_ex2 = false;
     const auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    const bool aligned = al(rgb) && al(rgb_out) && (!toned_or_null || al(toned_or_null)) &&
+    const bool aligned = al(rgb) && (!rgb_out || al(rgb_out)) && (!toned_or_null || al(toned_or_null)) &&
                          (!gray_or_null || al(gray_or_null));
     const int64_t ntiles = npix / kRgbTile;
     if (aligned && ntiles > 0 && make_tone_rgb_consts(beta_r, beta_k, midpoint, slope, &c, &two_ex2)) {
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ntiles, 3LL * sm_count(device)));
-        if (two_ex2)
-            launch_tone_rgb_fast<true>(grid, st, rgb, rgb_out, toned_or_null, gray_or_null, ntiles, npix, c, beta_r,
-                                       beta_k, sig);
-        else
-            launch_tone_rgb_fast<false>(grid, st, rgb, rgb_out, toned_or_null, gray_or_null, ntiles, npix, c, beta_r,
-                                        beta_k, sig);
+        auto launch = two_ex2 ? (rgb_out ? launch_tone_rgb_fast<true, true> : launch_tone_rgb_fast<true, false>)
+                              : (rgb_out ? launch_tone_rgb_fast<false, true> : launch_tone_rgb_fast<false, false>);
+        launch(grid, st, rgb, rgb_out, toned_or_null, gray_or_null, ntiles, npix, c, beta_r, beta_k, sig);
         return check_launch("tone_rgb_fast");
     }
     const unsigned blocks = static_cast<unsigned>(

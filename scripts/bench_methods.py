@@ -40,6 +40,7 @@ def main():
         "ours": lambda: wg.decolor(rgb, out=out.view(n)),
         "tone": lambda: wg.decolor_tone(rgb),
         "tone_rgb": lambda: wg.decolor_tone(rgb, return_rgb=True),
+        "tone_exact": lambda: wg.decolor_tone(rgb, exact=True),
         "y": lambda: wg.luma(rgb, "y"),
         "v": lambda: wg.luma(rgb, "v"),
         "lab": lambda: wg.luma(rgb, "lab"),

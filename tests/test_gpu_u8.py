@@ -269,6 +269,14 @@ def test_tone_rgb_u8_golden_and_cube(torch_dev, cube):
         n_g = int((gray.cpu().numpy() != want_g).sum())
         print(f"tone rgb cube m={m} k={k} betas {br}/{bk}: rgb diffs {n_o} toned diffs {n_t} gray diffs {n_g}")
         assert n_o == n_t == n_g == 0
+    # exact toned / gray without the colour image (rgb_out null): the same bytes
+    for m, k in [(0.5, 8.0), (0.6, 2000.0)]:
+        toned_e, gray_e, none = wg.decolor_tone(t, wg.SigmoidCurve(m, k), return_gray=True, exact=True)
+        assert none is None
+        _, want_t, want_g = oracle.tone_rgb_u8(cube, midpoint=m, slope=k, threads=oracle.default_threads())
+        assert np.array_equal(toned_e.cpu().numpy(), want_t) and np.array_equal(gray_e.cpu().numpy(), want_g)
+    assert np.array_equal(wg.decolor_tone(t, exact=True).cpu().numpy(),
+                          oracle.tone_rgb_u8(cube, threads=oracle.default_threads())[1])
     # toned-only request through the same kernel (gray pointer null)
     toned2, _, out2 = wg.decolor_tone(t, return_rgb=True)
     want_o, want_t, _ = oracle.tone_rgb_u8(cube, threads=oracle.default_threads())
@@ -284,6 +292,7 @@ def test_tone_rgb_u8_golden_and_cube(torch_dev, cube):
     toned, gray, out = wg.decolor_tone_host(h, return_gray=True, return_rgb=True)
     want_o, want_t, want_g = oracle.tone_rgb_u8(h)
     assert np.array_equal(out, want_o) and np.array_equal(toned, want_t) and np.array_equal(gray, want_g)
+    assert np.array_equal(wg.decolor_tone_host(h, exact=True), want_t)
 
 
 def test_tone_rgb_u8_voronoi_frames(torch_dev):
