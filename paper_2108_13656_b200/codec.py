@@ -186,13 +186,15 @@ def write_pnm_batch(paths, batch: np.ndarray, threads: int | None = None) -> Non
 
 
 def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=None, grid=None,
-                  batch: int = 32, threads: int | None = None, device: int | None = None) -> int:
+                  batch: int = 32, threads: int | None = None, device: int | None = None,
+                  exact: bool = False) -> int:
     """uint8 files in, uint8 gray files out, bytes never leave uint8.
 
     ``mode``: "gray" (decolor), "global" (decolor + sigmoid) or "local"
     (decolor + local tone map); outputs are bit-identical to
-    quantize_u8 of the reference's fp64 chain for "local" and within the
-    north-star bound (+-1 on <= 0.01% of pixels) for "gray" / "global".
+    quantize_u8 of the reference's fp64 chain for "local" (and for "gray" /
+    "global" with ``exact=True``), else within the north-star bound (+-1 on
+    <= 0.01% of pixels).
     Same-size binary PPM inputs go through the native batch reader in groups
     of ``batch``; outputs are written as PGM. Reading batch i + 1, the device
     pass of batch i and writing batch i - 1 overlap (pinned double buffers).
@@ -242,9 +244,10 @@ def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=N
                 writes[i % 2].result()  # output slot free again
             dst = buf(i % 2, "out", rgb.shape[:-1])
             if mode == "gray":
-                out = _batch.decolor_host(rgb, params, out=dst, device=device)
+                out = _batch.decolor_host(rgb, params, out=dst, device=device, exact=exact)
             elif mode == "global":
-                out = _batch.decolor_tone_host(rgb, curve or SigmoidCurve(), params, device=device, out=dst)
+                out = _batch.decolor_tone_host(rgb, curve or SigmoidCurve(), params, device=device, out=dst,
+                                               exact=exact)
             else:
                 out = _batch.decolor_tone_local_host(rgb, grid, params, device=device, out=dst)
             writes[i % 2] = pool.submit(write_pnm_batch, groups[i][1], out, threads)

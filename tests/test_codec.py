@@ -140,7 +140,7 @@ def test_save_image_round_trips(tmp_path, rng):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["gray", "local"])
+@pytest.mark.parametrize("mode", ["gray", "local", "gray_exact", "global_exact"])
 def test_decolor_files_vs_oracle(tmp_path, mode):
     from oracle import oracle
 
@@ -150,9 +150,14 @@ def test_decolor_files_vs_oracle(tmp_path, mode):
     src = [tmp_path / f"in{k}.ppm" for k in range(5)]
     dst = [tmp_path / f"out{k}.pgm" for k in range(5)]
     wg.write_pnm_batch(src, batch)
-    assert wg.decolor_files(src, dst, mode=mode, batch=2) == 5
+    exact = mode.endswith("_exact")
+    assert wg.decolor_files(src, dst, mode=mode.replace("_exact", ""), batch=2, exact=exact) == 5
     got = np.stack([wg.load_u8(p) for p in dst])
-    if mode == "gray":
+    if mode == "gray_exact":
+        np.testing.assert_array_equal(got, oracle.decolor_u8(batch))
+    elif mode == "global_exact":
+        np.testing.assert_array_equal(got, oracle.tone_rgb_u8(batch)[1])
+    elif mode == "gray":
         want = oracle.decolor_u8(batch)
         d = np.abs(got.astype(int) - want.astype(int))
         assert d.max() <= 1 and (d != 0).mean() <= 1e-4
