@@ -490,8 +490,8 @@ def run_methods(wg, torch, rgb, out, n_img, wl, stream, iters: int = 5):
     other extractors (colorspaces.py:87-112), all uint8 -> uint8 and
     bit-identical to quantize_u8 of the reference. "global_tone" is the fused
     decolor + global sigmoid (tonemap_image(mode="global"), north-star bar),
-    "global_tone_rgb" the same with the reinstated colour image as uint8
-    (fp64 chain, bit-identical), and "local_tone" the fused decolor + local tone map (mode="local",
+    "global_tone_exact" its bit-identical route, "global_tone_rgb" the same
+    with the reinstated colour image as uint8 (bit-identical), and "local_tone" the fused decolor + local tone map (mode="local",
     SURVEY 8 f1, bit-identical).
     """
     grid = wg.LocalHistogramGrid.for_image(wl.width, wl.height)
@@ -507,6 +507,7 @@ def run_methods(wg, torch, rgb, out, n_img, wl, stream, iters: int = 5):
     fns = {
         "ours": lambda: wg.decolor(rgb, out=out),
         "global_tone": lambda: wg.decolor_tone(rgb),
+        "global_tone_exact": lambda: wg.decolor_tone(rgb, exact=True),
         "global_tone_rgb": lambda: wg.decolor_tone(rgb, return_rgb=True),
         "y_bt601": lambda: wg.luma(rgb, "y"),
         "v_hsv": lambda: wg.luma(rgb, "v"),
