@@ -515,6 +515,14 @@ __device__ __forceinline__ void wq_flush(const uint32_t* q, int qn, F&& fix) {
     for (int j = static_cast<int>(threadIdx.x & 31); j < qn; j += 32) fix(q[j]);
 }
 
+// predicated shared-memory add without the compiler's warp-aggregation scaffolding
+__device__ __forceinline__ void red_shared_add(uint32_t* p, uint32_t v, bool pred) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.add.u32 [%0], %1;\n}" ::"r"(
+                     smem_addr(p)),
+                 "r"(v), "r"(static_cast<uint32_t>(pred))
+                 : "memory");
+}
+
 // kPacked (nb <= 512): the plane word carries the pixel's exact bin next to the
 // estimate, bin << 23 | the 23 fraction bits of 256 + g255 (ulp 2^-15), so the
 // apply pass neither recomputes the bin nor re-tests its edges; else the plane
@@ -587,27 +595,38 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
             float g255[kGrp];
             grp.gray255(L.k8, g255);
             uint32_t words[kGrp];
-            // runs of equal cells are merged before the shared-memory atomic; the
-            // first flush goes to the dummy cell
+            // runs of equal cells are merged before the shared-memory add (a
+            // predicated red.shared: no branch per pixel); the first flush goes to
+            // the dummy cell. Groups inside one tile (all but one in tw / 16 when
+            // tw >= 16) skip the per-pixel tile stepping.
             int run_cell = cells;
             uint32_t run = 0;
-#pragma unroll
-            for (int p = 0; p < kGrp; ++p) {
-                const bool step = x0 + p >= next;
-                tx += step;
-                next += step ? g.tw : 0;
+            const auto px = [&](int p, int cbase) {
                 bool sure;
                 const int b = L.bin_fast(g255[p], sure);
-                const int cell = tx * g.nb + b;
+                const int cell = cbase + b;
                 if constexpr (kPacked) words[p] = plane_word(g255[p], b);  // unsure bins are patched below
                 else words[p] = __float_as_uint(g255[p]);
                 slow |= static_cast<uint32_t>(!sure) << p;
                 const bool same = cell == run_cell;
-                if (sure && !same) atomicAdd(&sh[run_cell], run);
+                red_shared_add(&sh[run_cell], run, sure && !same);
                 run = sure ? (same ? run + 1 : 1u) : run;
                 run_cell = sure ? cell : run_cell;
+            };
+            if (x0 + kGrp <= next) {
+                const int cbase = tx * g.nb;
+#pragma unroll
+                for (int p = 0; p < kGrp; ++p) px(p, cbase);
+            } else {
+#pragma unroll
+                for (int p = 0; p < kGrp; ++p) {
+                    const bool step = x0 + p >= next;
+                    tx += step;
+                    next += step ? g.tw : 0;
+                    px(p, tx * g.nb);
+                }
             }
-            atomicAdd(&sh[run_cell], run);
+            red_shared_add(&sh[run_cell], run, true);
             // keep the estimate for the apply pass (4 B/px instead of recomputing the gray)
             uint32_t* wplane = reinterpret_cast<uint32_t*>(gplane);
             if (vec) {
