@@ -43,9 +43,11 @@ from .codec import (
     load_image,
     load_u8,
     quantize_u8,
+    read_batch,
     read_pnm_batch,
     save_image,
     save_u8,
+    write_batch,
     write_pnm_batch,
 )
 from .perf import BenchResult, format_table, run_benchmark
@@ -109,7 +111,9 @@ __all__ = [
     "save_image",
     "load_u8",
     "save_u8",
+    "read_batch",
     "read_pnm_batch",
+    "write_batch",
     "write_pnm_batch",
     "decolor_files",
     "BenchResult",

@@ -185,6 +185,71 @@ def write_pnm_batch(paths, batch: np.ndarray, threads: int | None = None) -> Non
                                               batch.shape[1], c, _threads(threads)), "wg_pnm_write_batch")
 
 
+def _image_shape(path: str) -> tuple:
+    """(H, W, 3) or (H, W) of a PNM or PNG file, from its header."""
+    if _is_pnm(path):
+        h, w, c = pnm_info(path)
+        return (h, w, 3) if c == 3 else (h, w)
+    from PIL import Image, UnidentifiedImageError
+
+    try:
+        with Image.open(path) as im:
+            if im.format != "PNG":
+                raise CodecError(f"{path}: unsupported format {im.format!r} (need PNG or binary PPM/PGM)")
+            return (im.size[1], im.size[0]) if im.mode in ("L", "LA") else (im.size[1], im.size[0], 3)
+    except UnidentifiedImageError:
+        raise CodecError(f"{path}: not a decodable image") from None
+
+
+def read_batch(paths, threads: int | None = None, out=None, pinned: bool = True) -> np.ndarray:
+    """Read same-size PNG / PPM / PGM files into one uint8 batch (pinned by default).
+
+    All-PNM batches go through the native reader (:func:`read_pnm_batch`);
+    otherwise each file is decoded (Pillow for PNG, as in the reference) on a
+    thread pool straight into the batch -- the decoders release the GIL.
+    """
+    paths = [os.fspath(p) for p in paths]
+    if not paths:
+        raise ValueError("read_batch needs at least one path")
+    if all(_is_pnm(p) for p in paths):
+        return read_pnm_batch(paths, threads=threads, pinned=pinned, out=out)
+    shape = (len(paths), *_image_shape(paths[0]))
+    if out is None:
+        out = _empty_batch(shape, pinned)
+    elif out.shape != shape or out.dtype != np.uint8 or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"out must be C-contiguous uint8 of shape {shape}")
+
+    def one(k):
+        img = load_u8(paths[k])
+        if img.shape != shape[1:]:
+            raise CodecError(f"{paths[k]}: shape {img.shape} differs from the batch's {shape[1:]}")
+        out[k] = img
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(_threads(threads), len(paths))) as pool:
+        list(pool.map(one, range(len(paths))))
+    return out
+
+
+def write_batch(paths, batch: np.ndarray, threads: int | None = None) -> None:
+    """Write a uint8 batch, one file per image, format by extension (.png / .ppm / .pgm).
+
+    All-PNM targets go through the native writer (:func:`write_pnm_batch`);
+    otherwise each file is encoded on a thread pool.
+    """
+    paths = [os.fspath(p) for p in paths]
+    if len(paths) != len(batch):
+        raise ValueError(f"{len(paths)} paths for {len(batch)} images")
+    if all(os.path.splitext(p)[1].lower() in (".ppm", ".pgm") for p in paths):
+        write_pnm_batch(paths, batch, threads=threads)
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(_threads(threads), len(paths))) as pool:
+        list(pool.map(lambda k: save_u8(paths[k], batch[k]), range(len(paths))))
+
+
 def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=None, grid=None,
                   batch: int = 32, threads: int | None = None, device: int | None = None,
                   exact: bool = False) -> int:
@@ -195,9 +260,11 @@ def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=N
     quantize_u8 of the reference's fp64 chain for "local" (and for "gray" /
     "global" with ``exact=True``), else within the north-star bound (+-1 on
     <= 0.01% of pixels).
-    Same-size binary PPM inputs go through the native batch reader in groups
-    of ``batch``; outputs are written as PGM. Reading batch i + 1, the device
-    pass of batch i and writing batch i - 1 overlap (pinned double buffers).
+    Same-size RGB inputs (binary PPM through the native reader, PNG through
+    Pillow on a thread pool) go in groups of ``batch``; outputs are written by
+    extension (.pgm natively, .png through Pillow). Reading batch i + 1, the
+    device pass of batch i and writing batch i - 1 overlap (pinned double
+    buffers).
     Returns the number of files.
     """
     from . import batch as _batch
@@ -224,10 +291,9 @@ def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=N
         return b
 
     def read(i):
-        paths = groups[i][0]
-        h, w, c = pnm_info(paths[0])
-        shape = (len(paths), h, w, 3) if c == 3 else (len(paths), h, w)
-        return read_pnm_batch(paths, threads=threads, out=buf(i % 2, "in", shape))
+        paths = [os.fspath(p) for p in groups[i][0]]
+        shape = (len(paths), *_image_shape(paths[0]))
+        return read_batch(paths, threads=threads, out=buf(i % 2, "in", shape))
 
     from concurrent.futures import ThreadPoolExecutor
 
@@ -250,7 +316,7 @@ def decolor_files(src_paths, dst_paths, mode: str = "gray", params=None, curve=N
                                                exact=exact)
             else:
                 out = _batch.decolor_tone_local_host(rgb, grid, params, device=device, out=dst)
-            writes[i % 2] = pool.submit(write_pnm_batch, groups[i][1], out, threads)
+            writes[i % 2] = pool.submit(write_batch, groups[i][1], out, threads)
         for f in writes:
             if f is not None:
                 f.result()

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--dir", default="/tmp/wg_files")
     ap.add_argument("--repeats", type=int, default=3)
+    ap.add_argument("--png", action="store_true", help="also time PNG in / PNG out")
     args = ap.parse_args()
 
     import paper_2108_13656_b200 as wg
@@ -61,6 +62,13 @@ def main():
         wg.decolor_files(src, dst, mode=mode)  # warm-up (pinned buffers, staging)
         best = min(_timed(lambda: wg.decolor_files(src, dst, mode=mode)) for _ in range(args.repeats))
         report(f"ours_{mode}", best, {"api": "wg.decolor_files", "cold_cache": False})
+    if args.png:  # PNG in / PNG out: Pillow decode / encode on a thread pool (zlib-bound)
+        psrc = [os.path.join(args.dir, f"in{k:04d}.png") for k in range(n)]
+        pdst = [os.path.join(args.dir, f"out{k:04d}.png") for k in range(n)]
+        wg.write_batch(psrc, imgs)
+        wg.decolor_files(psrc, pdst)
+        best = min(_timed(lambda: wg.decolor_files(psrc, pdst)) for _ in range(args.repeats))
+        report("ours_gray_png", best, {"api": "wg.decolor_files", "format": "png", "cold_cache": False})
     # page cache is warm for both arms: this is pipeline throughput, not disk
 
     threads = oracle.default_threads()

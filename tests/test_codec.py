@@ -140,20 +140,22 @@ def test_save_image_round_trips(tmp_path, rng):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["gray", "local", "gray_exact", "global_exact"])
+@pytest.mark.parametrize("mode", ["gray", "local", "gray_exact", "global_exact", "gray_png"])
 def test_decolor_files_vs_oracle(tmp_path, mode):
     from oracle import oracle
 
     rng = np.random.default_rng(5)
     batch = rng.integers(0, 256, (5, 96, 128, 3), dtype=np.uint8)
     batch[0, :40] = batch[0, :40] // 32 * 32
-    src = [tmp_path / f"in{k}.ppm" for k in range(5)]
-    dst = [tmp_path / f"out{k}.pgm" for k in range(5)]
-    wg.write_pnm_batch(src, batch)
-    exact = mode.endswith("_exact")
-    assert wg.decolor_files(src, dst, mode=mode.replace("_exact", ""), batch=2, exact=exact) == 5
+    ext_in, ext_out = (".png", ".png") if mode == "gray_png" else (".ppm", ".pgm")
+    src = [tmp_path / f"in{k}{ext_in}" for k in range(5)]
+    dst = [tmp_path / f"out{k}{ext_out}" for k in range(5)]
+    wg.write_batch(src, batch)
+    exact = mode.endswith("_exact") or mode == "gray_png"
+    base = mode.replace("_exact", "").replace("_png", "")
+    assert wg.decolor_files(src, dst, mode=base, batch=2, exact=exact) == 5
     got = np.stack([wg.load_u8(p) for p in dst])
-    if mode == "gray_exact":
+    if mode in ("gray_exact", "gray_png"):
         np.testing.assert_array_equal(got, oracle.decolor_u8(batch))
     elif mode == "global_exact":
         np.testing.assert_array_equal(got, oracle.tone_rgb_u8(batch)[1])
@@ -164,3 +166,20 @@ def test_decolor_files_vs_oracle(tmp_path, mode):
     else:
         g = wg.LocalHistogramGrid.for_image(128, 96)
         np.testing.assert_array_equal(got, oracle.tone_local_u8(batch, g.tile_w, g.tile_h, g.bins, g.strength))
+
+
+def test_read_write_batch_png_and_pnm(tmp_path):
+    """read_batch / write_batch: PNG through Pillow on a thread pool, PNM natively;
+    same bytes either way; mixed sizes rejected."""
+    rng = np.random.default_rng(9)
+    batch = rng.integers(0, 256, (4, 24, 40, 3), dtype=np.uint8)
+    png = [tmp_path / f"a{k}.png" for k in range(4)]
+    ppm = [tmp_path / f"a{k}.ppm" for k in range(4)]
+    wg.write_batch(png, batch)
+    wg.write_batch(ppm, batch)
+    np.testing.assert_array_equal(wg.read_batch(png, pinned=False), batch)
+    np.testing.assert_array_equal(wg.read_batch(ppm, pinned=False), batch)
+    np.testing.assert_array_equal(wg.read_batch([png[0], ppm[1]], pinned=False), batch[:2])  # mixed formats
+    wg.save_u8(tmp_path / "small.png", batch[0, :10])
+    with pytest.raises(wg.CodecError):
+        wg.read_batch([png[0], tmp_path / "small.png"], pinned=False)
