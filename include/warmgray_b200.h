@@ -106,9 +106,11 @@ WG_API int wg_tonemap_global_f64(const double* rgb, double* l_out, double* rgb_o
                           double beta_r, double beta_k, double midpoint, double slope,
                           void* stream);
 
-/* Fused decolor + global tone map on uint8 RGB:
+/* Fused decolor + global tone map on uint8 RGB (tonemap.py:72-83 after
+ * core.py:147-169, codec.py:22-29):
  * toned = quantize_u8(apply_sigmoid(decolor(rgb/255))); gray_or_null receives
- * quantize_u8(decolor(rgb/255)) when non-NULL. */
+ * quantize_u8(decolor(rgb/255)) when non-NULL. North-star bar (+-1 on rounding
+ * ties); wg_decolor_tone_rgb_u8 with rgb_out = NULL is the bit-identical route. */
 WG_API int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* gray_or_null, int64_t npix,
                        float beta_r, float beta_k, float midpoint, float slope, void* stream);
 
@@ -175,7 +177,10 @@ WG_API int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint8_t*
                                     int64_t tile_h, int64_t bins, double strength, void* scratch,
                                     size_t scratch_bytes, void* stream);
 
-/* ---- host-buffer entry points (synchronous; pipelined H2D/compute/D2H) ---- */
+/* ---- host-buffer entry points (synchronous; pipelined H2D/compute/D2H) ----
+ * Each wg_host_X takes host arrays and a device ordinal and replaces the same
+ * reference interface as the device entry wg_X above (cited there); results
+ * are identical to wg_X's. */
 
 /* bt601_rows / hsv_value_rows / lab_lightness_rows and lab_rows on host fp64
  * buffers, with the plugin's (rgb, out, ..., row0, row1) contract. */
