@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -40,11 +41,16 @@ struct ToneTable {
     float thr[256];          // f-domain thresholds 256 + x_j (j = 1..255 at [j-1]), +inf padded
     int multi;               // any bin with several thresholds (host-side flag)
     int pad[3];
+    // exact route only (not staged by OpToneU8): 1 where a neighbouring bin's
+    // threshold lies within kEdgeUnits (2^-15 units) of the shared edge
+    uint8_t edge[kToneBins];
 };
+constexpr uint32_t kEdgeUnits = 64;
+constexpr size_t kToneStaged = offsetof(ToneTable, edge);  // bytes OpToneU8 stages
 
 __device__ __forceinline__ ToneTable* tone_smem() {
-    __shared__ __align__(16) ToneTable t;
-    return &t;
+    __shared__ __align__(16) uint8_t t[kToneStaged];  // bins + thr (+ multi); edge is not staged here
+    return reinterpret_cast<ToneTable*>(t);
 }
 
 // kMulti: the curve's table has bins holding several thresholds (steep curves)
@@ -62,7 +68,7 @@ struct OpToneU8 {
         ToneTable* s = tone_smem();
         const float4* src = reinterpret_cast<const float4*>(tab);
         float4* dst = reinterpret_cast<float4*>(s);
-        for (int i = threadIdx.x; i < static_cast<int>(sizeof(ToneTable) / 16); i += blockDim.x) dst[i] = src[i];
+        for (int i = threadIdx.x; i < static_cast<int>(kToneStaged / 16); i += blockDim.x) dst[i] = src[i];
     }
     // toned byte from the f-domain bits of one pixel
     __device__ __forceinline__ uint32_t tone(uint32_t bits) const {
@@ -176,6 +182,15 @@ void build_tone_table(double m, double k, ToneTable* t) {
         float base;
         std::memcpy(&base, &cnt, 4);
         t->bins[b] = make_float2(base, tin);
+    }
+    std::memset(t->edge, 0, sizeof(t->edge));
+    for (int j = 0; j < 255; ++j) {
+        uint32_t bits;
+        std::memcpy(&bits, &xf[j], 4);
+        const int b = static_cast<int>((bits >> 11) & (kToneBins - 1));
+        const uint32_t low = bits & 0x7FFu;
+        if (low < kEdgeUnits && b > 0) t->edge[b - 1] = 1;
+        if (0x800u - low <= kEdgeUnits && b + 1 < kToneBins) t->edge[b + 1] = 1;
     }
 }
 
@@ -522,6 +537,151 @@ __global__ void __launch_bounds__(256, 3)
     }
 }
 
+// ---------------------------------------------------------------- exact toned-only route
+// decolor_tone(u8, exact=True) without the colour image: the threshold-table
+// kernel's arithmetic (decolor255_bits_x2, one table lookup per pixel) plus a
+// proof that the fast toned byte is the reference's: err = max |f_fast -
+// f_exact| over all 2^24 colours for (beta_r, beta_k), settled exhaustively
+// with the exact-u8 table (wg_u8exact.cu), and M = err + 2 units of 2^-15 (the
+// float rounding of the thresholds, one of slack). A pixel whose f lies
+// within M of the threshold of its bin -- or of an edge of a bin flagged with
+// a neighbour's threshold at that edge, or (gray requested) of a rounding
+// boundary -- goes through the per-warp queue to the reference's fp64 chain.
+constexpr int kExactQueue = 32 + 32 * kRgbPx;  // < 32 carried + one warp-tile
+template <bool kGray, bool kMulti>
+__global__ void __launch_bounds__(256, 4)
+    tone_u8_exact_kernel(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ toned, uint8_t* __restrict__ gray,
+                         int64_t ntiles, int64_t npix, const ToneTable* __restrict__ tab, U8Consts k, uint32_t M,
+                         double br, double bk, SigD sig) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    ToneTable* T = reinterpret_cast<ToneTable*>(dsm);  // bins + thr staged; edge folded into bins[].x
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t* queue = reinterpret_cast<uint32_t*>(dsm + kToneStaged) + wid * kExactQueue;
+    {
+        const float4* src = reinterpret_cast<const float4*>(tab);
+        float4* dst = reinterpret_cast<float4*>(T);
+        for (int i = tid; i < static_cast<int>(kToneStaged / 16); i += 256) dst[i] = src[i];
+        __syncthreads();
+        // the edge flag rides in bit 16 of each bin's count word: one LDS.64 per pixel
+        for (int b = tid; b < kToneBins; b += 256)
+            if (tab->edge[b])
+                T->bins[b].x = __uint_as_float(__float_as_uint(T->bins[b].x) | 0x10000u);
+    }
+    __syncthreads();
+    int qn = 0;
+    const int64_t stride = gridDim.x;
+    const auto pix = [&](uint32_t e) {  // (tile iteration << 9) | pixel offset in the warp's slice
+        return (static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(e >> 9) * stride) * kRgbTile + wid * 512 +
+               (e & 511u);
+    };
+    const auto fix = [&](int64_t p) {
+        tone_rgb_px(rgb, nullptr, toned, gray, p, br, bk, sig.m, sig.k, sig.lo, sig.hi);
+    };
+    // toned byte of one pixel's f-domain bits; near |= f within M of a threshold
+    const auto tone = [&](uint32_t bits, bool& near) -> uint32_t {
+        const uint32_t b = (bits >> 11) & (kToneBins - 1);
+        const float2 e = T->bins[b];
+        const float f = __uint_as_float(bits);
+        const uint32_t low = bits & 0x7FFu, cw = __float_as_uint(e.x);
+        near = near || ((cw >> 16) != 0u && (low < M || low >= 0x800u - M));
+        if constexpr (kMulti) {
+            if (e.y != e.y) {  // several thresholds in this bin: binary search, both neighbours checked
+                uint32_t c = 0;
+#pragma unroll
+                for (uint32_t st = 128; st; st >>= 1) c += (f >= T->thr[c + st - 1]) ? st : 0;
+                const uint32_t lo_b = c ? __float_as_uint(T->thr[c - 1]) : 0u;
+                const uint32_t hi_b = __float_as_uint(T->thr[c]);  // +inf pad: far away
+                near = near || bits - lo_b <= M || hi_b - bits <= M;
+                return c;
+            }
+        }
+        near = near || bits - __float_as_uint(e.y) + M <= 2u * M;  // |bits - thr| <= M (inf: no)
+        return (cw & 0xFFFFu) + (f >= e.y ? 1u : 0u);
+    };
+    int64_t t = blockIdx.x;
+    uint4 v[3];
+    if (t < ntiles) {
+        const uint4* p = reinterpret_cast<const uint4*>(rgb + t * (kRgbTile * 3)) + tid * 3;
+        v[0] = __ldcs(p);
+        v[1] = __ldcs(p + 1);
+        v[2] = __ldcs(p + 2);
+    }
+    for (int64_t it = 0; t < ntiles; t += stride, ++it) {
+        uint4 nx[3] = {v[0], v[1], v[2]};
+        if (t + stride < ntiles) {
+            const uint4* q = reinterpret_cast<const uint4*>(rgb + (t + stride) * (kRgbTile * 3)) + tid * 3;
+            nx[0] = __ldcs(q);
+            nx[1] = __ldcs(q + 1);
+            nx[2] = __ldcs(q + 2);
+        }
+        const uint32_t w[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y,
+                                v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
+        uint32_t ot[4], og[4];
+        uint32_t mask = 0;  // bit i: pixel i needs the fp64 chain
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+            uint32_t tt[4], gg[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = 2 * qd + h;
+                float2 ch[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int b0 = 3 * (2 * j) + c, b1 = 3 * (2 * j + 1) + c;
+                    ch[c] = add2(make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3)),
+                                 bc2(-kMagic));
+                }
+                const float2 f = decolor255_bits_x2(ch[0], ch[1], ch[2], k);
+                const uint32_t x = __float_as_uint(f.x), y = __float_as_uint(f.y);
+                bool n0 = false, n1 = false;
+                tt[2 * h] = tone(x, n0);
+                tt[2 * h + 1] = tone(y, n1);
+                if constexpr (kGray) {
+                    gg[2 * h] = x >> 15;
+                    gg[2 * h + 1] = y >> 15;
+                    n0 = n0 || bits_near_tie(x, M);
+                    n1 = n1 || bits_near_tie(y, M);
+                }
+                mask |= (n0 ? 1u : 0u) << (2 * j);
+                mask |= (n1 ? 1u : 0u) << (2 * j + 1);
+            }
+            ot[qd] = __byte_perm(__byte_perm(tt[0], tt[1], 0x0040u), __byte_perm(tt[2], tt[3], 0x0040u), 0x5410u);
+            if constexpr (kGray)
+                og[qd] = __byte_perm(__byte_perm(gg[0], gg[1], 0x0040u), __byte_perm(gg[2], gg[3], 0x0040u), 0x5410u);
+        }
+        const int64_t p0 = t * kRgbTile + static_cast<int64_t>(tid) * kRgbPx;
+        __stcs(reinterpret_cast<uint4*>(toned + p0), make_uint4(ot[0], ot[1], ot[2], ot[3]));
+        if constexpr (kGray) __stcs(reinterpret_cast<uint4*>(gray + p0), make_uint4(og[0], og[1], og[2], og[3]));
+        if (__any_sync(0xFFFFFFFFu, mask != 0u)) {
+            const int cnt = __popc(mask);
+            int pre = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+                if (lane >= d) pre += x;
+            }
+            int slot = qn + pre - cnt;
+            const uint32_t e0 = (static_cast<uint32_t>(it) << 9) | static_cast<uint32_t>(lane * kRgbPx);
+            for (uint32_t mm = mask; mm; mm &= mm - 1) queue[slot++] = e0 + (__ffs(mm) - 1);
+            qn += __shfl_sync(0xFFFFFFFFu, pre, 31);
+            __syncwarp();  // appends and this tile's provisional stores before the drain
+            if (qn >= kQueueDrain) {
+                for (int jj = lane; jj < qn; jj += 32) fix(pix(queue[jj]));
+                qn = 0;
+                __syncwarp();
+            }
+        }
+        v[0] = nx[0];
+        v[1] = nx[1];
+        v[2] = nx[2];
+    }
+    __syncwarp();
+    for (int jj = lane; jj < qn; jj += 32) fix(pix(queue[jj]));
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t p = ntiles * kRgbTile + tid; p < npix; p += 256) fix(p);
+    }
+}
+
 // fp32 constants and error budget of the fast kernel; false if the curve is
 // outside its range (then the fp64 kernel runs every pixel)
 bool make_tone_rgb_consts(double br, double bk, double m, double k, ToneRgbF* c, bool* two_ex2) {
@@ -610,6 +770,30 @@ extern "C" int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint
     const bool aligned = al(rgb) && (!rgb_out || al(rgb_out)) && (!toned_or_null || al(toned_or_null)) &&
                          (!gray_or_null || al(gray_or_null));
     const int64_t ntiles = npix / kRgbTile;
+    if (!rgb_out && toned_or_null && aligned && ntiles > 0 && !std::getenv("WG_TONE_EXACT_VIA_RGB")) {
+        // toned (+ gray) only: the threshold-table kernel with a proven margin
+        // (locks: tone cache, then exact-u8 cache, both held until the launch is enqueued)
+        const ToneTable* tab = nullptr;
+        bool multi = false;
+        std::unique_lock<std::mutex> hold_t, hold_e;
+        int rc = tone_table(midpoint, slope, &tab, &multi, &hold_t);
+        if (rc != WG_OK) return rc;
+        U8Exact ex;
+        rc = u8exact_get(beta_r, beta_k, &ex, &hold_e);
+        if (rc != WG_OK) return rc;
+        const uint32_t M = ex.err + 2;
+        if (M <= kEdgeUnits) {
+            const U8Consts k = make_u8_consts(beta_r, beta_k);
+            const size_t smem = kToneStaged + 8 * kExactQueue * sizeof(uint32_t);
+            const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ntiles, 4LL * sm_count(device)));
+            auto kern = gray_or_null ? (multi ? tone_u8_exact_kernel<true, true> : tone_u8_exact_kernel<true, false>)
+                                     : (multi ? tone_u8_exact_kernel<false, true> : tone_u8_exact_kernel<false, false>);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            kern<<<grid, 256, smem, st>>>(rgb, toned_or_null, gray_or_null, ntiles, npix, tab, k, M, beta_r, beta_k,
+                                         sig);
+            return check_launch("tone_u8_exact");
+        }
+    }
     if (aligned && ntiles > 0 && make_tone_rgb_consts(beta_r, beta_k, midpoint, slope, &c, &two_ex2)) {
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ntiles, 3LL * sm_count(device)));
         auto launch = two_ex2 ? (rgb_out ? launch_tone_rgb_fast<true, true> : launch_tone_rgb_fast<true, false>)

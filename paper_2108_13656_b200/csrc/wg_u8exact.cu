@@ -42,14 +42,23 @@ __device__ __forceinline__ uint32_t tie_distance(uint32_t bits) {
     return f < 0x4000u ? f : 0x8000u - f;
 }
 
-// largest boundary distance among colours whose fast byte is wrong
+// need[0]: largest boundary distance among colours whose fast byte is wrong;
+// need[1]: the largest |f_fast - f_exact| over all colours in 2^-15 units,
+// rounded up (f = 255 gray + 0.5 in the bits' fixed-point form) -- a true
+// error bound of the fast gray for this (beta_r, beta_k), which the exact
+// tone map compares against its thresholds
 __global__ void u8exact_need_kernel(U8Consts k, double br, double bk, uint32_t* need) {
-    uint32_t worst = 0;
+    uint32_t worst = 0, err = 0;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < kColours; c += gridDim.x * blockDim.x) {
         const uint32_t bits = fast_bits(c, k);
         if (bits_byte(bits) != exact_byte(c, br, bk)) worst = max(worst, tie_distance(bits) + 1);
+        const double v = decolor_f64(deq_byte(c >> 16), deq_byte((c >> 8) & 255u), deq_byte(c & 255u), br, bk);
+        const double exact_units = (v * 255.0 + 0.5) * 32768.0;  // bits & 0x7FFFFF = (f - 256) * 2^15
+        const double d = fabs(static_cast<double>(bits & 0x7FFFFFu) - exact_units);
+        err = max(err, static_cast<uint32_t>(ceil(d)));
     }
     if (worst) atomicMax(need, worst);
+    if (err) atomicMax(need + 1, err);
 }
 
 // every colour within the margin goes into the table with its exact byte
@@ -78,31 +87,31 @@ int g_next[kMaxDevices];
 std::mutex g_mu;
 
 int build(int device, double br, double bk, U8Exact* out) {
-    const U8Consts k = make_u8_consts(static_cast<float>(br), static_cast<float>(bk));
+    const U8Consts k = make_u8_consts(br, bk);  // exactly the constants the kernels use
     cudaStream_t st;
     cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e != cudaSuccess) return set_error(static_cast<int>(e), "u8 exact table: stream: %s", cudaGetErrorString(e));
-    uint32_t* scratch = nullptr;  // need, count
+    uint32_t* scratch = nullptr;  // need, error bound, count
     uint32_t* tab = nullptr;
     int rc = WG_OK;
     const int blocks = 8 * sm_count(device);
-    uint32_t host[2] = {0, 0};
+    uint32_t host[3] = {0, 0, 0};
     uint32_t slots = 1u << 15;
     do {
-        if ((e = cudaMalloc(&scratch, 8)) != cudaSuccess) break;
-        if ((e = cudaMemsetAsync(scratch, 0, 8, st)) != cudaSuccess) break;
+        if ((e = cudaMalloc(&scratch, 12)) != cudaSuccess) break;
+        if ((e = cudaMemsetAsync(scratch, 0, 12, st)) != cudaSuccess) break;
         u8exact_need_kernel<<<blocks, 256, 0, st>>>(k, br, bk, scratch);
-        if ((e = cudaMemcpyAsync(host, scratch, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(host, scratch, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
         const uint32_t margin = host[0] > kMinMargin ? host[0] : kMinMargin;
         for (;;) {  // grow until the table is at most half full
             if ((e = cudaMalloc(&tab, slots * 4ull)) != cudaSuccess) break;
             if ((e = cudaMemsetAsync(tab, 0xFF, slots * 4ull, st)) != cudaSuccess) break;
-            if ((e = cudaMemsetAsync(scratch + 1, 0, 4, st)) != cudaSuccess) break;
-            u8exact_fill_kernel<<<blocks, 256, 0, st>>>(k, br, bk, margin, tab, slots - 1, scratch + 1);
-            if ((e = cudaMemcpyAsync(host + 1, scratch + 1, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+            if ((e = cudaMemsetAsync(scratch + 2, 0, 4, st)) != cudaSuccess) break;
+            u8exact_fill_kernel<<<blocks, 256, 0, st>>>(k, br, bk, margin, tab, slots - 1, scratch + 2);
+            if ((e = cudaMemcpyAsync(host + 2, scratch + 2, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
             if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
-            if (host[1] * 2 <= slots) break;
+            if (host[2] * 2 <= slots) break;
             cudaFree(tab);
             tab = nullptr;
             slots <<= 2;
@@ -111,6 +120,7 @@ int build(int device, double br, double bk, U8Exact* out) {
         out->tab = tab;
         out->mask = slots - 1;
         out->margin = margin;
+        out->err = host[1];
     } while (false);
     if (e != cudaSuccess) {
         rc = set_error(static_cast<int>(e), "u8 exact table: %s", cudaGetErrorString(e));
@@ -156,7 +166,7 @@ int u8exact_get(double beta_r, double beta_k, U8Exact* out, std::unique_lock<std
 using namespace wg;
 
 // diagnostics: the margin and entry count of the table for (beta_r, beta_k)
-extern "C" int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, uint32_t* slots) {
+extern "C" int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, uint32_t* slots, uint32_t* err) {
     WG_CHECK_ARGS(check_params(beta_r, beta_k));
     U8Exact t;
     std::unique_lock<std::mutex> hold;
@@ -164,5 +174,6 @@ extern "C" int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, 
     if (rc != WG_OK) return rc;
     if (margin) *margin = t.margin;
     if (slots) *slots = t.mask + 1;
+    if (err) *err = t.err;
     return WG_OK;
 }

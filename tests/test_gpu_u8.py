@@ -94,12 +94,13 @@ def test_exact_table_info():
 
     from paper_2108_13656_b200 import _lib
 
-    margin, slots = ctypes.c_uint32(), ctypes.c_uint32()
-    _lib.call("wg_u8_exact_info", 0.55, 0.8, ctypes.byref(margin), ctypes.byref(slots))
-    print(f"near-tie table: margin {margin.value} units of 2^-15, {slots.value} slots")
+    margin, slots, err = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+    _lib.call("wg_u8_exact_info", 0.55, 0.8, ctypes.byref(margin), ctypes.byref(slots), ctypes.byref(err))
+    print(f"near-tie table: margin {margin.value} units of 2^-15, {slots.value} slots, max error {err.value} units")
     assert 3 <= margin.value <= 16 and slots.value >= 1024
+    assert 1 <= err.value <= 16  # the fast gray's exhaustive error bound (the exact tone map's margin - 2)
     with pytest.raises(ValueError):
-        _lib.call("wg_u8_exact_info", 0.5, 0.8, None, None)
+        _lib.call("wg_u8_exact_info", 0.5, 0.8, None, None, None)
 
 
 def test_c1_config(torch_dev):
@@ -328,6 +329,23 @@ def test_tone_rgb_u8_voronoi_frames(torch_dev):
     _, _, fo = wg.decolor_tone(flat, return_rgb=True)
     want, _, _ = oracle.tone_rgb_u8(pick[None])
     assert (fo.view(-1, 3).cpu().numpy() == want[0]).all()
+
+
+def test_exact_tone_routes_agree(torch_dev, cube, monkeypatch):
+    """decolor_tone(u8, exact=True) without the colour image runs the threshold
+    kernel with an exhaustively settled margin (tone_u8_exact_kernel); the
+    colour kernel with rgb_out = NULL (WG_TONE_EXACT_VIA_RGB) is the other
+    exact route: identical bytes, steep (multi-threshold bins) curves included."""
+    import paper_2108_13656_b200 as wg
+
+    torch, dev = torch_dev
+    t = torch.from_numpy(cube).to(dev)
+    for curve in (wg.SigmoidCurve(), wg.SigmoidCurve(0.2, 60.0), wg.SigmoidCurve(0.55, 500.0)):
+        a, ga, _ = wg.decolor_tone(t, curve, return_gray=True, exact=True)
+        monkeypatch.setenv("WG_TONE_EXACT_VIA_RGB", "1")
+        b, gb, _ = wg.decolor_tone(t, curve, return_gray=True, exact=True)
+        monkeypatch.delenv("WG_TONE_EXACT_VIA_RGB")
+        assert torch.equal(a, b) and torch.equal(ga, gb)
 
 
 def test_tone_rgb_u8_bound_headroom(torch_dev, cube, monkeypatch):
