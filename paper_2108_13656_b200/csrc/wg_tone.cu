@@ -44,10 +44,20 @@ struct ToneTable {
     // exact route only (not staged by OpToneU8): 1 where a neighbouring bin's
     // threshold lies within kEdgeUnits (2^-15 units) of the shared edge
     uint8_t edge[kToneBins];
+    // single-threshold curves (multi == 0), staged by OpToneU8<.., false>:
+    // step[b] = 2048 count + (2048 - low of the bin's threshold, or 0 without
+    // one) - (bits of the bin's first f), mod 2^32, so that for f in bin b
+    // (step[b] + bits(f)) >> 11 is the toned byte: the carry out of the 11 low
+    // bits is the threshold compare (one LDS.32, an IADD and a shift per pixel)
+    uint32_t step[kToneBins];
 };
 constexpr uint32_t kEdgeUnits = 64;
 constexpr size_t kToneStaged = offsetof(ToneTable, edge);  // bytes OpToneU8 stages
 
+__device__ __forceinline__ uint32_t* step_smem() {
+    __shared__ __align__(16) uint32_t t[kToneBins];
+    return t;
+}
 __device__ __forceinline__ ToneTable* tone_smem() {
     __shared__ __align__(16) uint8_t t[kToneStaged];  // bins + thr (+ multi); edge is not staged here
     return reinterpret_cast<ToneTable*>(t);
@@ -65,13 +75,25 @@ struct OpToneU8 {
     const ToneTable* tab;
 
     __device__ __forceinline__ void prologue() const {
-        ToneTable* s = tone_smem();
-        const float4* src = reinterpret_cast<const float4*>(tab);
-        float4* dst = reinterpret_cast<float4*>(s);
-        for (int i = threadIdx.x; i < static_cast<int>(kToneStaged / 16); i += blockDim.x) dst[i] = src[i];
+        if constexpr (kMulti) {
+            ToneTable* s = tone_smem();
+            const float4* src = reinterpret_cast<const float4*>(tab);
+            float4* dst = reinterpret_cast<float4*>(s);
+            for (int i = threadIdx.x; i < static_cast<int>(kToneStaged / 16); i += blockDim.x) dst[i] = src[i];
+        } else {
+            const uint4* src = reinterpret_cast<const uint4*>(tab->step);
+            uint4* dst = reinterpret_cast<uint4*>(step_smem());
+            for (int i = threadIdx.x; i < kToneBins / 4; i += blockDim.x) dst[i] = src[i];
+        }
     }
     // toned byte from the f-domain bits of one pixel
     __device__ __forceinline__ uint32_t tone(uint32_t bits) const {
+        if constexpr (!kMulti) {
+            // byte offset of bin (bits >> 11) & 4095 in the step table
+            const uint32_t off = (bits >> 9) & ((kToneBins - 1) << 2);
+            const uint32_t e = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(step_smem()) + off);
+            return (e + bits) >> 11;
+        }
         const ToneTable* s = tone_smem();
         const float f = __uint_as_float(bits);
         const float2 e = s->bins[(bits >> 11) & (kToneBins - 1)];
@@ -182,6 +204,13 @@ void build_tone_table(double m, double k, ToneTable* t) {
         float base;
         std::memcpy(&base, &cnt, 4);
         t->bins[b] = make_float2(base, tin);
+        uint32_t e = cnt << 11;
+        if (inside - below == 1) {
+            uint32_t tb;
+            std::memcpy(&tb, &xf[below], 4);
+            e += 0x800u - (tb & 0x7FFu);  // tb's low bits 0 -> +2048: the whole bin counts it
+        }
+        t->step[b] = e - (0x43800000u + (static_cast<uint32_t>(b) << 11));  // bits(256 + b/16)
     }
     std::memset(t->edge, 0, sizeof(t->edge));
     for (int j = 0; j < 255; ++j) {
