@@ -34,6 +34,14 @@ struct HasPrologue : std::false_type {};
 template <class T>
 struct HasPrologue<T, std::void_t<decltype(&T::prologue)>> : std::true_type {};
 
+// An Op with `static constexpr bool kPingPong = true` gets ldg_stream_kernel's
+// loop unrolled twice over two register buffers (no copies of the prefetched
+// tile); ops whose math already fills the register budget keep one buffer.
+template <class T, class = void>
+struct PingPong : std::false_type {};
+template <class T>
+struct PingPong<T, std::void_t<decltype(T::kPingPong)>> : std::bool_constant<T::kPingPong> {};
+
 template <class Op>
 __device__ __forceinline__ void run_prologue(const Op& op) {
     if constexpr (HasPrologue<Op>::value) {
@@ -124,21 +132,37 @@ __global__ void __launch_bounds__(kBlock, kBlock == kThreads ? 5 : 20)
     const int tid = threadIdx.x;
     const int64_t stride = gridDim.x;
     int64_t t = blockIdx.x;
-    if (t < ntiles) {
-        const uint4* p = reinterpret_cast<const uint4*>(in + t * kBlockBytes) + tid * 3;
-        uint4 v[3] = {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)};
+    const auto load = [&](int64_t tt, uint4 (&d)[3]) {
+        const uint4* q = reinterpret_cast<const uint4*>(in + tt * kBlockBytes) + tid * 3;
+        d[0] = __ldcs(q);
+        d[1] = __ldcs(q + 1);
+        d[2] = __ldcs(q + 2);
+    };
+    if (t < ntiles && !PingPong<Op>::value) {
+        uint4 v[3];
+        load(t, v);
         for (; t < ntiles; t += stride) {
             uint4 n[3] = {v[0], v[1], v[2]};
-            if (t + stride < ntiles) {
-                const uint4* q = reinterpret_cast<const uint4*>(in + (t + stride) * kBlockBytes) + tid * 3;
-                n[0] = __ldcs(q);
-                n[1] = __ldcs(q + 1);
-                n[2] = __ldcs(q + 2);
-            }
+            if (t + stride < ntiles) load(t + stride, n);
             op.vec(v, t * kTilePx + static_cast<int64_t>(tid) * Op::kPx);
             v[0] = n[0];
             v[1] = n[1];
             v[2] = n[2];
+        }
+    } else if (t < ntiles) {
+        // two register buffers used in turn (the loop body is unrolled twice),
+        // so the prefetched tile is never copied between registers
+        uint4 a[3], b[3];
+        load(t, a);
+        for (;;) {
+            if (t + stride < ntiles) load(t + stride, b);
+            op.vec(a, t * kTilePx + static_cast<int64_t>(tid) * Op::kPx);
+            t += stride;
+            if (t >= ntiles) break;
+            if (t + stride < ntiles) load(t + stride, a);
+            op.vec(b, t * kTilePx + static_cast<int64_t>(tid) * Op::kPx);
+            t += stride;
+            if (t >= ntiles) break;
         }
     }
     if (blockIdx.x == gridDim.x - 1) {

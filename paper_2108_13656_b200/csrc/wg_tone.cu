@@ -67,6 +67,7 @@ __device__ __forceinline__ ToneTable* tone_smem() {
 template <bool kGray, bool kMulti>
 struct OpToneU8 {
     static constexpr bool kLdg = true;
+    static constexpr bool kPingPong = !kGray && !kMulti;  // the others would spill
     static constexpr int kPx = 16;
     const uint8_t* in;
     uint8_t* toned;
