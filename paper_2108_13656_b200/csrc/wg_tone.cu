@@ -850,7 +850,8 @@ extern "C" int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* g
     const U8Consts k = make_u8_consts(beta_r, beta_k);
     const void* outs[2] = {toned, gray_or_null};
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (multi) {
+    // WG_TONE_BINS64=1: the 8-byte-bin variant for every curve (A/B tests of the step words)
+    if (multi || std::getenv("WG_TONE_BINS64")) {
         if (gray_or_null)
             return launch_stream(OpToneU8<true, true>{rgb, toned, gray_or_null, k, tab}, rgb, outs, 2, npix, st);
         return launch_stream(OpToneU8<false, true>{rgb, toned, nullptr, k, tab}, rgb, outs, 2, npix, st);

@@ -243,6 +243,26 @@ def test_tone_u8_cube(torch_dev, cube):
         assert torch.equal(wg.decolor_tone(t, wg.SigmoidCurve(m, k)), toned)
 
 
+def test_tone_u8_step_words_equal_bins(torch_dev, cube, monkeypatch):
+    """The single-threshold curves' 32-bit step words ((step + bits) >> 11) give
+    the same bytes as the 8-byte bins (count + float compare), over all 2^24
+    colours, toned-only and with gray."""
+    import paper_2108_13656_b200 as wg
+
+    torch, dev = torch_dev
+    t = torch.from_numpy(cube).to(dev)
+    for m, k in [(0.5, 8.0), (0.3, 12.0), (0.5, 1e-6), (0.0, 3.0), (1.0, 3.0), (0.45, 60.0)]:
+        curve = wg.SigmoidCurve(m, k)
+        a = wg.decolor_tone(t, curve)
+        ta, ga, _ = wg.decolor_tone(t, curve, return_gray=True)
+        monkeypatch.setenv("WG_TONE_BINS64", "1")
+        b = wg.decolor_tone(t, curve)
+        tb, gb, _ = wg.decolor_tone(t, curve, return_gray=True)
+        monkeypatch.delenv("WG_TONE_BINS64")
+        assert torch.equal(a, b) and torch.equal(ta, tb) and torch.equal(ga, gb), (m, k)
+        assert torch.equal(a, ta)
+
+
 def test_tone_rgb_u8_golden_and_cube(torch_dev, cube):
     """Colour output of the global tone map: bit-identical (fp64 chain per pixel)."""
     import paper_2108_13656_b200 as wg
