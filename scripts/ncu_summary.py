@@ -65,9 +65,10 @@ def main():
         rd = to_float(r[col["dram__bytes_read.sum"]]) if "dram__bytes_read.sum" in col else None
         wr = to_float(r[col["dram__bytes_write.sum"]]) if "dram__bytes_write.sum" in col else None
         if rd is not None and wr is not None:
-            unit = units[col["dram__bytes_read.sum"]]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            traffic = (rd + wr) * scale
+            scales = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            # ncu picks the unit per metric (e.g. Gbyte read, Mbyte written)
+            traffic = (rd * scales.get(units[col["dram__bytes_read.sum"]], 1)
+                       + wr * scales.get(units[col["dram__bytes_write.sum"]], 1))
             print(f"| traffic = read + write | {traffic:.6g} | byte |")
             if args.algo_bytes:
                 print(f"| traffic / algorithmic bytes | {traffic / args.algo_bytes:.4f} | |")
