@@ -68,6 +68,15 @@ struct Theta {
     double v[255];
 };
 
+// Programmatic dependent launch (stats and tone grids are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): the dependent grid's
+// launch overlaps its predecessor's completion, and griddepcontrol.wait blocks
+// until the predecessor has completed and its writes are visible (a no-op for
+// a grid launched without the attribute). C4: 293.7 -> 296.3 Gpix/s. An early
+// griddepcontrol.launch_dependents in the gray / stats grids measured slower
+// (291.7): the stats CTAs then sit on SM slots during the gray pass's last wave.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void discard_l2_line(const void* p) {
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
@@ -200,6 +209,7 @@ __global__ void __launch_bounds__(kT) hdr_stats_kernel(const float2* __restrict_
     __shared__ float s_thr[kLutBins];
     __shared__ int s_wsum[kWarps];
     const int img = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_wait();  // the gray pass's slots are complete and visible
     const float2* slots = parts + static_cast<int64_t>(img) * kSlots;
     float lo = INFINITY, hi = 0.0f;
     for (int q = tid; q < nslots; q += kT) {
@@ -414,6 +424,7 @@ __global__ void __launch_bounds__(kT) hdr_tone_tiled_kernel(const float* __restr
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint32_t s_lut[kLutBins];
     const int64_t img = blockIdx.y;
+    pdl_wait();  // stats / tables of the previous (stats) grid
     const HdrStat st = stats[img];
     const float* g = gray + img * ppi;
     uint8_t* o = out + img * ppi;
@@ -437,6 +448,7 @@ __global__ void __launch_bounds__(kT) hdr_tone_kernel(const float* __restrict__ 
                                                       bool discard) {
     __shared__ uint32_t s_lut[kLutBins];
     const int64_t img = blockIdx.y;
+    pdl_wait();  // stats / tables of the previous (stats) grid
     const HdrStat st = stats[img];
     const float* g = gray + img * ppi;
     uint8_t* o = out + img * ppi;
@@ -707,6 +719,26 @@ size_t l2_budget() {
     const char* e = getenv("WG_HDR_L2_BUDGET_MB");  // tuning knob (scripts/), default kL2Budget
     return e ? static_cast<size_t>(atoll(e)) << 20 : kL2Budget;
 }
+// launch with programmatic stream serialization (PDL) when `pdl`, else a plain launch
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, cudaStream_t s, bool pdl, Args... args) {
+    if (!pdl || getenv("WG_HDR_NO_PDL")) {
+        kern<<<grid, kT, 0, s>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 int group_size(int64_t nimg, int64_t ppi) {
     const int64_t fit = static_cast<int64_t>(l2_budget() / (static_cast<size_t>(ppi) * sizeof(float)));
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({fit, nimg, kMaxGroup})));
@@ -885,7 +917,8 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
             cudaEventRecord(hs->gray_done[gi % 2], st);
             cudaStreamWaitEvent(sb, hs->gray_done[gi % 2], 0);
         }
-        hdr_stats_kernel<<<g, kT, 0, sb>>>(parts, static_cast<int>(bx) * kWarps, stats, luts, theta);
+        launch_pdl(hdr_stats_kernel, dim3(static_cast<unsigned>(g)), sb, sb == st, parts, static_cast<int>(bx) * kWarps,
+                   stats, luts, theta);
         const int64_t twork = (pix_per_img & 15) == 0 ? pix_per_img / 16 : pix_per_img;
         const int64_t bt = std::max<int64_t>(1, std::min<int64_t>((twork + kT - 1) / kT, std::max<int64_t>(1, 8LL * sms / g)));
         // drop the gray lines from L2 only when the group's plane can actually be resident there
@@ -905,8 +938,9 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
             hdr_tone_tiled_kernel<<<dim3(static_cast<unsigned>(bt2), static_cast<unsigned>(g)), kT, kToneSmem, sb>>>(
                 gray, out + i0 * pix_per_img, pix_per_img, stats, luts, midpoint, slope, discard);
         } else {
-            hdr_tone_kernel<<<dim3(static_cast<unsigned>(bt), static_cast<unsigned>(g)), kT, 0, sb>>>(
-                gray, out + i0 * pix_per_img, pix_per_img, stats, luts, midpoint, slope, discard);
+            launch_pdl(hdr_tone_kernel, dim3(static_cast<unsigned>(bt), static_cast<unsigned>(g)), sb, true,
+                       static_cast<const float*>(gray), out + i0 * pix_per_img, pix_per_img,
+                       static_cast<const HdrStat*>(stats), static_cast<const float2*>(luts), midpoint, slope, discard);
         }
         if (nsets == 2) cudaEventRecord(hs->tone_done[gi % 2], sb);
         const int rc = check_launch("hdr_tonemap_u8");
