@@ -674,17 +674,16 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
 struct ApplySmem {
     static __host__ __device__ int64_t wpad(int64_t w) { return (w + kGrp - 1) / kGrp * kGrp; }
     static __host__ __device__ size_t bytes(int nx, int nb, int64_t w) {
-        return static_cast<size_t>(3) * nx * nb * 4 + static_cast<size_t>(wpad(w)) * 8 + 16 + kWqBytes;
+        return static_cast<size_t>(nx) * nb * 16 + static_cast<size_t>(wpad(w)) * 6 + 16 + kWqBytes;
     }
 };
 
 template <bool kGray, bool kIdent, bool kPacked>
 __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict__ toned, uint8_t* __restrict__ gray,
                                              const LheGeom& g, const LheBufs& s, int64_t y0, int64_t y1, int64_t img,
-                                             int jbase, const float* cur, const float* sxf, const uint32_t* sxo,
+                                             const float4* quad, const float* sxf, const uint16_t* sxo,
                                              int64_t G, bool vec, uint32_t* wq) {
     const float sf = static_cast<float>(g.strength);
-    const int dnb = g.nx > 1 ? g.nb : 0;  // i1 - i0 in curve-table units
     const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
     const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
     // the hist pass's gray estimates (identical to recomputing them), one group of
@@ -751,9 +750,7 @@ __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict
             g255[4 * q + 3] = nxt[q].w;
         }
         if (gi + blockDim.x < ngroups) load_est(gi + blockDim.x, nxt);
-        const int j0 = s.yi[y], j1 = g.ny > 1 ? j0 + 1 : 0;
-        const int r0nb = (j0 - jbase) * g.nx * g.nb, drow = (j1 - j0) * g.nx * g.nb;
-        const float wy = s.yff[y];
+        const float wy = s.yff[y];  // every row of the block blends the same tile-row pair
         // the group's 16 blend fractions and curve offsets as 128-bit shared loads
         float wxs[kGrp];
         uint32_t xos[kGrp];
@@ -761,15 +758,15 @@ __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict
 #pragma unroll
         for (int q = 0; q < kGrp / 4; ++q) {
             const float4 f = reinterpret_cast<const float4*>(sxf)[q * G + gcol];
-            const uint4 o = reinterpret_cast<const uint4*>(sxo)[q * G + gcol];
+            const uint2 o = reinterpret_cast<const uint2*>(sxo)[q * G + gcol];
             wxs[4 * q] = f.x;
             wxs[4 * q + 1] = f.y;
             wxs[4 * q + 2] = f.z;
             wxs[4 * q + 3] = f.w;
-            xos[4 * q] = o.x;
-            xos[4 * q + 1] = o.y;
-            xos[4 * q + 2] = o.z;
-            xos[4 * q + 3] = o.w;
+            xos[4 * q] = o.x & 0xFFFFu;
+            xos[4 * q + 1] = o.x >> 16;
+            xos[4 * q + 2] = o.y & 0xFFFFu;
+            xos[4 * q + 3] = o.y >> 16;
         }
         uint32_t ot[4] = {0u, 0u, 0u, 0u}, og[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -786,8 +783,8 @@ __device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict
                 v = g255[p];
                 b = L.bin_fast(v, sure);
             }
-            const int a00 = r0nb + static_cast<int>(xos[p]) + b, a10 = a00 + drow;
-            float c00 = cur[a00], c01 = cur[a00 + dnb], c10 = cur[a10], c11 = cur[a10 + dnb];
+            const float4 cq = quad[static_cast<int>(xos[p]) + b];  // the four curves: one LDS.128
+            float c00 = cq.x, c01 = cq.y, c10 = cq.z, c11 = cq.w;
             if constexpr (kIdent) {
                 c00 = c00 != c00 ? v : c00;  // NaN: identity tile (the pixel's own value)
                 c01 = c01 != c01 ? v : c01;
@@ -837,20 +834,32 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
                                                                int rows_per_chunk, bool vec) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int64_t img = blockIdx.z;
-    const int ty = blockIdx.y;
-    const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
-    const int64_t y1 = imin64(imin64(y0 + rows_per_chunk, static_cast<int64_t>(ty + 1) * g.th), g.h);
+    // Blocks cover bands of rows between consecutive tile-row centres (yi[y] ==
+    // band for every row of band `band`, lhe_axis_kernel), so all rows of a
+    // block blend the same pair of tile rows (j0, j1) = (band, band + 1), or
+    // (0, 0) for a single tile row.
+    const int band = blockIdx.y, nband = g.ny > 1 ? g.ny - 1 : 1;
+    const int64_t lo = band == 0 ? 0 : static_cast<int64_t>(ceil(centre(band, g.th, g.h)));
+    const int64_t hi = band == nband - 1 ? g.h : static_cast<int64_t>(ceil(centre(band + 1, g.th, g.h)));
+    const int64_t y0 = lo + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
+    const int64_t y1 = imin64(y0 + rows_per_chunk, hi);
     if (y0 >= y1) return;
-    // rows of this tile row blend tile rows {ty-1, ty, ty+1} at most
-    const int jbase = max(ty - 1, 0), nload = min(ty + 1, g.ny - 1) - jbase + 1;
+    const int jbase = g.ny > 1 ? band : 0, jrow = g.ny > 1 ? 1 : 0;  // j0 and j1 - j0
     const int64_t wp = ApplySmem::wpad(g.w);
-    float* cur = reinterpret_cast<float*>(smem);              // [3][nx][nb]: 255 * curve, NaN = identity
-    float* sxf = cur + static_cast<size_t>(3) * g.nx * g.nb;  // [wp]
-    uint32_t* sxo = reinterpret_cast<uint32_t*>(sxf + wp);    // [wp] i0 * nb
-    uint32_t* wq = sxo + wp + 4 + (threadIdx.x >> 5) * kWq;     // per-warp queues (after 16 B of slack)
-    const int64_t tile0 = img * g.ntile + static_cast<int64_t>(jbase) * g.nx;
-    const int ncur = nload * g.nx * g.nb;
-    for (int i = threadIdx.x; i < ncur; i += blockDim.x) cur[i] = s.curvef[tile0 * g.nb + i];
+    // quad[i0][b] = the four curves (j0,i0), (j0,i1), (j1,i0), (j1,i1) at bin b
+    // (255 * curve, NaN = identity tile; i1 = i0 + 1, or i0 for a single tile
+    // column): one 128-bit shared load per pixel instead of four random 32-bit ones
+    float4* quad = reinterpret_cast<float4*>(smem);                                 // [nx][nb]
+    float* sxf = reinterpret_cast<float*>(quad + static_cast<size_t>(g.nx) * g.nb);  // [wp]
+    uint16_t* sxo = reinterpret_cast<uint16_t*>(sxf + wp);                          // [wp] i0 * nb
+    uint32_t* wq = reinterpret_cast<uint32_t*>(sxo + wp) + 4 + (threadIdx.x >> 5) * kWq;  // per-warp queues
+    const float* cf = s.curvef + (img * g.ntile + static_cast<int64_t>(jbase) * g.nx) * g.nb;
+    const int rowoff = jrow * g.nx * g.nb;
+    for (int i = threadIdx.x; i < g.nx * g.nb; i += blockDim.x) {
+        const int b = i % g.nb, i0 = i / g.nb, i1 = g.nx > 1 ? min(i0 + 1, g.nx - 1) : i0;
+        quad[i] = make_float4(cf[i0 * g.nb + b], cf[i1 * g.nb + b], cf[rowoff + i0 * g.nb + b],
+                              cf[rowoff + i1 * g.nb + b]);
+    }
     // column x = 16 gc + 4 q + r is stored at ((q * G + gc) * 4 + r), G = wp / 16: the
     // lanes of a warp (consecutive groups gc) then read consecutive 16-byte vectors
     const int64_t G = wp / kGrp;
@@ -859,17 +868,17 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
         const int64_t gc = x / kGrp, q = (x % kGrp) >> 2, r = x & 3;
         const int64_t at = (q * G + gc) * 4 + r;
         sxf[at] = s.xff[xc];
-        sxo[at] = static_cast<uint32_t>(s.xi[xc] * g.nb);
+        sxo[at] = static_cast<uint16_t>(s.xi[xc] * g.nb);  // < 2^16 (checked by the launcher)
     }
     __syncthreads();
     // identity tiles (NaN curves) are rare: the per-pixel NaN selects only run in
     // blocks whose staged curve rows contain one
     bool any_ident = false;
-    for (int i = threadIdx.x; i < nload * g.nx; i += blockDim.x) any_ident |= cur[i * g.nb] != cur[i * g.nb];
+    for (int i = threadIdx.x; i < (1 + jrow) * g.nx; i += blockDim.x) any_ident |= cf[i * g.nb] != cf[i * g.nb];
     if (__syncthreads_or(any_ident))
-        apply_groups<kGray, true, kPacked>(L, toned, gray, g, s, y0, y1, img, jbase, cur, sxf, sxo, G, vec, wq);
+        apply_groups<kGray, true, kPacked>(L, toned, gray, g, s, y0, y1, img, quad, sxf, sxo, G, vec, wq);
     else
-        apply_groups<kGray, false, kPacked>(L, toned, gray, g, s, y0, y1, img, jbase, cur, sxf, sxo, G, vec, wq);
+        apply_groups<kGray, false, kPacked>(L, toned, gray, g, s, y0, y1, img, quad, sxf, sxo, G, vec, wq);
 }
 
 // ------------------------------------------------------------------ driver
@@ -1052,7 +1061,8 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     // group apply reads the gray plane the group hist writes, so both or neither
     // (the per-warp queue entries are group * 16 + pixel within one row chunk: < 2^32)
     const bool group_ok = bins <= 65536 && hsmem <= kHistSmemCap && asmem <= kApplySmemCap &&
-                          static_cast<int64_t>(c.rows_per_chunk) * ApplySmem::wpad(g.w) < (int64_t(1) << 32);
+                          static_cast<int64_t>(c.rows_per_chunk) * ApplySmem::wpad(g.w) < (int64_t(1) << 32) &&
+                          static_cast<int64_t>(g.nx) * g.nb <= 65536;  // u16 column offsets i0 * nb
     const bool packed = bins <= 512;  // the plane word carries the bin (9 bits)
     if (group_ok) {
         auto hk = packed ? lhe_hist_u8g_kernel<true> : lhe_hist_u8g_kernel<false>;
@@ -1082,7 +1092,9 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
             bi.ident += i0 * g.ntile;
             const int64_t off = i0 * g.h * g.w;
             bi.gray255 += off;
-            kern<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, asmem, st>>>(
+            // row bands between tile-row centres are at most ~1.5 tile heights (+2 rows)
+            const int achunks = static_cast<int>((2LL * g.th + 2 + c.rows_per_chunk - 1) / c.rows_per_chunk);
+            kern<<<dim3(achunks, g.ny > 1 ? g.ny - 1 : 1, static_cast<unsigned>(gi.nimg)), kBlock, asmem, st>>>(
                 Li, toned + off, gray_or_null ? gray_or_null + off : nullptr, gi, bi, c.rows_per_chunk, vec);
         });
     } else {
