@@ -59,6 +59,15 @@ def _stream(stream, device):
     return s.cuda_stream
 
 
+def _check_out(out, shape, like, dtype=None):
+    """A caller-supplied output tensor: contiguous, ``shape``, ``like``'s device, ``dtype`` (default like's)."""
+    dtype = like.dtype if dtype is None else dtype
+    if tuple(out.shape) != tuple(shape) or out.dtype != dtype or not out.is_contiguous() \
+            or out.device != like.device:
+        raise ValueError(f"out must be a contiguous {dtype} tensor of shape {tuple(shape)} on {like.device}")
+    return out
+
+
 def decolor(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, stream=None, exact: bool = False):
     """Gray of a device-resident (..., 3) uint8 / float32 / float64 batch.
 
@@ -68,11 +77,8 @@ def decolor(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, stream=None, 
     """
     torch = _torch()
     name = _check_rgb_tensor(rgb, _DECOLOR_FN)
-    if out is None:
-        out = torch.empty(rgb.shape[:-1], dtype=rgb.dtype, device=rgb.device)
-    elif out.shape != rgb.shape[:-1] or out.dtype != rgb.dtype or not out.is_contiguous() \
-            or out.device != rgb.device:
-        raise ValueError("out must be a contiguous tensor of shape rgb.shape[:-1], same dtype/device")
+    out = _check_out(out, rgb.shape[:-1], rgb) if out is not None else \
+        torch.empty(rgb.shape[:-1], dtype=rgb.dtype, device=rgb.device)
     n = out.numel()
     fn = "wg_decolor_u8_exact" if exact and name == "uint8" else _DECOLOR_FN[name]
     with torch.cuda.device(rgb.device):
@@ -81,7 +87,8 @@ def decolor(rgb, params: DecolorParams = DEFAULT_PARAMS, out=None, stream=None, 
 
 
 def decolor_tone(rgb, curve: SigmoidCurve = SigmoidCurve(), params: DecolorParams = DEFAULT_PARAMS,
-                 return_gray: bool = False, return_rgb: bool = False, stream=None, exact: bool = False):
+                 return_gray: bool = False, return_rgb: bool = False, stream=None, exact: bool = False,
+                 out=None):
     """Fused decolor + global sigmoid on a device batch.
 
     uint8 -> toned uint8 (and gray uint8 if ``return_gray``; with
@@ -92,12 +99,14 @@ def decolor_tone(rgb, curve: SigmoidCurve = SigmoidCurve(), params: DecolorParam
     rigorous error bound, the fp64 chain for pixels in doubt).
     float32 -> toned float32 (+ gray, + reinstated rgb if requested).
     Returns the toned tensor, or a tuple ``(toned, gray, rgb_out)`` with
-    ``None`` for outputs not requested when either flag is set.
+    ``None`` for outputs not requested when either flag is set. ``out``: a
+    preallocated toned tensor (contiguous, rgb's dtype and device, shape
+    ``rgb.shape[:-1]``).
     """
     torch = _torch()
     name = _check_rgb_tensor(rgb, ("uint8", "float32"))
     shape = rgb.shape[:-1]
-    toned = torch.empty(shape, dtype=rgb.dtype, device=rgb.device)
+    toned = _check_out(out, shape, rgb) if out is not None else torch.empty(shape, dtype=rgb.dtype, device=rgb.device)
     gray = torch.empty(shape, dtype=rgb.dtype, device=rgb.device) if return_gray else None
     rgb_out = None
     with torch.cuda.device(rgb.device):

@@ -22,6 +22,14 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 32-bit load from a shared-memory (CTA window) address; non-volatile, so the
+// compiler schedules it like a plain LDS and folds address arithmetic into it
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
                  : "memory");
@@ -110,6 +118,11 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
 __device__ __forceinline__ float2 add2_rz(float2 a, float2 b) {
     unsigned long long d;
     asm("add.rz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)));
+    return upk(d);
+}
+__device__ __forceinline__ float2 add2_rm(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk(a)), "l"(pk(b)));
     return upk(d);
 }
 __device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
@@ -314,6 +327,51 @@ __device__ __forceinline__ float2 decolor255_bits_x2(float2 R, float2 G, float2 
     float2 X = fma2(T, S2k, bc2(1e-30f));
     float2 y = make_float2(rsqrt_mufu(X.x), rsqrt_mufu(X.y));
     return fma2(T, y, bc2(kMagicFrac));
+}
+// The model's T and S of a pixel pair, T as in decolor255_bits_x2 and S
+// returned biased by 2^23 (Sb = (R + G) + (B + 2^23), exact: its float bits
+// are 0x4B000000 + S), for the square-domain routes that never take the
+// final root: (gray255)^2 = T c4^2 / S^2 (csrc/wg_tone.cu OpToneSqU8).
+__device__ __forceinline__ void decolor255_T_x2(float2 R, float2 G, float2 B, float2 Bb, const U8Consts& k,
+                                                float2& T, float2& Sb) {
+    float2 R2 = mul2(R, R);
+    float2 G2 = mul2(G, G);
+    float2 RG2 = add2(R2, G2);
+    float2 q = fma2(B, B, RG2);
+    float2 p = fma2(R2, bc2(k.cr), G2);
+    float2 Rc1 = mul2(R, bc2(k.c1));
+    float2 W = make_float2(sqrt_mufu(q.x), sqrt_mufu(q.y));
+    float2 RGq = make_float2(sqrt_mufu(p.x), sqrt_mufu(p.y));
+    float2 RG = add2(R, G);
+    Sb = add2(RG, Bb);
+    float2 GB = add2(G, B);
+    float2 t1 = mul2(GB, W);
+    float2 A = fma2(Rc1, RGq, t1);
+    float2 u = fma2(RG, bc2(k.sqrt3), W);
+    float2 Bp = mul2(B, u);
+    float2 B2 = mul2(Bp, Bp);
+    float2 A2 = mul2(A, A);
+    T = fma2(B2, bc2(k.c3), A2);
+}
+__device__ __forceinline__ void decolor255_T_x1(float r, float g, float b, const U8Consts& k, float& T, float& S) {
+    float R2 = __fmul_rn(r, r);
+    float G2 = __fmul_rn(g, g);
+    float RG2 = __fadd_rn(R2, G2);
+    float q = __fmaf_rn(b, b, RG2);
+    float p = __fmaf_rn(R2, k.cr, G2);
+    float Rc1 = __fmul_rn(r, k.c1);
+    float W = sqrt_mufu(q);
+    float RGq = sqrt_mufu(p);
+    float RG = __fadd_rn(r, g);
+    S = __fadd_rn(RG, b);
+    float GB = __fadd_rn(g, b);
+    float t1 = __fmul_rn(GB, W);
+    float A = __fmaf_rn(Rc1, RGq, t1);
+    float u = __fmaf_rn(RG, k.sqrt3, W);
+    float Bp = __fmul_rn(b, u);
+    float B2 = __fmul_rn(Bp, Bp);
+    float A2 = __fmul_rn(A, A);
+    T = __fmaf_rn(B2, k.c3, A2);
 }
 // scalar twin (lane-exact: identical IEEE rn operation sequence)
 __device__ __forceinline__ uint32_t decolor255_bits_x1(float r, float g, float b, const U8Consts& k) {

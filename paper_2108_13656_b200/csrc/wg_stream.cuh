@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "wg_device.cuh"
@@ -41,6 +42,18 @@ template <class T, class = void>
 struct PingPong : std::false_type {};
 template <class T>
 struct PingPong<T, std::void_t<decltype(T::kPingPong)>> : std::bool_constant<T::kPingPong> {};
+
+// Optional Op traits of ldg_stream_kernel's 256-thread shape: kMinBlocks
+// (resident CTAs per SM the register budget is cut for; default 5) and
+// kGridPerSm (CTAs launched per SM; default 40).
+template <class T, class = void>
+struct MinBlocks : std::integral_constant<int, 5> {};
+template <class T>
+struct MinBlocks<T, std::void_t<decltype(T::kMinBlocks)>> : std::integral_constant<int, T::kMinBlocks> {};
+template <class T, class = void>
+struct GridPerSm : std::integral_constant<int, 40> {};
+template <class T>
+struct GridPerSm<T, std::void_t<decltype(T::kGridPerSm)>> : std::integral_constant<int, T::kGridPerSm> {};
 
 template <class Op>
 __device__ __forceinline__ void run_prologue(const Op& op) {
@@ -124,7 +137,7 @@ __global__ void __launch_bounds__(kThreads) stream_kernel(Op op, const uint8_t* 
 // couple of waves) use 64-thread CTAs so a single image still spreads over
 // every SM (C1: 256 CTAs instead of 64).
 template <class Op, int kBlock = kThreads>
-__global__ void __launch_bounds__(kBlock, kBlock == kThreads ? 5 : 20)
+__global__ void __launch_bounds__(kBlock, kBlock == kThreads ? MinBlocks<Op>::value : 20)
     ldg_stream_kernel(Op op, const uint8_t* __restrict__ in, int64_t ntiles, int64_t npix) {
     constexpr int kTilePx = kBlock * Op::kPx;
     constexpr int64_t kBlockBytes = kBlock * 48;
@@ -218,7 +231,9 @@ static int launch_stream(const Op& op, const void* in, const void* const* outs, 
         ldg_stream_kernel<Op, kSmall><<<static_cast<unsigned>(grid), kSmall, 0, stream>>>(
             op, static_cast<const uint8_t*>(in), st, npix);
     } else if (aligned && Op::kLdg) {
-        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, 40LL * sm_count(device)));
+        int64_t per_sm = GridPerSm<Op>::value;
+        if (const char* e = std::getenv("WG_LDG_GRID_PER_SM")) per_sm = std::max(1, std::atoi(e));  // tuning knob
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, per_sm * sm_count(device)));
         ldg_stream_kernel<Op><<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(
             op, static_cast<const uint8_t*>(in), ntiles, npix);
     } else if (aligned) {

@@ -5,15 +5,20 @@
 // The toned byte is a monotone step function of the gray v: it is the number
 // of the 255 thresholds theta_j (least v whose toned byte reaches j) that v
 // reaches. The host finds them by bisection over the reference's fp64
-// logistic + clip + round-half-up (once per curve, cached per device). The
-// kernel computes the gray with the decolor kernel's packed MUFU sequence,
-// keeping 15 fraction bits of f = 256 + (255 v + 0.5) (decolor255_bits_x2), and
-// replaces exp / tanh / division by one shared-memory lookup: 4096 bins of
-// x = 255 v + 0.5 (bin = bits >> 11), each holding the count of thresholds
-// below it and the one threshold inside it, compared in the f domain. Bins
-// holding two or more thresholds (curves steeper than ~16 thresholds per
-// gray level) fall back to a binary search over all 255. The optional gray
-// output is the rounded gray of the same computation (bits >> 15).
+// logistic + clip + round-half-up (once per curve, cached per device), and
+// the kernels replace exp / tanh / division by one shared-memory "step word"
+// per pixel whose byte 3, after adding the pixel's float bits, is the toned
+// byte. Two routes:
+//  * square domain (default, OpToneSqU8): the step words are indexed by
+//    u = (255 v)^2 + 1/8 = T W[S] + 1/8, so the decolor's final rsqrt is never
+//    taken (W[S] = c4^2 / S^2 comes from a 768-entry shared table, S = r+g+b
+//    being an integer) -- 2 MUFU per pixel instead of 3, the MUFU (XU) pipe
+//    being what binds the decolor kernel;
+//  * linear (OpToneU8): the decolor kernel's packed MUFU sequence keeping 15
+//    fraction bits of f = 256 + (255 v + 0.5) and 4096 bins of 255 v + 0.5;
+//    used when a square-domain bin would hold several thresholds, with 8-byte
+//    bins and a binary search when even linear bins do (k >~ 100).
+// The optional gray output is the rounded gray of the same computation.
 // Parity: the north-star bar (+-1 on <= 0.01%; only pixels whose gray lies
 // within the fp32 error of a threshold or a rounding boundary can differ).
 #include <cuda_runtime.h>
@@ -35,6 +40,10 @@ namespace wg {
 namespace {
 
 constexpr int kToneBins = 4096;  // bins of x = 255 v + 0.5 over [0, 256), width 1/16
+constexpr int kSqBins = 19 * 256;          // square-domain bins: 19 octaves [2^-3, 2^16), 256 per octave
+constexpr uint32_t kSqLoBits = 0x3E000000u;  // bits of 2^-3, the first square-domain bin
+constexpr float kSqBias = 0.125f;            // u = (255 v)^2 + 2^-3 >= 2^-3 for every pixel (black too)
+constexpr int kSqW = 768;                    // W[S] = c4^2 / S^2 for S = r + g + b in [0, 765]
 
 struct ToneTable {
     float2 bins[kToneBins];  // {count of thresholds below the bin (as bits), f-domain threshold inside or NaN}
@@ -45,11 +54,24 @@ struct ToneTable {
     // threshold lies within kEdgeUnits (2^-15 units) of the shared edge
     uint8_t edge[kToneBins];
     // single-threshold curves (multi == 0), staged by OpToneU8<.., false>:
-    // step[b] = 2048 count + (2048 - low of the bin's threshold, or 0 without
-    // one) - (bits of the bin's first f), mod 2^32, so that for f in bin b
-    // (step[b] + bits(f)) >> 11 is the toned byte: the carry out of the 11 low
-    // bits is the threshold compare (one LDS.32, an IADD and a shift per pixel)
+    // step[b] = 2^24 count + (2^24 - L) - (bits of the bin's first f), mod
+    // 2^32, L = the low 11 bits of the bin's threshold (2048 without one), so
+    // that for f in bin b byte 3 of step[b] + bits(f) is the toned byte: the
+    // in-bin offset minus L borrows from (or carries into) bit 24 exactly when
+    // f is below (at or above) the threshold -- one LDS.32 and an IADD per
+    // pixel, and the pack's PRMT picks byte 3 directly (no shift)
     uint32_t step[kToneBins];
+    // square-domain route (OpToneSqU8): u = (255 v)^2 + 1/8 in [2^-3, 2^16),
+    // 256 log-spaced bins per octave (bin = float bits >> 15), step words as
+    // above with a 15-bit in-bin offset: step[b] = 2^24 count + (2^24 - L) -
+    // (bits of the bin's first u), L = the low 15 bits of the bin's threshold
+    // (2^15 without one). sq_gray holds the rounding thresholds (j - 1/2)^2 + 1/8
+    // of quantize_u8 (the gray byte), sq_multi flags bins with several toned
+    // thresholds (then the linear route above runs).
+    uint32_t sq_step[kSqBins];
+    uint32_t sq_gray[kSqBins];
+    int sq_multi;
+    int sq_pad[3];
 };
 constexpr uint32_t kEdgeUnits = 64;
 constexpr size_t kToneStaged = offsetof(ToneTable, edge);  // bytes OpToneU8 stages
@@ -63,7 +85,11 @@ __device__ __forceinline__ ToneTable* tone_smem() {
     return reinterpret_cast<ToneTable*>(t);
 }
 
-// kMulti: the curve's table has bins holding several thresholds (steep curves)
+// Linear route (WG_TONE_ROUTE=linear, and curves whose square-domain table
+// has a bin with several thresholds). kMulti: the curve's linear table has
+// such bins too (steep curves): 8-byte bins and a binary search.
+// (r02 A/B on C3, toned only: one register buffer, 4 or 6 CTAs/SM and 10/20
+// CTAs per SM all lost to two buffers at 5 CTAs/SM and 40 per SM.)
 template <bool kGray, bool kMulti>
 struct OpToneU8 {
     static constexpr bool kLdg = true;
@@ -87,14 +113,19 @@ struct OpToneU8 {
             for (int i = threadIdx.x; i < kToneBins / 4; i += blockDim.x) dst[i] = src[i];
         }
     }
-    // toned byte from the f-domain bits of one pixel
+    // step route: the word whose byte 3 is the toned byte of f. gbits = bits
+    // of g = fl_rm(f + (2^17 - 256)) = 2^17 + floor(64 x) / 64 (exact floor:
+    // f - 256 = x is exact and the ulp of g is 2^-6), so gbits & 0x3FFC =
+    // 4 floor(16 x) is the byte offset of f's bin (bits(f) >> 11) & 4095 --
+    // one FADD2.RM per pixel pair and a LOP3 instead of a shift and a mask
+    static constexpr float kBinAdd = 130816.0f;  // 2^17 - 256
+    __device__ __forceinline__ uint32_t step_word(uint32_t gbits, uint32_t bits) const {
+        const uint32_t e =
+            *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(step_smem()) + (gbits & 0x3FFCu));
+        return e + bits;
+    }
+    // toned byte from the f-domain bits of one pixel (kMulti tables)
     __device__ __forceinline__ uint32_t tone(uint32_t bits) const {
-        if constexpr (!kMulti) {
-            // byte offset of bin (bits >> 11) & 4095 in the step table
-            const uint32_t off = (bits >> 9) & ((kToneBins - 1) << 2);
-            const uint32_t e = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(step_smem()) + off);
-            return (e + bits) >> 11;
-        }
         const ToneTable* s = tone_smem();
         const float f = __uint_as_float(bits);
         const float2 e = s->bins[(bits >> 11) & (kToneBins - 1)];
@@ -129,12 +160,19 @@ struct OpToneU8 {
                 }
                 const float2 f = decolor255_bits_x2(ch[0], ch[1], ch[2], k);
                 const uint32_t x = __float_as_uint(f.x), y = __float_as_uint(f.y);
-                t[2 * h] = tone(x);
-                t[2 * h + 1] = tone(y);
+                if constexpr (kMulti) {
+                    t[2 * h] = tone(x);
+                    t[2 * h + 1] = tone(y);
+                } else {
+                    const float2 g = add2_rm(f, bc2(kBinAdd));
+                    t[2 * h] = step_word(__float_as_uint(g.x), x);
+                    t[2 * h + 1] = step_word(__float_as_uint(g.y), y);
+                }
                 q[2 * h] = x >> 15;
                 q[2 * h + 1] = y >> 15;
             }
-            tw[qd] = __byte_perm(__byte_perm(t[0], t[1], 0x0040u), __byte_perm(t[2], t[3], 0x0040u), 0x5410u);
+            constexpr uint32_t sel = kMulti ? 0x0040u : 0x0073u;  // low byte / byte 3 of each word
+            tw[qd] = __byte_perm(__byte_perm(t[0], t[1], sel), __byte_perm(t[2], t[3], sel), 0x5410u);
             if constexpr (kGray)
                 gw[qd] = __byte_perm(__byte_perm(q[0], q[1], 0x0040u), __byte_perm(q[2], q[3], 0x0040u), 0x5410u);
         }
@@ -144,8 +182,127 @@ struct OpToneU8 {
     __device__ __forceinline__ void scalar(int64_t p) const {
         const uint32_t bits = decolor255_bits_x1(static_cast<float>(in[3 * p]), static_cast<float>(in[3 * p + 1]),
                                                  static_cast<float>(in[3 * p + 2]), k);
-        toned[p] = static_cast<uint8_t>(tone(bits));
+        if constexpr (kMulti)
+            toned[p] = static_cast<uint8_t>(tone(bits));
+        else
+            toned[p] = static_cast<uint8_t>(
+                step_word(__float_as_uint(__fadd_rd(__uint_as_float(bits), kBinAdd)), bits) >> 24);
         if constexpr (kGray) gray[p] = static_cast<uint8_t>(bits >> 15);
+    }
+};
+
+// Square-domain route: toned (and gray) bytes without the final root.
+// (gray255)^2 = c4^2 T / S^2 (decolor255_T_x2), S = r + g + b an integer in
+// [0, 765], so 1 / S^2 is a shared-memory table W[S] (indexed by the bits of
+// the 2^23-biased S, one LEA) instead of the MUFU rsqrt of the linear route:
+// u = T W[S] + 1/8 = (255 v)^2 + 1/8 (one FFMA per pixel), and the toned byte
+// is the number of the curve's thresholds U_j = (255 theta_j)^2 + 1/8 that u
+// reaches, read from log-spaced step words (SHF + LOP3 for the bin address,
+// LDS, IADD; byte 3). Two MUFU per pixel instead of three: the decolor
+// kernel is bound by the MUFU (XU) pipe at 3 per pixel (16 per clock per SM),
+// the tone map's extra lookup work then fits in the issue slots the XU left.
+// Parity: the north-star bar, as the linear route (u carries ~10 u of
+// relative error, half of that in v: only pixels within ~5e-7 relative of a
+// threshold can differ).
+__device__ __forceinline__ uint32_t* sq_step_smem() {
+    __shared__ __align__(16) uint32_t t[kSqBins];
+    return t;
+}
+__device__ __forceinline__ uint32_t* sq_gray_smem() {
+    __shared__ __align__(16) uint32_t t[kSqBins];
+    return t;
+}
+__device__ __forceinline__ float* sq_w_smem() {
+    __shared__ __align__(16) float t[kSqW];
+    return t;
+}
+template <bool kGray>
+struct OpToneSqU8 {
+    static constexpr bool kLdg = true;
+    static constexpr bool kPingPong = !kGray;
+    static constexpr int kPx = 16;
+    const uint8_t* in;
+    uint8_t* toned;
+    uint8_t* gray;
+    U8Consts k;
+    const ToneTable* tab;
+    uint32_t wofs;  // -(0x4B000000 << 2) mod 2^32
+    float w[kSqW];  // W[S] = c4^2 / S^2 (host fp64, rounded once), W[0] = 0
+
+    __device__ __forceinline__ void prologue() const {
+        const uint4* src = reinterpret_cast<const uint4*>(tab->sq_step);
+        uint4* dst = reinterpret_cast<uint4*>(sq_step_smem());
+        for (int i = threadIdx.x; i < kSqBins / 4; i += blockDim.x) dst[i] = src[i];
+        if constexpr (kGray) {
+            const uint4* sg = reinterpret_cast<const uint4*>(tab->sq_gray);
+            uint4* dg = reinterpret_cast<uint4*>(sq_gray_smem());
+            for (int i = threadIdx.x; i < kSqBins / 4; i += blockDim.x) dg[i] = sg[i];
+        }
+        float* ws = sq_w_smem();
+        for (int i = threadIdx.x; i < kSqW; i += blockDim.x) ws[i] = w[i];
+    }
+    // W[S] from the bits of Sb = S + 2^23: shared address (bits << 2) + (W - (0x4B000000 << 2)) = W + 4 S
+    // (mod 2^32: one LEA)
+    // (the bias offset comes in as a kernel parameter, wofs = -(0x4B000000 << 2),
+    // so the compiler folds table address + offset into one uniform register and
+    // keeps a single LEA per pixel instead of LEA + IADD with an immediate)
+    __device__ __forceinline__ uint32_t w_base() const { return smem_addr(sq_w_smem()) + wofs; }
+    __device__ __forceinline__ static float w_at(uint32_t sb, uint32_t wb) {
+        return __uint_as_float(lds_u32((sb << 2) + wb));
+    }
+    // byte offset of u's bin: ((bits >> 15) - (kSqLoBits >> 15)) * 4
+    __device__ __forceinline__ static uint32_t bin_off(uint32_t ub) {
+        return ((ub >> 13) & 0xFFFFCu) - (kSqLoBits >> 13);
+    }
+    __device__ __forceinline__ static uint32_t word(const uint32_t* t, uint32_t off, uint32_t ub) {
+        return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(t) + off) + ub;
+    }
+    __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
+        const uint32_t w[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y,
+                                v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
+        uint32_t tw[4], gw[4];
+        const uint32_t wb = w_base();
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+            uint32_t t[4], q[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = 2 * qd + h;
+                float2 cb[3], ch[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int b0 = 3 * (2 * j) + c, b1 = 3 * (2 * j + 1) + c;
+                    cb[c] = make_float2(byte_biased(w[b0 >> 2], b0 & 3), byte_biased(w[b1 >> 2], b1 & 3));
+                    ch[c] = add2(cb[c], bc2(-kMagic));
+                }
+                float2 T, Sb;
+                decolor255_T_x2(ch[0], ch[1], ch[2], cb[2], k, T, Sb);
+                const float2 W = make_float2(w_at(__float_as_uint(Sb.x), wb), w_at(__float_as_uint(Sb.y), wb));
+                const float2 u = fma2(T, W, bc2(kSqBias));
+                const uint32_t ux = __float_as_uint(u.x), uy = __float_as_uint(u.y);
+                const uint32_t ox = bin_off(ux), oy = bin_off(uy);
+                t[2 * h] = word(sq_step_smem(), ox, ux);
+                t[2 * h + 1] = word(sq_step_smem(), oy, uy);
+                if constexpr (kGray) {
+                    q[2 * h] = word(sq_gray_smem(), ox, ux);
+                    q[2 * h + 1] = word(sq_gray_smem(), oy, uy);
+                }
+            }
+            tw[qd] = __byte_perm(__byte_perm(t[0], t[1], 0x0073u), __byte_perm(t[2], t[3], 0x0073u), 0x5410u);
+            if constexpr (kGray)
+                gw[qd] = __byte_perm(__byte_perm(q[0], q[1], 0x0073u), __byte_perm(q[2], q[3], 0x0073u), 0x5410u);
+        }
+        st_global_cs_v4(toned + px0, make_uint4(tw[0], tw[1], tw[2], tw[3]));
+        if constexpr (kGray) st_global_cs_v4(gray + px0, make_uint4(gw[0], gw[1], gw[2], gw[3]));
+    }
+    __device__ __forceinline__ void scalar(int64_t p) const {
+        float T, S;
+        decolor255_T_x1(static_cast<float>(in[3 * p]), static_cast<float>(in[3 * p + 1]),
+                        static_cast<float>(in[3 * p + 2]), k, T, S);
+        const uint32_t ub = __float_as_uint(__fmaf_rn(T, sq_w_smem()[static_cast<int>(S)], kSqBias));
+        const uint32_t o = bin_off(ub);
+        toned[p] = static_cast<uint8_t>(word(sq_step_smem(), o, ub) >> 24);
+        if constexpr (kGray) gray[p] = static_cast<uint8_t>(word(sq_gray_smem(), o, ub) >> 24);
     }
 };
 
@@ -164,10 +321,40 @@ int host_toned(const HostSig& s, double v) {
     return static_cast<int>(std::floor(o * 255.0 + 0.5));
 }
 
+// step words over sorted float thresholds uf[0..n) for bins of `shift` low
+// bits starting at float bits `lo_bits` (nbins bins); returns true if a bin
+// holds several thresholds
+bool sq_step_words(const float* uf, int n, uint32_t* step, int nbins, uint32_t lo_bits, int shift) {
+    bool multi = false;
+    int below = 0;
+    for (int b = 0; b < nbins; ++b) {
+        const uint32_t first = lo_bits + (static_cast<uint32_t>(b) << shift), next = first + (1u << shift);
+        const auto bits_of = [&](int j) {
+            uint32_t x;
+            std::memcpy(&x, &uf[j], 4);
+            return x;
+        };
+        while (below < n && bits_of(below) < first) ++below;
+        int inside = below;
+        while (inside < n && bits_of(inside) < next) ++inside;
+        uint32_t L = 1u << shift;  // no threshold in the bin: never reached
+        if (inside - below == 1) L = bits_of(below) - first;
+        if (inside - below > 1) multi = true;
+        step[b] = (static_cast<uint32_t>(below) << 24) + (0x1000000u - L) - first;
+    }
+    return multi;
+}
+
+void sq_weights(double c4sq, float* w) {
+    w[0] = 0.0f;  // black: T = 0
+    for (int i = 1; i < kSqW; ++i) w[i] = static_cast<float>(c4sq / (static_cast<double>(i) * i));
+}
+
 void build_tone_table(double m, double k, ToneTable* t) {
     const HostSig s = host_sig(m, k);
     t->multi = 0;
     float xf[255];  // f-domain thresholds
+    float uf[255];  // square-domain thresholds (255 theta)^2 + 1/8
     for (int j = 1; j <= 255; ++j) {
         // least double v in [0, 1] with toned(v) >= j (non-negative doubles order like their bits)
         double v0 = 0.0, v1 = 1.0;
@@ -187,7 +374,12 @@ void build_tone_table(double m, double k, ToneTable* t) {
         double th;
         std::memcpy(&th, &hi, 8);
         xf[j - 1] = static_cast<float>(256.0 + (th * 255.0 + 0.5));  // f = 256 + 255 v + 0.5
+        uf[j - 1] = static_cast<float>((th * 255.0) * (th * 255.0) + 0.125);
     }
+    t->sq_multi = sq_step_words(uf, 255, t->sq_step, kSqBins, kSqLoBits, 15) ? 1 : 0;
+    float gf[255];  // quantize_u8's boundaries: byte j from 255 v = j - 1/2 on
+    for (int j = 1; j <= 255; ++j) gf[j - 1] = static_cast<float>((j - 0.5) * (j - 0.5) + 0.125);
+    sq_step_words(gf, 255, t->sq_gray, kSqBins, kSqLoBits, 15);
     for (int j = 0; j < 256; ++j) t->thr[j] = j < 255 ? xf[j] : INFINITY;
     int below = 0;
     for (int b = 0; b < kToneBins; ++b) {
@@ -205,13 +397,13 @@ void build_tone_table(double m, double k, ToneTable* t) {
         float base;
         std::memcpy(&base, &cnt, 4);
         t->bins[b] = make_float2(base, tin);
-        uint32_t e = cnt << 11;
+        uint32_t L = 0x800u;  // no threshold in the bin: never reached
         if (inside - below == 1) {
             uint32_t tb;
             std::memcpy(&tb, &xf[below], 4);
-            e += 0x800u - (tb & 0x7FFu);  // tb's low bits 0 -> +2048: the whole bin counts it
+            L = tb & 0x7FFu;  // 0: the whole bin counts it
         }
-        t->step[b] = e - (0x43800000u + (static_cast<uint32_t>(b) << 11));  // bits(256 + b/16)
+        t->step[b] = (cnt << 24) + (0x1000000u - L) - (0x43800000u + (static_cast<uint32_t>(b) << 11));  // bits(256 + b/16)
     }
     std::memset(t->edge, 0, sizeof(t->edge));
     for (int j = 0; j < 255; ++j) {
@@ -229,6 +421,7 @@ struct Entry {
     double m = 0, k = 0;
     ToneTable* dev = nullptr;
     bool multi = false;
+    bool sq_multi = false;
 };
 constexpr int kCache = 8;
 Entry g_cache[kMaxDevices][kCache];
@@ -238,7 +431,8 @@ std::mutex g_mu;
 // The table stays valid while *hold is locked: the caller enqueues its kernel
 // before releasing it, so an eviction by another thread (cudaFree, which waits
 // for the device's queued work) cannot free a table a pending launch uses.
-int tone_table(double m, double k, const ToneTable** out, bool* multi, std::unique_lock<std::mutex>* hold) {
+int tone_table(double m, double k, const ToneTable** out, bool* multi, std::unique_lock<std::mutex>* hold,
+               bool* sq_multi = nullptr) {
     int device = 0;
     cudaGetDevice(&device);
     if (device < 0 || device >= kMaxDevices) return set_error(WG_ENODEV, "device ordinal out of range");
@@ -247,6 +441,7 @@ int tone_table(double m, double k, const ToneTable** out, bool* multi, std::uniq
         if (e.used && e.m == m && e.k == k) {
             *out = e.dev;
             *multi = e.multi;
+            if (sq_multi) *sq_multi = e.sq_multi;
             return WG_OK;
         }
     static ToneTable host;  // under g_mu
@@ -261,9 +456,10 @@ int tone_table(double m, double k, const ToneTable** out, bool* multi, std::uniq
     Entry& slot = g_cache[device][g_next[device]];
     g_next[device] = (g_next[device] + 1) % kCache;
     if (slot.used) cudaFree(slot.dev);
-    slot = {true, m, k, d, host.multi != 0};
+    slot = {true, m, k, d, host.multi != 0, host.sq_multi != 0};
     *out = d;
     *multi = host.multi != 0;
+    if (sq_multi) *sq_multi = host.sq_multi != 0;
     return WG_OK;
 }
 
@@ -843,13 +1039,28 @@ extern "C" int wg_decolor_tone_u8(const uint8_t* rgb, uint8_t* toned, uint8_t* g
                   check_curve(midpoint, slope));
     if (npix == 0) return WG_OK;
     const ToneTable* tab = nullptr;
-    bool multi = false;
+    bool multi = false, sq_multi = false;
     std::unique_lock<std::mutex> hold;  // keeps the cached table alive until the launch is enqueued
-    const int rc = tone_table(midpoint, slope, &tab, &multi, &hold);
+    const int rc = tone_table(midpoint, slope, &tab, &multi, &hold, &sq_multi);
     if (rc != WG_OK) return rc;
     const U8Consts k = make_u8_consts(beta_r, beta_k);
     const void* outs[2] = {toned, gray_or_null};
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // square-domain route unless a bin holds several thresholds (steep curves)
+    // or WG_TONE_ROUTE=linear (A/B tests of the linear step words)
+    const char* route = std::getenv("WG_TONE_ROUTE");
+    if (!sq_multi && !(route && std::strcmp(route, "linear") == 0) && !std::getenv("WG_TONE_BINS64")) {
+        const double c4sq = static_cast<double>(beta_k) / 3.0;
+        if (gray_or_null)
+        if (gray_or_null) {
+            OpToneSqU8<true> op{rgb, toned, gray_or_null, k, tab, 0u - (0x4B000000u << 2), {}};
+            sq_weights(c4sq, op.w);
+            return launch_stream(op, rgb, outs, 2, npix, st);
+        }
+        OpToneSqU8<false> op{rgb, toned, nullptr, k, tab, 0u - (0x4B000000u << 2), {}};
+        sq_weights(c4sq, op.w);
+        return launch_stream(op, rgb, outs, 2, npix, st);
+    }
     // WG_TONE_BINS64=1: the 8-byte-bin variant for every curve (A/B tests of the step words)
     if (multi || std::getenv("WG_TONE_BINS64")) {
         if (gray_or_null)

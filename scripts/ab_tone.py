@@ -1,0 +1,80 @@
+"""A/B of the global tone map uint8 kernel variants against the decolor kernel
+on the C3 batch (256 Voronoi 4K frames, device-generated), CUDA events.
+
+    python scripts/ab_tone.py [--images 256] [--iters 20] [--rounds 3]
+        [--configs "ROUTE=linear;GRID=20"]
+
+Each config sets WG_TONE_ROUTE / WG_LDG_GRID_PER_SM for the library calls;
+rounds interleave decolor and every config, the median is printed.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2108_13656_b200 as wg  # noqa: E402
+from paper_2108_13656_b200 import synth  # noqa: E402
+
+KEYS = {"GRID": "WG_LDG_GRID_PER_SM", "ROUTE": "WG_TONE_ROUTE"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--images", type=int, default=256)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--workload", default="C3")
+    ap.add_argument("--configs", default="ROUTE=linear")
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    wl = synth.WORKLOADS[args.workload]
+    rgb = synth.make_batch(wl, dev, n_images=args.images)
+    out = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=dev)
+    tone_ref = wg.decolor_tone(rgb)
+    npx = out.numel()
+    configs = [dict(kv.split("=") for kv in c.split(",") if kv) for c in args.configs.split(";")]
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return npx / (e0.elapsed_time(e1) / args.iters) / 1e6
+
+    def setenv(cfg):
+        for k, v in KEYS.items():
+            os.environ.pop(v, None)
+        for k, v in cfg.items():
+            os.environ[KEYS[k]] = v
+
+    res = {"decolor": []}
+    for r in range(args.rounds):
+        setenv({})
+        res["decolor"].append(timed(lambda: wg.decolor(rgb, out=out)))
+        for cfg in configs:
+            setenv(cfg)
+            name = ",".join(f"{k}={v}" for k, v in cfg.items()) or "default"
+            res.setdefault(name, []).append(timed(lambda: wg.decolor_tone(rgb, out=out)))
+            if r == 0:
+                diff = (out.view(-1).int() - tone_ref.view(-1).int()).abs()
+                print(json.dumps({"config": name, "vs_default_max": int(diff.max()),
+                                  "vs_default_frac": float((diff > 0).float().mean())}))
+    setenv({})
+    base = statistics.median(res["decolor"])
+    for name, v in res.items():
+        m = statistics.median(v)
+        print(json.dumps({"kernel": name, "gpix_s": round(m, 1), "vs_decolor": round(m / base, 3),
+                          "frac_4Bpx": round(m * 4 / 6545.3, 3), "all": [round(x, 1) for x in v]}))
+
+
+if __name__ == "__main__":
+    main()

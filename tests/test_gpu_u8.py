@@ -244,13 +244,14 @@ def test_tone_u8_cube(torch_dev, cube):
 
 
 def test_tone_u8_step_words_equal_bins(torch_dev, cube, monkeypatch):
-    """The single-threshold curves' 32-bit step words ((step + bits) >> 11) give
-    the same bytes as the 8-byte bins (count + float compare), over all 2^24
+    """The linear route's 32-bit step words (byte 3 of step + bits) give the
+    same bytes as its 8-byte bins (count + float compare), over all 2^24
     colours, toned-only and with gray."""
     import paper_2108_13656_b200 as wg
 
     torch, dev = torch_dev
     t = torch.from_numpy(cube).to(dev)
+    monkeypatch.setenv("WG_TONE_ROUTE", "linear")
     for m, k in [(0.5, 8.0), (0.3, 12.0), (0.5, 1e-6), (0.0, 3.0), (1.0, 3.0), (0.45, 60.0)]:
         curve = wg.SigmoidCurve(m, k)
         a = wg.decolor_tone(t, curve)
@@ -261,6 +262,29 @@ def test_tone_u8_step_words_equal_bins(torch_dev, cube, monkeypatch):
         monkeypatch.delenv("WG_TONE_BINS64")
         assert torch.equal(a, b) and torch.equal(ta, tb) and torch.equal(ga, gb), (m, k)
         assert torch.equal(a, ta)
+
+
+def test_tone_u8_routes_vs_oracle(torch_dev, cube, monkeypatch):
+    """Both uint8 tone routes -- the square-domain step words (default: no
+    final root, 1/S^2 from a table) and the linear step words -- meet the bar
+    against the oracle over all 2^24 colours, toned and gray."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+
+    torch, dev = torch_dev
+    t = torch.from_numpy(cube).to(dev)
+    for m, k in [(0.5, 8.0), (0.3, 12.0), (0.5, 1e-6), (0.0, 3.0), (1.0, 3.0), (0.45, 60.0)]:
+        want_t, want_g = oracle.tone_u8(cube, midpoint=m, slope=k, threads=oracle.default_threads(),
+                                        with_gray=True)
+        for route in ("square", "linear"):
+            if route == "linear":
+                monkeypatch.setenv("WG_TONE_ROUTE", "linear")
+            toned, gray, _ = wg.decolor_tone(t, wg.SigmoidCurve(m, k), return_gray=True)
+            monkeypatch.delenv("WG_TONE_ROUTE", raising=False)
+            for name, got, want in (("toned", toned, want_t), ("gray", gray, want_g)):
+                mx, frac = u8_mismatch(got.cpu().numpy(), want)
+                print(f"tone route {route} m={m} k={k} {name}: max {mx} frac {frac:.3e}")
+                assert mx <= 1 and frac <= U8_MAX_FRAC, (route, m, k, name)
 
 
 def test_tone_rgb_u8_golden_and_cube(torch_dev, cube):
