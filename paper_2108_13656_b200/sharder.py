@@ -41,10 +41,11 @@ def shard_sizes(n_items: int, world_size: int) -> list[int]:
 def gather_to_root(local, n_items: int, group=None, root: int = 0):
     """Assemble every rank's shard (leading axis = items) on ``root``.
 
-    Shards are padded to the largest shard size and exchanged with one
-    ``all_gather_into_tensor`` (NCCL over NVLink on GPUs, gloo on CPU); the
-    root trims the padding and concatenates in rank order. Returns the full
-    batch on ``root`` and ``None`` elsewhere.
+    Shards are padded to the largest shard size and sent to ``root`` with one
+    ``gather`` (NCCL send/recv over NVLink on GPUs: only the root receives and
+    holds the whole batch; gloo on CPU falls back to an all-gather); the root
+    trims the padding and concatenates in rank order. Returns the full batch
+    on ``root`` and ``None`` elsewhere.
     """
     import torch
     import torch.distributed as dist
@@ -58,12 +59,14 @@ def gather_to_root(local, n_items: int, group=None, root: int = 0):
     padded = torch.zeros((cap, *local.shape[1:]), dtype=local.dtype, device=local.device)
     if local.shape[0]:
         padded[: local.shape[0]] = local
-    full = torch.empty((world * cap, *local.shape[1:]), dtype=local.dtype, device=local.device)
-    if dist.get_backend(group) == "gloo" or not hasattr(dist, "all_gather_into_tensor"):
+    if dist.get_backend(group) == "gloo":
+        full = torch.empty((world * cap, *local.shape[1:]), dtype=local.dtype, device=local.device)
         parts = list(full.chunk(world)) if world else []
         dist.all_gather(parts, padded, group=group)
     else:
-        dist.all_gather_into_tensor(full, padded, group=group)
+        full = torch.empty((world * cap, *local.shape[1:]), dtype=local.dtype, device=local.device) \
+            if rank == root else None
+        dist.gather(padded, list(full.chunk(world)) if full is not None else None, dst=root, group=group)
     if rank != root:
         return None
     pieces = [full[r * cap: r * cap + sizes[r]] for r in range(world)]

@@ -91,3 +91,25 @@ def test_c5_shard_edges():
         if k == 0:
             np.testing.assert_array_equal(wg.decolor(rgb, exact=True).cpu().numpy(), want)
     assert bad <= U8_MAX_FRAC * total
+
+
+def test_run_on_devices_every_visible_gpu():
+    """sharder.run_on_devices (one process, one host thread per device) over every
+    visible GPU gives the bytes of the single-device call and meets the bar
+    against the oracle; with one GPU the shards all land on device 0 (the
+    multi-device fan-out is then exercised with repeated ordinals)."""
+    import torch
+
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+    from paper_2108_13656_b200 import sharder
+
+    ndev = torch.cuda.device_count()
+    batch = oracle.synth_uniform_u8(6, 64, 96, seed=3)
+    whole = wg.decolor_host(batch, device=0)
+    for devices in (list(range(ndev)), [0] * 3, list(range(ndev)) * 2):
+        got = sharder.run_on_devices(lambda shard, d: wg.decolor_host(shard, device=d), batch, devices)
+        assert np.array_equal(got, whole), devices
+    mx, frac = u8_mismatch(whole, oracle.decolor_u8(batch))
+    assert mx <= 1 and frac <= U8_MAX_FRAC
+    print(f"run_on_devices over {ndev} visible GPU(s): identical to the single-device call")
