@@ -50,7 +50,7 @@ extern "C" {
 
 #define WG_OK 0
 #define WG_EINVAL (-1)      /* bad argument (size, parameter range, null pointer) */
-#define WG_EALIGN (-2)      /* reserved: misaligned buffer where alignment is mandatory */
+#define WG_EALIGN (-2)      /* misaligned buffer where alignment is mandatory (hdr out / scratch) */
 #define WG_ESCRATCH (-3)    /* scratch buffer too small */
 #define WG_ENODEV (-4)      /* no CUDA device / bad ordinal */
 #define WG_ECODEC (-5)      /* unsupported or malformed image file (reference: CodecError) */
@@ -140,7 +140,11 @@ WG_API int wg_dequantize_u8_f64(const uint8_t* in, double* out, int64_t n, void*
 /* HDR adapter (no reference counterpart):
  * nimg fp32 linear-radiance images of pix_per_img pixels -> uint8 via
  * per-image log-range normalisation of the gray channel, then the global
- * sigmoid. Two passes with an atomics-free per-block min/max statistic. */
+ * sigmoid. Exact per-CTA min/max partials (no atomics on the statistic); one
+ * warp-specialised persistent kernel (cooperative launch) when pix_per_img is
+ * a multiple of 32, else gray / stats / tone kernels. `out` must be 16-byte
+ * aligned (WG_EALIGN), `scratch` 256-byte aligned and at least
+ * wg_hdr_scratch_bytes() long (WG_ESCRATCH). */
 WG_API size_t wg_hdr_scratch_bytes(int64_t nimg, int64_t pix_per_img);
 WG_API int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
                       float beta_r, float beta_k, float midpoint, float slope, void* scratch,

@@ -242,6 +242,8 @@ def hdr_tonemap(rgb, params: DecolorParams = DEFAULT_PARAMS, curve: SigmoidCurve
     ppi = rgb[0].numel() // 3 if n else 0
     if out is None:
         out = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=rgb.device)
+    else:
+        _check_out(out, rgb.shape[:-1], rgb, dtype=torch.uint8)
     need = int(_lib.load().wg_hdr_scratch_bytes(n, ppi))
     if scratch is None or scratch.nbytes < need:
         scratch = HdrScratch(n, ppi, device=rgb.device)

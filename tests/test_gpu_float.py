@@ -271,22 +271,70 @@ def test_hdr_c4_images(torch_dev):
 
 
 def test_hdr_schedules_agree(torch_dev, monkeypatch):
-    """The opt-in schedules equal the default bit for bit: the bulk-copy tone ring
-    (WG_HDR_TILED; it once raced: LDS in flight vs TMA refill) and the fused
-    persistent kernel (WG_HDR_FUSED)."""
+    """Every schedule gives the same bytes: the warp-specialised persistent kernel
+    (default), the grouped three-kernel schedule (WG_HDR_SCHEDULE=grouped) and
+    its bulk-copy tone ring (WG_HDR_TILED; it once raced: LDS in flight vs TMA
+    refill). 7 images > the persistent kernel's ring slots, so slots are
+    reused; repeated calls reuse the scratch."""
     import paper_2108_13656_b200 as wg
     from paper_2108_13656_b200 import synth
 
     torch, dev = torch_dev
-    rgb = torch.empty((3, 1024, 2048, 3), dtype=torch.float32, device=dev)
+    rgb = torch.empty((7, 1024, 2048, 3), dtype=torch.float32, device=dev)
     synth.fill_hdr_f32(rgb, seed=9)
+    rgb[3] = 0.0  # all-black image
+    rgb[5] = 0.25  # constant image (gmax == gmin)
     plain = wg.hdr_tonemap(rgb)
+    scratch = wg.HdrScratch(7, 1024 * 2048)
+    for _ in range(3):
+        assert torch.equal(wg.hdr_tonemap(rgb, scratch=scratch), plain)
+    monkeypatch.setenv("WG_HDR_SCHEDULE", "grouped")
+    assert torch.equal(wg.hdr_tonemap(rgb), plain)
     monkeypatch.setenv("WG_HDR_TILED", "1")
     for _ in range(3):
         assert torch.equal(wg.hdr_tonemap(rgb), plain)
-    monkeypatch.delenv("WG_HDR_TILED")
-    monkeypatch.setenv("WG_HDR_FUSED", "1")
-    assert torch.equal(wg.hdr_tonemap(rgb), plain)
+    assert int(plain[3].max()) == 0 and bool((plain[5] == 255).all())
+
+
+@pytest.mark.parametrize("shape", [(5, 16, 17), (6, 64, 96), (3, 1, 32), (9, 48, 40), (2, 1, 1)])
+def test_hdr_multi_image_shapes_vs_oracle(torch_dev, shape, monkeypatch):
+    """Small multi-image batches against the oracle, both schedules: 16x17 (272 px,
+    plane offsets of 64 B mod 128: the grouped tone pass must not discard a
+    line the neighbouring image still needs), 64x96 / 1x32 / 48x40 (the
+    persistent kernel's 32-px lines; more CTAs than lines), 1x1."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+    from paper_2108_13656_b200 import synth
+
+    torch, dev = torch_dev
+    rgb = torch.empty((*shape, 3), dtype=torch.float32, device=dev)
+    synth.fill_hdr_f32(rgb, seed=31)
+    want = oracle.hdr_u8(rgb.cpu().numpy(), threads=4)
+    for sched in ("default", "grouped"):
+        if sched == "grouped":
+            monkeypatch.setenv("WG_HDR_SCHEDULE", "grouped")
+        for _ in range(2):
+            got = wg.hdr_tonemap(rgb).cpu().numpy()
+            mx, frac = u8_mismatch(got, want)
+            assert mx <= 1 and frac <= 2e-3, (sched, shape, mx, frac)
+
+
+def test_hdr_out_validated(torch_dev):
+    import paper_2108_13656_b200 as wg
+
+    torch, dev = torch_dev
+    rgb = torch.rand((2, 64, 64, 3), dtype=torch.float32, device=dev)
+    ok = torch.empty((2, 64, 64), dtype=torch.uint8, device=dev)
+    assert wg.hdr_tonemap(rgb, out=ok) is ok
+    for bad in (torch.empty((2, 64, 63), dtype=torch.uint8, device=dev),
+                torch.empty((2, 64, 64), dtype=torch.float32, device=dev),
+                torch.empty((2, 64, 128), dtype=torch.uint8, device=dev)[:, :, ::2]):
+        with pytest.raises(ValueError):
+            wg.hdr_tonemap(rgb, out=bad)
+    # contiguous but not 16-byte aligned: the C ABI refuses it (WG_EALIGN -> ValueError)
+    buf = torch.empty(2 * 64 * 64 + 16, dtype=torch.uint8, device=dev)
+    with pytest.raises(ValueError):
+        wg.hdr_tonemap(rgb, out=buf[1:1 + 2 * 64 * 64].view(2, 64, 64))
 
 
 def test_hdr_shard_invariance(torch_dev):
