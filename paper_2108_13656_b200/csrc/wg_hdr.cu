@@ -501,10 +501,8 @@ __global__ void __launch_bounds__(kT) hdr_tone_kernel(const float* __restrict__ 
 // in + 1 B/px out (the gray plane stays in L2). Same per-pixel gray, min/max
 // and table arithmetic as the grouped schedule: identical bytes.
 constexpr int kWsT = 1024;   // one CTA per SM
-constexpr int kWsProd = 24;  // producers: the gray pass is bound by the loads in flight per SM
-constexpr int kWsCons = 8;   // consumers: table build + tone from L2 (latency-bound)
-constexpr int kWsProdT = kWsProd * 32;
-constexpr int kWsConsT = kWsCons * 32;
+// warps: kWsT / 32 - kCons producers (the gray pass is bound by the loads in
+// flight per SM), kCons consumers (table build + tone from L2, latency-bound)
 constexpr int kWsLinePx = 32;    // partition unit: one 128 B gray line
 constexpr int kWsMaxGrid = 1024;  // partial slots per image
 constexpr int kWsMaxRing = 4;
@@ -577,7 +575,7 @@ struct WsMap {
 // consumer tone of a CTA's chunks: 16-px chunks, chunk pairs (one 128 B gray
 // line) on lanes (2l, 2l + 1) of one warp, the line dropped from L2 once both
 // are read
-template <int kU, class Px>
+template <int kU, int kConsT, class Px>
 __device__ __forceinline__ void ws_tone_range(const float* __restrict__ gsl, uint8_t* __restrict__ o,
                                               const WsMap& mp, int ct, Px px) {
     // warp-uniform trip count (the __syncwarp below needs every lane); lanes past
@@ -586,18 +584,18 @@ __device__ __forceinline__ void ws_tone_range(const float* __restrict__ gsl, uin
     // before any use (L2 latency, not bandwidth, bounds these few warps).
     const int lane = ct & 31;
     const int64_t nch = mp.nchunks();
-    for (int64_t base = ct - lane; base < nch; base += kU * kWsConsT) {
+    for (int64_t base = ct - lane; base < nch; base += kU * kConsT) {
         float4 x[kU][4];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {  // unconditional loads (clamped index): no maybe-unset registers
-            const int64_t ch = mp.chunk(min(base + lane + u * kWsConsT, nch - 1));
+            const int64_t ch = mp.chunk(min(base + lane + u * kConsT, nch - 1));
             const float4* src = reinterpret_cast<const float4*>(gsl + (ch << 4));
 #pragma unroll
             for (int j = 0; j < 4; ++j) x[u][j] = __ldcg(src + j);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const int64_t v = base + lane + u * kWsConsT;
+            const int64_t v = base + lane + u * kConsT;
             if (v < nch) {
                 const int64_t ch = mp.chunk(v);
                 uint32_t w[4];
@@ -610,20 +608,22 @@ __device__ __forceinline__ void ws_tone_range(const float* __restrict__ gsl, uin
         __syncwarp();  // both chunks of each line are read (their values are used above)
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const int64_t v = base + lane + u * kWsConsT;
+            const int64_t v = base + lane + u * kConsT;
             if (v < nch && (lane & 1) == 0) discard_l2_line(gsl + (mp.chunk(v) << 4));
         }
     }
 }
 
+template <int kCons_>
 __global__ void __launch_bounds__(kWsT, 1)
     hdr_ws_kernel(const float* __restrict__ rgb, uint8_t* __restrict__ out, float* __restrict__ ring,
                   float2* __restrict__ parts, unsigned* __restrict__ counts, int64_t nimg, int64_t ppi, int nring,
                   U8Consts k, float m, float slope, Theta theta) {
+    constexpr int kProd_ = kWsT / 32 - kCons_, kProdT_ = kProd_ * 32, kConsT_ = kCons_ * 32;
     __shared__ uint32_t s_lut[kLutBins];
     __shared__ int s_cnt[kLutBins];
-    __shared__ float s_plo[kWsProd], s_phi[kWsProd], s_clo[kWsCons], s_chi[kWsCons];
-    __shared__ int s_wsum[kWsCons];
+    __shared__ float s_plo[kProd_], s_phi[kProd_], s_clo[kCons_], s_chi[kCons_];
+    __shared__ int s_wsum[kCons_];
     __shared__ int s_conflict;
     __shared__ volatile int s_toned;  // images this CTA's consumers have finished
     float* s_thr = reinterpret_cast<float*>(s_lut);  // thresholds, then the entries in place
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kWsT, 1)
     if (tid == 0) s_toned = 0;
     __syncthreads();
 
-    if (warp < kWsProd) {
+    if (warp < kProd_) {
         // ---------------- producers: three 128-bit loads per quad, the next quad in flight
         const uint64_t pol_gray = l2_policy_evict_last();
         const int64_t nq = mp.nquads();  // this CTA's quads (4 px) of every image
@@ -656,11 +656,11 @@ __global__ void __launch_bounds__(kWsT, 1)
                 n1 = __ldcs(src + 1);
                 n2 = __ldcs(src + 2);
             }
-            for (; u < nq; u += kWsProdT) {
+            for (; u < nq; u += kProdT_) {
                 const int64_t q = mp.quad(u);
                 const float4 v0 = n0, v1 = n1, v2 = n2;
-                if (u + kWsProdT < nq) {
-                    const float4* src = reinterpret_cast<const float4*>(in + 12 * mp.quad(u + kWsProdT));
+                if (u + kProdT_ < nq) {
+                    const float4* src = reinterpret_cast<const float4*>(in + 12 * mp.quad(u + kProdT_));
                     n0 = __ldcs(src);
                     n1 = __ldcs(src + 1);
                     n2 = __ldcs(src + 2);
@@ -681,9 +681,9 @@ __global__ void __launch_bounds__(kWsT, 1)
                 s_phi[warp] = hi;
             }
             __threadfence();  // this thread's gray stores before the image's completion count
-            named_bar(1, kWsProdT);
+            named_bar(1, kProdT_);
             if (tid == 0) {
-                for (int w = 0; w < kWsProd; ++w) {
+                for (int w = 0; w < kProd_; ++w) {
                     lo = fminf(lo, s_plo[w]);
                     hi = fmaxf(hi, s_phi[w]);
                 }
@@ -691,19 +691,19 @@ __global__ void __launch_bounds__(kWsT, 1)
                 __threadfence();
                 atomicAdd(counts + i, 1u);
             }
-            named_bar(1, kWsProdT);  // s_plo / s_phi are rewritten for the next image
+            named_bar(1, kProdT_);  // s_plo / s_phi are rewritten for the next image
         }
         return;
     }
 
     // ---------------- consumers
-    const int ct = tid - kWsProdT, cw = ct >> 5;
+    const int ct = tid - kProdT_, cw = ct >> 5;
     const ToneU8 tc = make_tone_u8(m, slope);
     for (int64_t i = 0; i < nimg; ++i) {
         if (ct == 0) wait_geq(counts + i, static_cast<unsigned>(G));
-        named_bar(2, kWsConsT);
+        named_bar(2, kConsT_);
         float lo = INFINITY, hi = 0.0f;
-        for (int q = ct; q < G; q += kWsConsT) {
+        for (int q = ct; q < G; q += kConsT_) {
             const float2 pr = __ldcg(parts + i * kWsMaxGrid + q);
             lo = fminf(lo, pr.x);
             hi = fmaxf(hi, pr.y);
@@ -713,32 +713,33 @@ __global__ void __launch_bounds__(kWsT, 1)
             s_clo[cw] = lo;
             s_chi[cw] = hi;
         }
-        for (int b = ct; b < kLutBins; b += kWsConsT) {
+        for (int b = ct; b < kLutBins; b += kConsT_) {
             s_cnt[b] = 0;
             s_thr[b] = INFINITY;
         }
         if (ct == 0) s_conflict = 0;
-        named_bar(2, kWsConsT);
+        named_bar(2, kConsT_);
         lo = s_clo[0];
         hi = s_chi[0];
-        for (int w = 1; w < kWsCons; ++w) {
+        for (int w = 1; w < kCons_; ++w) {
             lo = fminf(lo, s_clo[w]);
             hi = fmaxf(hi, s_chi[w]);
         }
         double lr;
         HdrStat st = hdr_stat_of(lo, hi, &lr);
         if (st.mode == 1 && lr < kLutOct - 1) {  // uniform over the consumer warps
-            for (int j = ct; j < 255; j += kWsConsT) {
+            for (int j = ct; j < 255; j += kConsT_) {
                 const float gam = static_cast<float>(exp2(theta.v[j] * lr));  // > 1 since theta > 0
                 const int b = lut_bin(gam);
                 if (atomicAdd(&s_cnt[b], 1) != 0) s_conflict = 1;  // shared counter: table layout only
                 s_thr[b] = gam;
             }
-            named_bar(2, kWsConsT);
+            named_bar(2, kConsT_);
             // exclusive scan of s_cnt: 16 consecutive bins per thread
-            constexpr int kPer = kLutBins / kWsConsT;
+            constexpr int kPer = (kLutBins + kConsT_ - 1) / kConsT_;  // bins per thread (the last thread may have fewer)
+            const int b0 = min(ct * kPer, kLutBins), b1 = min(b0 + kPer, kLutBins);
             int sum = 0;
-            for (int j = 0; j < kPer; ++j) sum += s_cnt[ct * kPer + j];
+            for (int b = b0; b < b1; ++b) sum += s_cnt[b];
             int incl = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -746,28 +747,28 @@ __global__ void __launch_bounds__(kWsT, 1)
                 if (lane >= o) incl += v;
             }
             if (lane == 31) s_wsum[cw] = incl;
-            named_bar(2, kWsConsT);
+            named_bar(2, kConsT_);
             int off = incl - sum;
             for (int w = 0; w < cw; ++w) off += s_wsum[w];
-            for (int j = 0; j < kPer; ++j) {  // second pass: running prefix (no per-thread array)
-                s_lut[ct * kPer + j] = lut_entry(off, s_thr[ct * kPer + j]);
-                off += s_cnt[ct * kPer + j];
+            for (int b = b0; b < b1; ++b) {  // second pass: running prefix (no per-thread array)
+                s_lut[b] = lut_entry(off, s_thr[b]);
+                off += s_cnt[b];
             }
             st.lut = s_conflict ? 0 : 1;
-            named_bar(2, kWsConsT);
+            named_bar(2, kConsT_);
         }
         // tone this CTA's lines (per-image mode hoisted out of the pixel loop)
         const float* gsl = ring + (i % nring) * ppi;
         uint8_t* o = out + i * ppi;
         if (st.mode == 1 && st.lut) {
             const float inv = st.inv_gmin;
-            ws_tone_range<2>(gsl, o, mp, ct, [&](float v) -> uint32_t { return lut_px32(v, inv, s_lut); });
+            ws_tone_range<2, kConsT_>(gsl, o, mp, ct, [&](float v) -> uint32_t { return lut_px32(v, inv, s_lut); });
         } else if (st.mode == 2) {
-            ws_tone_range<2>(gsl, o, mp, ct, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });
+            ws_tone_range<2, kConsT_>(gsl, o, mp, ct, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });
         } else {
-            ws_tone_range<2>(gsl, o, mp, ct, [&](float v) -> uint32_t { return tone_arith_call(v, st, tc); });
+            ws_tone_range<2, kConsT_>(gsl, o, mp, ct, [&](float v) -> uint32_t { return tone_arith_call(v, st, tc); });
         }
-        named_bar(2, kWsConsT);  // every consumer is done with the slot and with s_lut
+        named_bar(2, kConsT_);  // every consumer is done with the slot and with s_lut
         if (ct == 0) s_toned = static_cast<int>(i + 1);
     }
 }
@@ -904,9 +905,10 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
     // its CTAs wait on each other's partials, so all must be co-resident)
     const bool ws_ok = (pix_per_img % kWsLinePx) == 0 && (reinterpret_cast<uintptr_t>(rgb) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(out) & 15) == 0 && device >= 0 && device < kMaxDevices;
+    // 8 consumer warps of 32 (C4: 4 -> 274, 12 -> 261, 16 -> 270 vs 308 Gpix/s)
     static std::atomic<int> ws_occ[1][kMaxDevices];  // idempotent lazy cache
     const int var = 0;
-    const auto ws_kern = hdr_ws_kernel;
+    const auto ws_kern = hdr_ws_kernel<8>;
     if (ws_ok && ws_enabled()) {
         if (!ws_occ[var][device]) {
             int coop = 0, occ = 0;
