@@ -154,12 +154,6 @@ __device__ __forceinline__ uint32_t tone_arith(float g, const HdrStat& st, const
     const float v = fminf(fmaxf(__fmul_rn(__fadd_rn(tanhf(__fmul_rn(c.hk, __fsub_rn(t, c.m))), c.t0), c.inv_den), 0.0f), 1.0f);
     return __float_as_uint(__fadd_rz(__fmaf_rn(v, 255.0f, 0.5f), kMagic)) & 0xFFu;
 }
-__device__ __forceinline__ uint32_t tone_lut(float g, float inv_gmin, const float2* s_lut) {
-    const float r = __fmul_rn(g, inv_gmin);
-    const float2 e = s_lut[lut_bin(r)];
-    const uint32_t u = static_cast<uint32_t>(__float_as_int(e.y)) + (r >= e.x ? 1u : 0u);
-    return g > 0.0f ? u : 0u;
-}
 
 // ---------------------------------------------------------------- pass 1: gray + per-warp (min, max)
 __global__ void __launch_bounds__(kT) hdr_gray_kernel(const float* __restrict__ rgb, float* __restrict__ gray,

@@ -216,11 +216,23 @@ struct OpToneF32 {
 };
 
 // ------------------------------------------------------------------ elementwise fp64 kernels
+// Two pixels per thread per iteration (p and p + stride: independent dependency
+// chains of IEEE divisions and roots the scheduler interleaves), so an image of
+// up to two grids' worth of pixels finishes in one chain latency instead of
+// two waves (800x600: 9.6 -> ~5 us).
 __global__ void decolor_f64_kernel(const double* __restrict__ rgb, double* __restrict__ out,
                                    int64_t npix, double br, double bk) {
-    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npix;
-         p += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[p] = decolor_f64(rgb[3 * p], rgb[3 * p + 1], rgb[3 * p + 2], br, bk);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; p < npix; p += 2 * stride) {
+        const int64_t q = p + stride;
+        const bool two = q < npix;
+        const double r0 = rgb[3 * p], g0 = rgb[3 * p + 1], b0 = rgb[3 * p + 2];
+        const double r1 = two ? rgb[3 * q] : 0.0, g1 = two ? rgb[3 * q + 1] : 0.0, b1 = two ? rgb[3 * q + 2] : 0.0;
+        const double v0 = decolor_f64(r0, g0, b0, br, bk);
+        const double v1 = decolor_f64(r1, g1, b1, br, bk);
+        out[p] = v0;
+        if (two) out[q] = v1;
+    }
 }
 
 __global__ void sigmoid_f64_kernel(const double* __restrict__ in, double* __restrict__ out,

@@ -40,6 +40,7 @@ namespace wg {
 namespace {
 
 constexpr int kToneBins = 4096;  // bins of x = 255 v + 0.5 over [0, 256), width 1/16
+constexpr float kBinAdd = 130816.0f;  // 2^17 - 256: fl_rm(f + kBinAdd) = 2^17 + floor(64 x) / 64
 constexpr int kSqBins = 19 * 256;          // square-domain bins: 19 octaves [2^-3, 2^16), 256 per octave
 constexpr uint32_t kSqLoBits = 0x3E000000u;  // bits of 2^-3, the first square-domain bin
 constexpr float kSqBias = 0.125f;            // u = (255 v)^2 + 2^-3 >= 2^-3 for every pixel (black too)
@@ -118,7 +119,6 @@ struct OpToneU8 {
     // f - 256 = x is exact and the ulp of g is 2^-6), so gbits & 0x3FFC =
     // 4 floor(16 x) is the byte offset of f's bin (bits(f) >> 11) & 4095 --
     // one FADD2.RM per pixel pair and a LOP3 instead of a shift and a mask
-    static constexpr float kBinAdd = 130816.0f;  // 2^17 - 256
     __device__ __forceinline__ uint32_t step_word(uint32_t gbits, uint32_t bits) const {
         const uint32_t e =
             *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(step_smem()) + (gbits & 0x3FFCu));
