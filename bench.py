@@ -167,8 +167,8 @@ def op_spec(wl, op: str) -> dict:
         return {"kernel": "ldg_stream_kernel<OpDecolorF32>", "bytes_per_px": 16, "launches": 1,
                 "api": "decolor (wg_decolor_f32)", "e2e_api": "decolor_host -> wg_host_decolor_f32",
                 "io": "float32->gray float32"}
-    return {"kernel": "hdr_gray_kernel + hdr_stats_kernel + hdr_tone_kernel", "bytes_per_px": wl.bytes_per_px,
-            "launches": 3, "api": "hdr_tonemap (wg_hdr_tonemap_u8)",
+    return {"kernel": "hdr_ws_kernel", "bytes_per_px": wl.bytes_per_px,
+            "launches": 1, "api": "hdr_tonemap (wg_hdr_tonemap_u8)",
             "e2e_api": "hdr_tonemap_host -> wg_host_hdr_tonemap_u8", "io": "float32 radiance->uint8 (HDR adapter)"}
 
 
@@ -463,10 +463,7 @@ def main():
             return lambda: wg.decolor_tone(rgb, out=out)
         return lambda: wg.decolor(rgb, out=out)
 
-    launches_per_step = spec["launches"]
-    if wl.output == "hdr_u8":
-        # wg_hdr.cu: gray + stats + tone per group of images
-        launches_per_step = 3 * (-(-n_img // max(1, min(32, n_img))))
+    launches_per_step = spec["launches"]  # hdr: one persistent kernel (+ a memset of its completion counts)
     in_bytes = rgb.numel() * rgb.element_size()
     flush = None
     if in_bytes < 4 * L2_BYTES:  # small batches: flush L2 between timed steps
