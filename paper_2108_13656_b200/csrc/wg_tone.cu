@@ -34,6 +34,7 @@
 #include "../../include/warmgray_b200.h"
 #include "wg_device.cuh"
 #include "wg_internal.h"
+#include "wg_square.cuh"
 #include "wg_stream.cuh"
 
 namespace wg {
@@ -41,10 +42,7 @@ namespace {
 
 constexpr int kToneBins = 4096;  // bins of x = 255 v + 0.5 over [0, 256), width 1/16
 constexpr float kBinAdd = 130816.0f;  // 2^17 - 256: fl_rm(f + kBinAdd) = 2^17 + floor(64 x) / 64
-constexpr int kSqBins = 19 * 256;          // square-domain bins: 19 octaves [2^-3, 2^16), 256 per octave
-constexpr uint32_t kSqLoBits = 0x3E000000u;  // bits of 2^-3, the first square-domain bin
-constexpr float kSqBias = 0.125f;            // u = (255 v)^2 + 2^-3 >= 2^-3 for every pixel (black too)
-constexpr int kSqW = 768;                    // W[S] = c4^2 / S^2 for S = r + g + b in [0, 765]
+
 
 struct ToneTable {
     float2 bins[kToneBins];  // {count of thresholds below the bin (as bits), f-domain threshold inside or NaN}
@@ -250,12 +248,9 @@ struct OpToneSqU8 {
     __device__ __forceinline__ static float w_at(uint32_t sb, uint32_t wb) {
         return __uint_as_float(lds_u32((sb << 2) + wb));
     }
-    // byte offset of u's bin: ((bits >> 15) - (kSqLoBits >> 15)) * 4
-    __device__ __forceinline__ static uint32_t bin_off(uint32_t ub) {
-        return ((ub >> 13) & 0xFFFFCu) - (kSqLoBits >> 13);
-    }
+    __device__ __forceinline__ static uint32_t bin_off(uint32_t ub) { return sq_bin_off(ub); }
     __device__ __forceinline__ static uint32_t word(const uint32_t* t, uint32_t off, uint32_t ub) {
-        return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(t) + off) + ub;
+        return sq_word(t, off, ub);
     }
     __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
         const uint32_t w[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y,
@@ -321,6 +316,8 @@ int host_toned(const HostSig& s, double v) {
     return static_cast<int>(std::floor(o * 255.0 + 0.5));
 }
 
+}  // namespace
+
 // step words over sorted float thresholds uf[0..n) for bins of `shift` low
 // bits starting at float bits `lo_bits` (nbins bins); returns true if a bin
 // holds several thresholds
@@ -349,6 +346,8 @@ void sq_weights(double c4sq, float* w) {
     w[0] = 0.0f;  // black: T = 0
     for (int i = 1; i < kSqW; ++i) w[i] = static_cast<float>(c4sq / (static_cast<double>(i) * i));
 }
+
+namespace {
 
 void build_tone_table(double m, double k, ToneTable* t) {
     const HostSig s = host_sig(m, k);

@@ -1,17 +1,22 @@
-"""A/B of the global tone map uint8 kernel variants against the decolor kernel
-on the C3 batch (256 Voronoi 4K frames, device-generated), CUDA events.
+"""A/B of uint8 kernel variants (tuning knobs set through the environment)
+against the default decolor kernel on the C3 batch (256 Voronoi 4K frames,
+device-generated), CUDA events.
 
-    python scripts/ab_tone.py [--images 256] [--iters 20] [--rounds 3]
-        [--configs "ROUTE=linear;GRID=20"]
+    python scripts/ab_tone.py [--op tone|decolor] [--images 256] [--iters 20] [--rounds 3]
+        [--sleep 2] [--configs "ROUTE=linear;GRID=20"]
 
-Each config sets WG_TONE_ROUTE / WG_LDG_GRID_PER_SM for the library calls;
-rounds interleave decolor and every config, the median is printed.
+Each config sets WG_TONE_ROUTE / WG_LDG_GRID_PER_SM for
+the library calls; rounds interleave the default decolor and every config
+(with --sleep seconds between measurements so the board's power average
+recovers); the median is printed, and each config's output is compared
+with the default call's bytes.
 """
 import argparse
 import json
 import os
 import statistics
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -30,16 +35,22 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--configs", default="ROUTE=linear")
+    ap.add_argument("--op", default="tone", choices=("tone", "decolor"))
+    ap.add_argument("--sleep", type=float, default=0.0)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     wl = synth.WORKLOADS[args.workload]
     rgb = synth.make_batch(wl, dev, n_images=args.images)
     out = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=dev)
-    tone_ref = wg.decolor_tone(rgb)
+    op = (lambda: wg.decolor_tone(rgb, out=out)) if args.op == "tone" else (lambda: wg.decolor(rgb, out=out))
+    tone_ref = wg.decolor_tone(rgb) if args.op == "tone" else wg.decolor(rgb)
     npx = out.numel()
     configs = [dict(kv.split("=") for kv in c.split(",") if kv) for c in args.configs.split(";")]
 
     def timed(fn):
+        if args.sleep:
+            torch.cuda.synchronize()
+            time.sleep(args.sleep)
         fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -63,7 +74,7 @@ def main():
         for cfg in configs:
             setenv(cfg)
             name = ",".join(f"{k}={v}" for k, v in cfg.items()) or "default"
-            res.setdefault(name, []).append(timed(lambda: wg.decolor_tone(rgb, out=out)))
+            res.setdefault(name, []).append(timed(op))
             if r == 0:
                 diff = (out.view(-1).int() - tone_ref.view(-1).int()).abs()
                 print(json.dumps({"config": name, "vs_default_max": int(diff.max()),
