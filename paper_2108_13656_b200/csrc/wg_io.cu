@@ -59,14 +59,15 @@ bool next_token(const std::vector<char>& buf, size_t& pos, std::string& tok) {
 bool parse_int(const std::string& tok, int64_t& v) {
     // int(token) of the reference: optional sign, decimal digits, single '_' between digits
     if (tok.empty() || tok.size() > 24) return false;
-    size_t i = (tok[0] == '+' || tok[0] == '-') ? 1 : 0;
-    if (i == tok.size()) return false;
+    const size_t first = (tok[0] == '+' || tok[0] == '-') ? 1 : 0;
+    if (first == tok.size()) return false;
     int64_t x = 0;
     int digits = 0;
-    for (; i < tok.size(); ++i) {
+    for (size_t i = first; i < tok.size(); ++i) {
         const char c = tok[i];
-        if (c == '_') {
-            if (i + 1 >= tok.size() || tok[i - 1] < '0' || tok[i - 1] > '9' || tok[i + 1] < '0' || tok[i + 1] > '9')
+        if (c == '_') {  // only between two digits: never first (after the sign) or last
+            if (i == first || i + 1 >= tok.size() || tok[i - 1] < '0' || tok[i - 1] > '9' || tok[i + 1] < '0' ||
+                tok[i + 1] > '9')
                 return false;
             continue;
         }
@@ -128,8 +129,12 @@ Err probe(const char* path, PnmInfo& info) {
         return e;
     }
     info.offset = static_cast<int64_t>(pos) + 1;  // single whitespace byte after maxval
-    const int64_t need = info.width * info.height * info.channels;
-    if (info.file_bytes - info.offset < need) {
+    // width * height * channels without overflow (header values reach 10^18): a
+    // product beyond the file is "truncated", as the reference's frombuffer count is
+    int64_t need = 0;
+    const bool overflow = __builtin_mul_overflow(info.width, info.height, &need) ||
+                          __builtin_mul_overflow(need, static_cast<int64_t>(info.channels), &need);
+    if (overflow || info.file_bytes - info.offset < need) {
         e = {WG_ECODEC, std::string(path) + ": PNM pixel data truncated"};
         return e;
     }

@@ -183,3 +183,16 @@ def test_read_write_batch_png_and_pnm(tmp_path):
     wg.save_u8(tmp_path / "small.png", batch[0, :10])
     with pytest.raises(wg.CodecError):
         wg.read_batch([png[0], tmp_path / "small.png"], pinned=False)
+
+
+@pytest.mark.parametrize("header", [b"P6\n_5 4\n255\n", b"P6\n5_ 4\n255\n", b"P6\n+_5 4\n255\n", b"P5\n5 _\n255\n",
+                                    b"P6\n999999999999999999 999999999999999999\n255\n",
+                                    b"P5\n4294967296 4294967296\n255\n"])
+def test_hostile_headers_are_codec_errors(tmp_path, header):
+    """Untrusted headers: a leading / trailing '_' in a number (the reference's
+    int() rejects it) and dimensions whose product overflows 64 bits or exceeds
+    the file are CodecErrors, never an out-of-bounds read or a wrapped size."""
+    p = tmp_path / "h.ppm"
+    p.write_bytes(header + b"\x00" * 64)
+    with pytest.raises(wg.CodecError):
+        wg.load_u8(p)
