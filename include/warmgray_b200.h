@@ -77,11 +77,14 @@ WG_API int wg_decolor_u8(const uint8_t* rgb, uint8_t* gray, int64_t npix, double
  * colours against the fp64 chain (built on the first call, cached per device). */
 WG_API int wg_decolor_u8_exact(const uint8_t* rgb, uint8_t* gray, int64_t npix, double beta_r, double beta_k,
                                void* stream);
-/* Diagnostics of that table: boundary margin (2^-15 units), slot count and
+/* Diagnostics of that table: boundary margin (2^-15 units), slot count,
  * err, the max |fast - exact| of 255 * gray + 0.5 over all 2^24 colours
- * (2^-15 units, rounded up; the exact tone map's margin is err + 2). Any
+ * (2^-15 units, rounded up; the linear exact tone route's margin is err + 2),
+ * and err_sq, the max |bits(u_fast) - bits(float((255 v)^2 + 1/8))| of the
+ * square-domain route (its exact tone route's margin is err_sq + 1). Any
  * output pointer may be NULL. */
-WG_API int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, uint32_t* slots, uint32_t* err);
+WG_API int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, uint32_t* slots, uint32_t* err,
+                            uint32_t* err_sq);
 
 /* fp32 RGB in [0,1] -> fp32 gray (decolor_image on float data; core.py:147-169). */
 WG_API int wg_decolor_f32(const float* rgb, float* gray, int64_t npix, float beta_r, float beta_k,

@@ -442,6 +442,7 @@ struct U8Exact {
     uint32_t mask;    // slots - 1 (power of two)
     uint32_t margin;  // in 2^-15 units
     uint32_t err;     // max |f_fast - f_exact| over all colours, 2^-15 units, rounded up
+    uint32_t err_sq;  // max |bits(u_fast) - bits(F(v_exact))| over all colours (square-domain route)
 };
 __host__ __device__ __forceinline__ uint32_t u8exact_slot(uint32_t key, uint32_t mask) {
     return (key * 2654435761u >> 8) & mask;

@@ -27,10 +27,19 @@ __device__ __forceinline__ uint32_t sq_word(const uint32_t* t, uint32_t off, uin
     return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(t) + off) + ub;
 }
 
+constexpr uint32_t kSqReach = 64;  // anchor reach (float-bit units of u): the exact route's margin limit
+constexpr int kSqMulti = 1, kSqCrowded = 2;
+
+// W[S] as a kernel parameter, with the bias offset of its shared-memory lookup
+// (ofs = -(0x4B000000 << 2) mod 2^32: W + 4 S = (bits(S + 2^23) << 2) + W + ofs)
+struct SqWeights {
+    uint32_t ofs;
+    float w[kSqW];
+};
+
 // host side (csrc/wg_tone.cu)
 void sq_weights(double c4sq, float* w);  // W[S] = c4^2 / S^2 (fp64, rounded once), W[0] = 0
-// step words over sorted float thresholds uf[0..n); true if a bin holds several
-bool sq_step_words(const float* uf, int n, uint32_t* step, int nbins, uint32_t lo_bits, int shift);
+int sq_step_words(const float* uf, int n, uint32_t* step, int nbins, uint32_t lo_bits, int shift, uint32_t reach);
 
 }  // namespace wg
 

@@ -70,7 +70,8 @@ struct ToneTable {
     uint32_t sq_step[kSqBins];
     uint32_t sq_gray[kSqBins];
     int sq_multi;
-    int sq_pad[3];
+    int sq_exact_ok;  // every bin's anchor is its only threshold within kSqReach (both tables)
+    int sq_pad[2];
 };
 constexpr uint32_t kEdgeUnits = 64;
 constexpr size_t kToneStaged = offsetof(ToneTable, edge);  // bytes OpToneU8 stages
@@ -318,28 +319,52 @@ int host_toned(const HostSig& s, double v) {
 
 }  // namespace
 
-// step words over sorted float thresholds uf[0..n) for bins of `shift` low
-// bits starting at float bits `lo_bits` (nbins bins); returns true if a bin
-// holds several thresholds
-bool sq_step_words(const float* uf, int n, uint32_t* step, int nbins, uint32_t lo_bits, int shift) {
-    bool multi = false;
-    int below = 0;
+// Anchored step words over sorted float thresholds uf[0..n) for nbins bins of
+// `shift` low bits starting at float bits `lo_bits` (csrc/wg_square.cuh). The
+// anchor A of bin b is its threshold, else the one within `reach` units of
+// the bin, else a virtual one 2^23 units below it; step[b] = (c0 << 24) +
+// 2^24 - bits(A), c0 = #{thresholds below A} (for the virtual anchor: the
+// count below the bin, minus one). Byte 3 of step[b] + bits(u) is the number
+// of thresholds <= u for every u of the bin, and its low 24 bits are bits(u) -
+// bits(A) mod 2^24, the exact route's distance to the nearest threshold.
+// Returns kSqMulti if a bin holds two thresholds (the route cannot decide
+// it), kSqCrowded if a bin has two thresholds within reach (the exact
+// route's distance test would miss one).
+int sq_step_words(const float* uf, int n, uint32_t* step, int nbins, uint32_t lo_bits, int shift, uint32_t reach) {
+    const auto bits_of = [&](int j) {
+        uint32_t x;
+        std::memcpy(&x, &uf[j], 4);
+        return x;
+    };
+    int flags = 0;
+    int below = 0, near_lo = 0;
     for (int b = 0; b < nbins; ++b) {
         const uint32_t first = lo_bits + (static_cast<uint32_t>(b) << shift), next = first + (1u << shift);
-        const auto bits_of = [&](int j) {
-            uint32_t x;
-            std::memcpy(&x, &uf[j], 4);
-            return x;
-        };
         while (below < n && bits_of(below) < first) ++below;
+        while (near_lo < n && bits_of(near_lo) + reach < first) ++near_lo;  // first threshold >= first - reach
         int inside = below;
         while (inside < n && bits_of(inside) < next) ++inside;
-        uint32_t L = 1u << shift;  // no threshold in the bin: never reached
-        if (inside - below == 1) L = bits_of(below) - first;
-        if (inside - below > 1) multi = true;
-        step[b] = (static_cast<uint32_t>(below) << 24) + (0x1000000u - L) - first;
+        int near_hi = inside;
+        while (near_hi < n && bits_of(near_hi) < next + reach) ++near_hi;
+        if (inside - below > 1) flags |= kSqMulti;
+        if (near_hi - near_lo > 1) flags |= kSqCrowded;
+        int a = -1;  // anchor index
+        if (inside > below) {
+            a = below;
+        } else if (near_hi > near_lo) {  // the nearest threshold within reach
+            a = near_lo;
+            for (int j = near_lo + 1; j < near_hi; ++j) {
+                const uint32_t dj = bits_of(j) < first ? first - bits_of(j) : bits_of(j) - next + 1;
+                const uint32_t da = bits_of(a) < first ? first - bits_of(a) : bits_of(a) - next + 1;
+                if (dj < da) a = j;
+            }
+        }
+        if (a >= 0)
+            step[b] = (static_cast<uint32_t>(a) << 24) + 0x1000000u - bits_of(a);
+        else  // virtual anchor first - 2^23: byte 3 = (below - 1) + 1
+            step[b] = (static_cast<uint32_t>(below - 1) << 24) + 0x1000000u - (first - 0x800000u);
     }
-    return multi;
+    return flags;
 }
 
 void sq_weights(double c4sq, float* w) {
@@ -349,36 +374,47 @@ void sq_weights(double c4sq, float* w) {
 
 namespace {
 
+// least double v in [0, 1] with pred(v) true, pred monotone (false ... true);
+// non-negative doubles order like their bits
+template <class Pred>
+double least_double(Pred pred) {
+    double v0 = 0.0, v1 = 1.0;
+    uint64_t lo, hi;
+    std::memcpy(&lo, &v0, 8);
+    std::memcpy(&hi, &v1, 8);
+    if (pred(0.0)) return 0.0;
+    while (hi - lo > 1) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        double mv;
+        std::memcpy(&mv, &mid, 8);
+        (pred(mv) ? hi : lo) = mid;
+    }
+    double th;
+    std::memcpy(&th, &hi, 8);
+    return th;
+}
+
 void build_tone_table(double m, double k, ToneTable* t) {
     const HostSig s = host_sig(m, k);
     t->multi = 0;
     float xf[255];  // f-domain thresholds
     float uf[255];  // square-domain thresholds (255 theta)^2 + 1/8
     for (int j = 1; j <= 255; ++j) {
-        // least double v in [0, 1] with toned(v) >= j (non-negative doubles order like their bits)
-        double v0 = 0.0, v1 = 1.0;
-        uint64_t lo, hi;
-        std::memcpy(&lo, &v0, 8);
-        std::memcpy(&hi, &v1, 8);
-        if (host_toned(s, 0.0) >= j) {
-            hi = lo;
-        } else {
-            while (hi - lo > 1) {
-                const uint64_t mid = lo + (hi - lo) / 2;
-                double mv;
-                std::memcpy(&mv, &mid, 8);
-                (host_toned(s, mv) >= j ? hi : lo) = mid;
-            }
-        }
-        double th;
-        std::memcpy(&th, &hi, 8);
+        const double th = least_double([&](double v) { return host_toned(s, v) >= j; });  // theta_j
         xf[j - 1] = static_cast<float>(256.0 + (th * 255.0 + 0.5));  // f = 256 + 255 v + 0.5
         uf[j - 1] = static_cast<float>((th * 255.0) * (th * 255.0) + 0.125);
     }
-    t->sq_multi = sq_step_words(uf, 255, t->sq_step, kSqBins, kSqLoBits, 15) ? 1 : 0;
-    float gf[255];  // quantize_u8's boundaries: byte j from 255 v = j - 1/2 on
-    for (int j = 1; j <= 255; ++j) gf[j - 1] = static_cast<float>((j - 0.5) * (j - 0.5) + 0.125);
-    sq_step_words(gf, 255, t->sq_gray, kSqBins, kSqLoBits, 15);
+    const int tf = sq_step_words(uf, 255, t->sq_step, kSqBins, kSqLoBits, 15, kSqReach);
+    // quantize_u8's boundaries g_j (least v with floor(v * 255 + 0.5) >= j, by bisection
+    // over the reference's fp64 expression) through the same map u = (255 v)^2 + 1/8
+    float gf[255];
+    for (int j = 1; j <= 255; ++j) {
+        const double g = least_double([&](double v) { return std::floor(v * 255.0 + 0.5) >= j; });
+        gf[j - 1] = static_cast<float>((g * 255.0) * (g * 255.0) + 0.125);
+    }
+    const int gfl = sq_step_words(gf, 255, t->sq_gray, kSqBins, kSqLoBits, 15, kSqReach);
+    t->sq_multi = (tf & kSqMulti) ? 1 : 0;
+    t->sq_exact_ok = ((tf | gfl) & (kSqMulti | kSqCrowded)) ? 0 : 1;
     for (int j = 0; j < 256; ++j) t->thr[j] = j < 255 ? xf[j] : INFINITY;
     int below = 0;
     for (int b = 0; b < kToneBins; ++b) {
@@ -421,6 +457,7 @@ struct Entry {
     ToneTable* dev = nullptr;
     bool multi = false;
     bool sq_multi = false;
+    bool sq_exact_ok = false;
 };
 constexpr int kCache = 8;
 Entry g_cache[kMaxDevices][kCache];
@@ -431,7 +468,7 @@ std::mutex g_mu;
 // before releasing it, so an eviction by another thread (cudaFree, which waits
 // for the device's queued work) cannot free a table a pending launch uses.
 int tone_table(double m, double k, const ToneTable** out, bool* multi, std::unique_lock<std::mutex>* hold,
-               bool* sq_multi = nullptr) {
+               bool* sq_multi = nullptr, bool* sq_exact_ok = nullptr) {
     int device = 0;
     cudaGetDevice(&device);
     if (device < 0 || device >= kMaxDevices) return set_error(WG_ENODEV, "device ordinal out of range");
@@ -441,6 +478,7 @@ int tone_table(double m, double k, const ToneTable** out, bool* multi, std::uniq
             *out = e.dev;
             *multi = e.multi;
             if (sq_multi) *sq_multi = e.sq_multi;
+            if (sq_exact_ok) *sq_exact_ok = e.sq_exact_ok;
             return WG_OK;
         }
     static ToneTable host;  // under g_mu
@@ -455,10 +493,11 @@ int tone_table(double m, double k, const ToneTable** out, bool* multi, std::uniq
     Entry& slot = g_cache[device][g_next[device]];
     g_next[device] = (g_next[device] + 1) % kCache;
     if (slot.used) cudaFree(slot.dev);
-    slot = {true, m, k, d, host.multi != 0, host.sq_multi != 0};
+    slot = {true, m, k, d, host.multi != 0, host.sq_multi != 0, host.sq_exact_ok != 0};
     *out = d;
     *multi = host.multi != 0;
     if (sq_multi) *sq_multi = host.sq_multi != 0;
+    if (sq_exact_ok) *sq_exact_ok = host.sq_exact_ok != 0;
     return WG_OK;
 }
 
@@ -907,6 +946,158 @@ __global__ void __launch_bounds__(256, 4)
     }
 }
 
+// ---------------------------------------------------------------- exact square-domain route
+// decolor_tone(u8, exact=True) without the colour image, on the square-domain
+// step words (OpToneSqU8's arithmetic) plus a proof per pixel: err_sq = max
+// |bits(u_fast) - bits(F(v))| over all 2^24 colours for (beta_r, beta_k),
+// F(v) = float((255 v)^2 + 1/8) the monotone map the thresholds went through
+// (wg_u8exact.cu settles it exhaustively), and M = err_sq + 1. A threshold
+// U_j = F(theta_j) more than M float-bit units from bits(u_fast) is decided
+// exactly: F(v) lies on the same side of U_j, and F is monotone, so v lies on
+// the same side of theta_j. Each bin's step word is anchored at the only
+// threshold within kSqReach >= M units of the bin (tables with two are not
+// used here: ToneTable::sq_exact_ok), so the low 24 bits of word + bits(u) -- the
+// signed distance to that anchor -- settle the pixel with two ALU ops; a
+// pixel within M of its anchor (for the toned byte, or the gray's boundary
+// table when gray is requested) goes through the per-warp queue to the
+// reference's fp64 chain. Bit-identical to the reference by construction.
+// the square-domain words (toned, gray) of pixel pair j of a thread's 16
+// pixels (12 input words): exactly OpToneSqU8's arithmetic
+template <bool kGray>
+__device__ __forceinline__ void sq_pair_words(const uint32_t (&wd)[12], int j, const U8Consts& k,
+                                              const uint32_t* s_step, const uint32_t* s_gray, uint32_t wb,
+                                              uint32_t (&t)[2], uint32_t (&g)[2]) {
+    float2 cb[3], ch[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int b0 = 3 * (2 * j) + c, b1 = 3 * (2 * j + 1) + c;
+        cb[c] = make_float2(byte_biased(wd[b0 >> 2], b0 & 3), byte_biased(wd[b1 >> 2], b1 & 3));
+        ch[c] = add2(cb[c], bc2(-kMagic));
+    }
+    float2 T, Sb;
+    decolor255_T_x2(ch[0], ch[1], ch[2], cb[2], k, T, Sb);
+    const float2 W = make_float2(__uint_as_float(lds_u32((__float_as_uint(Sb.x) << 2) + wb)),
+                                 __uint_as_float(lds_u32((__float_as_uint(Sb.y) << 2) + wb)));
+    const float2 u = fma2(T, W, bc2(kSqBias));
+    const uint32_t ux = __float_as_uint(u.x), uy = __float_as_uint(u.y);
+    const uint32_t ox = sq_bin_off(ux), oy = sq_bin_off(uy);
+    t[0] = sq_word(s_step, ox, ux);
+    t[1] = sq_word(s_step, oy, uy);
+    if constexpr (kGray) {
+        g[0] = sq_word(s_gray, ox, ux);
+        g[1] = sq_word(s_gray, oy, uy);
+    }
+}
+
+template <bool kGray>
+__global__ void __launch_bounds__(256, kGray ? 3 : 4)
+    tone_sq_exact_kernel(const uint8_t* __restrict__ rgb, uint8_t* __restrict__ toned, uint8_t* __restrict__ gray,
+                         int64_t ntiles, int64_t npix, const ToneTable* __restrict__ tab, U8Consts k, SqWeights w,
+                         uint32_t M, double br, double bk, SigD sig) {
+    extern __shared__ __align__(16) uint8_t dsm[];
+    uint32_t* s_step = reinterpret_cast<uint32_t*>(dsm);
+    uint32_t* s_gray = s_step + kSqBins;
+    float* s_w = reinterpret_cast<float*>(s_step + (kGray ? 2 : 1) * kSqBins);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t* queue = reinterpret_cast<uint32_t*>(s_w + kSqW) + wid * kExactQueue;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(tab->sq_step);
+        for (int i = tid; i < kSqBins / 4; i += 256) reinterpret_cast<uint4*>(s_step)[i] = src[i];
+        if constexpr (kGray) {
+            const uint4* sg = reinterpret_cast<const uint4*>(tab->sq_gray);
+            for (int i = tid; i < kSqBins / 4; i += 256) reinterpret_cast<uint4*>(s_gray)[i] = sg[i];
+        }
+        for (int i = tid; i < kSqW; i += 256) s_w[i] = w.w[i];
+    }
+    __syncthreads();
+    const uint32_t wb = smem_addr(s_w) + w.ofs;  // shared address of W[S] = (bits(S + 2^23) << 2) + wb
+    const uint32_t twoM = 2 * M;
+    int qn = 0;
+    const int64_t stride = gridDim.x;
+    const auto pix = [&](uint32_t e) {  // (tile iteration << 9) | pixel offset in the warp's slice
+        return (static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(e >> 9) * stride) * kRgbTile + wid * 512 +
+               (e & 511u);
+    };
+    const auto fix = [&](int64_t p) {
+        tone_rgb_px(rgb, nullptr, toned, gray, p, br, bk, sig.m, sig.k, sig.lo, sig.hi);
+    };
+    int64_t t = blockIdx.x;
+    uint4 v[3];
+    if (t < ntiles) {
+        const uint4* p = reinterpret_cast<const uint4*>(rgb + t * (kRgbTile * 3)) + tid * 3;
+        v[0] = __ldcs(p);
+        v[1] = __ldcs(p + 1);
+        v[2] = __ldcs(p + 2);
+    }
+    for (int64_t it = 0; t < ntiles; t += stride, ++it) {
+        uint4 nx[3] = {v[0], v[1], v[2]};
+        if (t + stride < ntiles) {
+            const uint4* q = reinterpret_cast<const uint4*>(rgb + (t + stride) * (kRgbTile * 3)) + tid * 3;
+            nx[0] = __ldcs(q);
+            nx[1] = __ldcs(q + 1);
+            nx[2] = __ldcs(q + 2);
+        }
+        const uint32_t wd[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y,
+                                 v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
+        uint32_t ot[4], og[4];
+        uint32_t mask = 0;  // bit i: pixel i needs the fp64 chain
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+            uint32_t tt[4], gg[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t t2[2], g2[2];
+                sq_pair_words<kGray>(wd, 2 * qd + h, k, s_step, s_gray, wb, t2, g2);
+                tt[2 * h] = t2[0];
+                tt[2 * h + 1] = t2[1];
+                // |bits(u) - bits(anchor)| <= M  <=>  ((word + M) mod 2^24) <= 2M
+                const int j = 2 * qd + h;
+                mask |= ((((t2[0] + M) & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j);
+                mask |= ((((t2[1] + M) & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j + 1);
+                if constexpr (kGray) {
+                    gg[2 * h] = g2[0];
+                    gg[2 * h + 1] = g2[1];
+                    mask |= ((((g2[0] + M) & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j);
+                    mask |= ((((g2[1] + M) & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j + 1);
+                }
+            }
+            ot[qd] = __byte_perm(__byte_perm(tt[0], tt[1], 0x0073u), __byte_perm(tt[2], tt[3], 0x0073u), 0x5410u);
+            if constexpr (kGray)
+                og[qd] = __byte_perm(__byte_perm(gg[0], gg[1], 0x0073u), __byte_perm(gg[2], gg[3], 0x0073u), 0x5410u);
+        }
+        const int64_t p0 = t * kRgbTile + static_cast<int64_t>(tid) * kRgbPx;
+        __stcs(reinterpret_cast<uint4*>(toned + p0), make_uint4(ot[0], ot[1], ot[2], ot[3]));
+        if constexpr (kGray) __stcs(reinterpret_cast<uint4*>(gray + p0), make_uint4(og[0], og[1], og[2], og[3]));
+        if (__any_sync(0xFFFFFFFFu, mask != 0u)) {
+            const int cnt = __popc(mask);
+            int pre = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+                if (lane >= d) pre += x;
+            }
+            int slot = qn + pre - cnt;
+            const uint32_t e0 = (static_cast<uint32_t>(it) << 9) | static_cast<uint32_t>(lane * kRgbPx);
+            for (uint32_t mm = mask; mm; mm &= mm - 1) queue[slot++] = e0 + (__ffs(mm) - 1);
+            qn += __shfl_sync(0xFFFFFFFFu, pre, 31);
+            __syncwarp();  // appends and this tile's provisional stores before the drain
+            if (qn >= kQueueDrain) {
+                for (int jj = lane; jj < qn; jj += 32) fix(pix(queue[jj]));
+                qn = 0;
+                __syncwarp();
+            }
+        }
+        v[0] = nx[0];
+        v[1] = nx[1];
+        v[2] = nx[2];
+    }
+    __syncwarp();
+    for (int jj = lane; jj < qn; jj += 32) fix(pix(queue[jj]));
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t p = ntiles * kRgbTile + tid; p < npix; p += 256) fix(p);
+    }
+}
+
 // fp32 constants and error budget of the fast kernel; false if the curve is
 // outside its range (then the fp64 kernel runs every pixel)
 bool make_tone_rgb_consts(double br, double bk, double m, double k, ToneRgbF* c, bool* two_ex2) {
@@ -999,13 +1190,30 @@ extern "C" int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint
         // toned (+ gray) only: the threshold-table kernel with a proven margin
         // (locks: tone cache, then exact-u8 cache, both held until the launch is enqueued)
         const ToneTable* tab = nullptr;
-        bool multi = false;
+        bool multi = false, sq_multi = false, sq_exact_ok = false;
         std::unique_lock<std::mutex> hold_t, hold_e;
-        int rc = tone_table(midpoint, slope, &tab, &multi, &hold_t);
+        int rc = tone_table(midpoint, slope, &tab, &multi, &hold_t, &sq_multi, &sq_exact_ok);
         if (rc != WG_OK) return rc;
         U8Exact ex;
         rc = u8exact_get(beta_r, beta_k, &ex, &hold_e);
         if (rc != WG_OK) return rc;
+        const char* route = std::getenv("WG_TONE_ROUTE");
+        const uint32_t Msq = ex.err_sq + 1;
+        if (sq_exact_ok && Msq <= kSqReach && !(route && std::strcmp(route, "linear") == 0)) {
+            // square-domain route with its proven margin
+            const U8Consts k = make_u8_consts(beta_r, beta_k);
+            SqWeights w;
+            w.ofs = 0u - (0x4B000000u << 2);
+            sq_weights(beta_k / 3.0, w.w);
+            const size_t smem = ((gray_or_null ? 2 : 1) * kSqBins + kSqW + 8 * kExactQueue) * sizeof(uint32_t);
+            const unsigned grid =
+                static_cast<unsigned>(std::min<int64_t>(ntiles, (gray_or_null ? 3LL : 4LL) * sm_count(device)));
+            auto kern = gray_or_null ? tone_sq_exact_kernel<true> : tone_sq_exact_kernel<false>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            kern<<<grid, 256, smem, st>>>(rgb, toned_or_null, gray_or_null, ntiles, npix, tab, k, w, Msq, beta_r,
+                                          beta_k, sig);
+            return check_launch("tone_sq_exact");
+        }
         const uint32_t M = ex.err + 2;
         if (M <= kEdgeUnits) {
             const U8Consts k = make_u8_consts(beta_r, beta_k);

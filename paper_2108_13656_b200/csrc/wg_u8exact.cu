@@ -46,9 +46,14 @@ __device__ __forceinline__ uint32_t tie_distance(uint32_t bits) {
 // need[1]: the largest |f_fast - f_exact| over all colours in 2^-15 units,
 // rounded up (f = 255 gray + 0.5 in the bits' fixed-point form) -- a true
 // error bound of the fast gray for this (beta_r, beta_k), which the exact
-// tone map compares against its thresholds
+// tone map compares against its thresholds;
+// need[2]: the same for the square-domain route (csrc/wg_square.cuh): the
+// largest |bits(u_fast) - bits(F(v))| with u_fast = T W[S] + 1/8 exactly as
+// the tone kernel forms it and F(v) = float((255 v)^2 + 1/8) of the
+// reference's fp64 gray v (the map its thresholds go through)
 __global__ void u8exact_need_kernel(U8Consts k, double br, double bk, uint32_t* need) {
-    uint32_t worst = 0, err = 0;
+    uint32_t worst = 0, err = 0, err_sq = 0;
+    const double c4sq = bk / 3.0;
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < kColours; c += gridDim.x * blockDim.x) {
         const uint32_t bits = fast_bits(c, k);
         if (bits_byte(bits) != exact_byte(c, br, bk)) worst = max(worst, tie_distance(bits) + 1);
@@ -56,9 +61,19 @@ __global__ void u8exact_need_kernel(U8Consts k, double br, double bk, uint32_t* 
         const double exact_units = (v * 255.0 + 0.5) * 32768.0;  // bits & 0x7FFFFF = (f - 256) * 2^15
         const double d = fabs(static_cast<double>(bits & 0x7FFFFFu) - exact_units);
         err = max(err, static_cast<uint32_t>(ceil(d)));
+        float T, S;
+        decolor255_T_x1(static_cast<float>(c >> 16), static_cast<float>((c >> 8) & 255u),
+                        static_cast<float>(c & 255u), k, T, S);
+        const float W = S > 0.0f ? static_cast<float>(__ddiv_rn(c4sq, __dmul_rn(S, S))) : 0.0f;  // sq_weights
+        const float uf = __fmaf_rn(T, W, 0.125f);
+        const double v255 = __dmul_rn(v, 255.0);
+        const float ue = static_cast<float>(__dadd_rn(__dmul_rn(v255, v255), 0.125));
+        const int64_t du = static_cast<int64_t>(__float_as_uint(uf)) - static_cast<int64_t>(__float_as_uint(ue));
+        err_sq = max(err_sq, static_cast<uint32_t>(du < 0 ? -du : du));
     }
     if (worst) atomicMax(need, worst);
     if (err) atomicMax(need + 1, err);
+    if (err_sq) atomicMax(need + 2, err_sq);
 }
 
 // every colour within the margin goes into the table with its exact byte
@@ -91,27 +106,27 @@ int build(int device, double br, double bk, U8Exact* out) {
     cudaStream_t st;
     cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e != cudaSuccess) return set_error(static_cast<int>(e), "u8 exact table: stream: %s", cudaGetErrorString(e));
-    uint32_t* scratch = nullptr;  // need, error bound, count
+    uint32_t* scratch = nullptr;  // need, error bound, square-domain error bound, count
     uint32_t* tab = nullptr;
     int rc = WG_OK;
     const int blocks = 8 * sm_count(device);
-    uint32_t host[3] = {0, 0, 0};
+    uint32_t host[4] = {0, 0, 0, 0};
     uint32_t slots = 1u << 15;
     do {
-        if ((e = cudaMalloc(&scratch, 12)) != cudaSuccess) break;
-        if ((e = cudaMemsetAsync(scratch, 0, 12, st)) != cudaSuccess) break;
+        if ((e = cudaMalloc(&scratch, 16)) != cudaSuccess) break;
+        if ((e = cudaMemsetAsync(scratch, 0, 16, st)) != cudaSuccess) break;
         u8exact_need_kernel<<<blocks, 256, 0, st>>>(k, br, bk, scratch);
-        if ((e = cudaMemcpyAsync(host, scratch, 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(host, scratch, 12, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
         const uint32_t margin = host[0] > kMinMargin ? host[0] : kMinMargin;
         for (;;) {  // grow until the table is at most half full
             if ((e = cudaMalloc(&tab, slots * 4ull)) != cudaSuccess) break;
             if ((e = cudaMemsetAsync(tab, 0xFF, slots * 4ull, st)) != cudaSuccess) break;
-            if ((e = cudaMemsetAsync(scratch + 2, 0, 4, st)) != cudaSuccess) break;
-            u8exact_fill_kernel<<<blocks, 256, 0, st>>>(k, br, bk, margin, tab, slots - 1, scratch + 2);
-            if ((e = cudaMemcpyAsync(host + 2, scratch + 2, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+            if ((e = cudaMemsetAsync(scratch + 3, 0, 4, st)) != cudaSuccess) break;
+            u8exact_fill_kernel<<<blocks, 256, 0, st>>>(k, br, bk, margin, tab, slots - 1, scratch + 3);
+            if ((e = cudaMemcpyAsync(host + 3, scratch + 3, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
             if ((e = cudaStreamSynchronize(st)) != cudaSuccess) break;
-            if (host[2] * 2 <= slots) break;
+            if (host[3] * 2 <= slots) break;
             cudaFree(tab);
             tab = nullptr;
             slots <<= 2;
@@ -121,6 +136,7 @@ int build(int device, double br, double bk, U8Exact* out) {
         out->mask = slots - 1;
         out->margin = margin;
         out->err = host[1];
+        out->err_sq = host[2];
     } while (false);
     if (e != cudaSuccess) {
         rc = set_error(static_cast<int>(e), "u8 exact table: %s", cudaGetErrorString(e));
@@ -166,7 +182,8 @@ int u8exact_get(double beta_r, double beta_k, U8Exact* out, std::unique_lock<std
 using namespace wg;
 
 // diagnostics: the margin and entry count of the table for (beta_r, beta_k)
-extern "C" int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, uint32_t* slots, uint32_t* err) {
+extern "C" int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, uint32_t* slots, uint32_t* err,
+                                uint32_t* err_sq) {
     WG_CHECK_ARGS(check_params(beta_r, beta_k));
     U8Exact t;
     std::unique_lock<std::mutex> hold;
@@ -175,5 +192,6 @@ extern "C" int wg_u8_exact_info(double beta_r, double beta_k, uint32_t* margin, 
     if (margin) *margin = t.margin;
     if (slots) *slots = t.mask + 1;
     if (err) *err = t.err;
+    if (err_sq) *err_sq = t.err_sq;
     return WG_OK;
 }

@@ -35,15 +35,16 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--configs", default="ROUTE=linear")
-    ap.add_argument("--op", default="tone", choices=("tone", "decolor"))
+    ap.add_argument("--op", default="tone", choices=("tone", "decolor", "tone_exact"))
     ap.add_argument("--sleep", type=float, default=0.0)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     wl = synth.WORKLOADS[args.workload]
     rgb = synth.make_batch(wl, dev, n_images=args.images)
     out = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=dev)
-    op = (lambda: wg.decolor_tone(rgb, out=out)) if args.op == "tone" else (lambda: wg.decolor(rgb, out=out))
-    tone_ref = wg.decolor_tone(rgb) if args.op == "tone" else wg.decolor(rgb)
+    op = {"tone": lambda: wg.decolor_tone(rgb, out=out), "decolor": lambda: wg.decolor(rgb, out=out),
+          "tone_exact": lambda: wg.decolor_tone(rgb, out=out, exact=True)}[args.op]
+    tone_ref = op().clone()
     npx = out.numel()
     configs = [dict(kv.split("=") for kv in c.split(",") if kv) for c in args.configs.split(";")]
 

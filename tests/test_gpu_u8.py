@@ -94,13 +94,16 @@ def test_exact_table_info():
 
     from paper_2108_13656_b200 import _lib
 
-    margin, slots, err = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
-    _lib.call("wg_u8_exact_info", 0.55, 0.8, ctypes.byref(margin), ctypes.byref(slots), ctypes.byref(err))
-    print(f"near-tie table: margin {margin.value} units of 2^-15, {slots.value} slots, max error {err.value} units")
+    margin, slots, err, err_sq = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+    _lib.call("wg_u8_exact_info", 0.55, 0.8, ctypes.byref(margin), ctypes.byref(slots), ctypes.byref(err),
+              ctypes.byref(err_sq))
+    print(f"near-tie table: margin {margin.value} units of 2^-15, {slots.value} slots, max error {err.value} units, "
+          f"square-domain max error {err_sq.value} float-bit units")
     assert 3 <= margin.value <= 16 and slots.value >= 1024
     assert 1 <= err.value <= 16  # the fast gray's exhaustive error bound (the exact tone map's margin - 2)
+    assert 1 <= err_sq.value < 64  # the square-domain bound, within the tables' anchor reach
     with pytest.raises(ValueError):
-        _lib.call("wg_u8_exact_info", 0.5, 0.8, None, None, None)
+        _lib.call("wg_u8_exact_info", 0.5, 0.8, None, None, None, None)
 
 
 def test_c1_config(torch_dev):
@@ -376,20 +379,45 @@ def test_tone_rgb_u8_voronoi_frames(torch_dev):
 
 
 def test_exact_tone_routes_agree(torch_dev, cube, monkeypatch):
-    """decolor_tone(u8, exact=True) without the colour image runs the threshold
-    kernel with an exhaustively settled margin (tone_u8_exact_kernel); the
-    colour kernel with rgb_out = NULL (WG_TONE_EXACT_VIA_RGB) is the other
-    exact route: identical bytes, steep (multi-threshold bins) curves included."""
+    """decolor_tone(u8, exact=True) without the colour image: the square-domain
+    kernel with its exhaustively settled margin (tone_sq_exact_kernel, default),
+    the linear threshold kernel (tone_u8_exact_kernel, WG_TONE_ROUTE=linear) and
+    the colour kernel with rgb_out = NULL (WG_TONE_EXACT_VIA_RGB) give identical
+    bytes -- toned-only and with gray, steep (multi-threshold bins) curves
+    included -- and equal the oracle's (the reference's bytes)."""
     import paper_2108_13656_b200 as wg
+    from oracle import oracle
 
     torch, dev = torch_dev
     t = torch.from_numpy(cube).to(dev)
-    for curve in (wg.SigmoidCurve(), wg.SigmoidCurve(0.2, 60.0), wg.SigmoidCurve(0.55, 500.0)):
+    for curve in (wg.SigmoidCurve(), wg.SigmoidCurve(0.3, 12.0), wg.SigmoidCurve(0.0, 3.0),
+                  wg.SigmoidCurve(0.2, 60.0), wg.SigmoidCurve(0.55, 500.0)):
         a, ga, _ = wg.decolor_tone(t, curve, return_gray=True, exact=True)
-        monkeypatch.setenv("WG_TONE_EXACT_VIA_RGB", "1")
-        b, gb, _ = wg.decolor_tone(t, curve, return_gray=True, exact=True)
-        monkeypatch.delenv("WG_TONE_EXACT_VIA_RGB")
-        assert torch.equal(a, b) and torch.equal(ga, gb)
+        a_only = wg.decolor_tone(t, curve, exact=True)
+        want_t, want_g = oracle.tone_u8(cube, midpoint=curve.midpoint, slope=curve.slope,
+                                        threads=oracle.default_threads(), with_gray=True)
+        assert np.array_equal(a.cpu().numpy(), want_t) and np.array_equal(ga.cpu().numpy(), want_g), curve
+        assert torch.equal(a_only, a)
+        for env in ("WG_TONE_ROUTE", "WG_TONE_EXACT_VIA_RGB"):
+            monkeypatch.setenv(env, "linear" if env == "WG_TONE_ROUTE" else "1")
+            b, gb, _ = wg.decolor_tone(t, curve, return_gray=True, exact=True)
+            monkeypatch.delenv(env)
+            assert torch.equal(a, b) and torch.equal(ga, gb), (curve, env)
+
+
+def test_exact_tone_voronoi_frames(torch_dev):
+    """exact=True on 16 C3 frames (4K Voronoi) equals the oracle byte for byte."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+    from paper_2108_13656_b200 import synth
+
+    torch, dev = torch_dev
+    for first in (0, 120, 240):
+        rgb = torch.empty((2, 2160, 3840, 3), dtype=torch.uint8, device=dev)
+        synth.fill_voronoi_u8(rgb, seed=0, first_image=first)
+        toned, gray, _ = wg.decolor_tone(rgb, return_gray=True, exact=True)
+        want_t, want_g = oracle.tone_u8(rgb.cpu().numpy(), threads=oracle.default_threads(), with_gray=True)
+        assert np.array_equal(toned.cpu().numpy(), want_t) and np.array_equal(gray.cpu().numpy(), want_g)
 
 
 def test_tone_rgb_u8_bound_headroom(torch_dev, cube, monkeypatch):
