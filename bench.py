@@ -862,7 +862,8 @@ def run_dropin(wg, wl, img):
             "api": "PlanarImage -> decolor_image -> wg_host_decolor_rows_f64"
                    + (" (+ dequantize_u8 / quantize_u8)" if img.dtype == np.uint8 else ""),
             "sample": f"1 image {wl.width}x{wl.height}, {reps} calls",
-            "note": "fp64 drop-in, bit-identical to the reference; host-bound by PlanarImage's fp64 layout"}
+            "note": "fp64 drop-in, bit-identical to the reference; PCIe-bound (32 B/px of fp64 through pinned "
+                    "staging) plus the host-side dequantize / validate / quantize of PlanarImage's fp64 layout"}
 
 
 def committed_traffic(workload: str, kernel: str):

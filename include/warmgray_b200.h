@@ -56,6 +56,12 @@ extern "C" {
 #define WG_ECODEC (-5)      /* unsupported or malformed image file (reference: CodecError) */
 #define WG_EIO (-6)         /* file could not be opened / written (reference: OSError) */
 
+/* ---- host-side container check ---------------------------------------------
+ * PlanarImage's validation (core.py:69-80) of n host float64 samples, on host
+ * threads: *result = 0 ok, 1 a non-finite sample (checked first, as the
+ * reference does), 2 a sample outside [0, 1]. No device work. */
+WG_API int wg_host_check_unit_f64(const double* p, int64_t n, int* result);
+
 /* ---- library / device info ------------------------------------------------ */
 WG_API int wg_version(void);                              /* 100 * major + minor */
 WG_API const char* wg_last_error(void);                   /* thread-local; "" when none */

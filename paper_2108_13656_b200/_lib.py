@@ -51,6 +51,7 @@ SIGNATURES = {
     "wg_sm_count": (_i, [_i]),
     "wg_decolor_u8": (_i, [_vp, _vp, _i64, _d, _d, _vp]),
     "wg_decolor_u8_exact": (_i, [_vp, _vp, _i64, _d, _d, _vp]),
+    "wg_host_check_unit_f64": (_i, [_vp, _i64, ctypes.POINTER(ctypes.c_int)]),
     "wg_u8_exact_info": (_i, [_d, _d, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32),
                               ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]),
     "wg_decolor_f32": (_i, [_vp, _vp, _i64, _f, _f, _vp]),

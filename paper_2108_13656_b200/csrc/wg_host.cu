@@ -9,6 +9,9 @@
 // copy of chunk i-1 overlap (PCIe is full duplex), then return when the
 // output is complete. Staging buffers are allocated once per device and
 // grown on demand (the device-buffer manager), guarded by a per-device mutex.
+// Pageable caller buffers (a NumPy array, the reference's PlanarImage data)
+// are staged through per-slot pinned host buffers filled / drained by host
+// threads, so their copies overlap the device work like pinned ones.
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -19,8 +22,9 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
-#include <vector>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/warmgray_b200.h"
 #include "wg_internal.h"
@@ -99,6 +103,8 @@ struct Slot {
     cudaStream_t stream = nullptr;
     void* dbuf = nullptr;
     size_t cap = 0;
+    void* hbuf = nullptr;  // pinned staging for pageable host buffers (cudaHostAlloc)
+    size_t hcap = 0;
 };
 struct DevCtx {
     std::mutex mu;
@@ -132,6 +138,42 @@ struct HostOut {
     size_t bpu;
 };
 
+// Pageable (not page-locked) host memory: a cudaMemcpyAsync from it is staged
+// by the driver through its own small bounce buffer and blocks the calling
+// thread (~8 GB/s, no overlap). Such buffers go through the slots' pinned
+// staging instead, filled and drained by host threads in parallel.
+static bool is_pageable(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+// memcpy split over up to 8 host threads (the calling thread takes one part):
+// one thread copies pageable <-> pinned at ~8-10 GB/s
+static void parallel_copy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kPart = size_t(4) << 20;
+    static const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>({8, hw, (bytes + kPart - 1) / kPart});
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t per = (bytes + nt - 1) / nt;
+    std::vector<std::thread> ts;
+    ts.reserve(nt - 1);
+    for (size_t t = 1; t < nt; ++t) {
+        const size_t a = t * per, b = std::min(bytes, a + per);
+        if (a < b)
+            ts.emplace_back([=] { std::memcpy(static_cast<uint8_t*>(dst) + a, static_cast<const uint8_t*>(src) + a, b - a); });
+    }
+    std::memcpy(dst, src, std::min(per, bytes));
+    for (std::thread& t : ts) t.join();
+}
+
 // Streams `nunits` units (pixels or images) through the device in chunks.
 // launch(dev_in[], dev_out[], dev_scratch, n_units, stream) -> WG status.
 template <class Launch, class ScratchFn>
@@ -160,6 +202,13 @@ static int host_pipeline(int device, int64_t nunits, const HostIn* ins, int nin,
     for (int i = 0; i < nout; ++i) need += align256(chunk * outs[i].bpu);
     const size_t scratch = align256(scratch_bytes(chunk));
     need += scratch;
+    // pinned staging for the pageable buffers: per slot, their chunks in order
+    bool pg_in[4] = {false, false, false, false}, pg_out[4] = {false, false, false, false};
+    size_t hneed = 0;
+    for (int i = 0; i < nin; ++i)
+        if ((pg_in[i] = is_pageable(ins[i].p))) hneed += align256(chunk * ins[i].bpu);
+    for (int i = 0; i < nout; ++i)
+        if ((pg_out[i] = is_pageable(outs[i].p))) hneed += align256(chunk * outs[i].bpu);
 
     DevCtx& ctx = g_ctx[device];
     std::lock_guard<std::mutex> lock(ctx.mu);
@@ -179,21 +228,70 @@ static int host_pipeline(int device, int64_t nunits, const HostIn* ins, int nin,
             if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
             s.cap = need;
         }
+        if (s.hcap < hneed) {
+            if (s.hbuf) cudaFreeHost(s.hbuf);
+            s.hbuf = nullptr;
+            s.hcap = 0;
+            cudaError_t e = cudaHostAlloc(&s.hbuf, hneed, cudaHostAllocDefault);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc(staging)");
+            s.hcap = hneed;
+        }
     }
+
+    // a slot's pending pageable outputs: (chunk, unit offset, unit count), drained
+    // into the caller's buffers once the slot's stream has delivered them
+    struct Pending {
+        bool active = false;
+        int64_t u0 = 0, n = 0;
+    } pend[kSlots];
+    const auto drain = [&](int si) -> int {
+        Slot& s = ctx.slots[si];
+        if (!pend[si].active) return WG_OK;
+        cudaError_t e = cudaStreamSynchronize(s.stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+        uint8_t* h = static_cast<uint8_t*>(s.hbuf);
+        for (int i = 0; i < nin; ++i)
+            if (pg_in[i]) h += align256(chunk * ins[i].bpu);
+        for (int i = 0; i < nout; ++i) {
+            if (!pg_out[i]) continue;
+            if (outs[i].p)
+                parallel_copy(static_cast<uint8_t*>(outs[i].p) + pend[si].u0 * outs[i].bpu, h,
+                              pend[si].n * outs[i].bpu);
+            h += align256(chunk * outs[i].bpu);
+        }
+        pend[si].active = false;
+        return WG_OK;
+    };
 
     int rc = WG_OK;
     const int64_t nchunks = (nunits + chunk - 1) / chunk;
     for (int64_t c = 0; c < nchunks && rc == WG_OK; ++c) {
-        Slot& s = ctx.slots[c % kSlots];
+        const int si = static_cast<int>(c % kSlots);
+        Slot& s = ctx.slots[si];
+        if (hneed) {  // the slot's staging is reused: its previous chunk must be complete and drained
+            rc = drain(si);
+            if (rc != WG_OK) break;
+            if (c >= kSlots && !pend[si].active) {
+                cudaError_t e = cudaStreamSynchronize(s.stream);
+                if (e != cudaSuccess) { rc = cuda_fail(e, "cudaStreamSynchronize"); break; }
+            }
+        }
         const int64_t u0 = c * chunk;
         const int64_t n = std::min<int64_t>(chunk, nunits - u0);
         uint8_t* cur = static_cast<uint8_t*>(s.dbuf);
+        uint8_t* hcur = static_cast<uint8_t*>(s.hbuf);
         const void* din[4] = {nullptr, nullptr, nullptr, nullptr};
         void* dout[4] = {nullptr, nullptr, nullptr, nullptr};
+        uint8_t* hout[4] = {nullptr, nullptr, nullptr, nullptr};
         for (int i = 0; i < nin; ++i) {
             din[i] = cur;
-            cudaError_t e = cudaMemcpyAsync(cur, static_cast<const uint8_t*>(ins[i].p) + u0 * ins[i].bpu,
-                                            n * ins[i].bpu, cudaMemcpyHostToDevice, s.stream);
+            const uint8_t* src = static_cast<const uint8_t*>(ins[i].p) + u0 * ins[i].bpu;
+            if (pg_in[i]) {  // pageable: host threads fill the pinned stage, the DMA engine takes it from there
+                parallel_copy(hcur, src, n * ins[i].bpu);
+                src = hcur;
+                hcur += align256(chunk * ins[i].bpu);
+            }
+            cudaError_t e = cudaMemcpyAsync(cur, src, n * ins[i].bpu, cudaMemcpyHostToDevice, s.stream);
             if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemcpyAsync H2D"); break; }
             cur += align256(chunk * ins[i].bpu);
         }
@@ -201,18 +299,26 @@ static int host_pipeline(int device, int64_t nunits, const HostIn* ins, int nin,
         for (int i = 0; i < nout; ++i) {
             dout[i] = outs[i].p ? cur : nullptr;
             cur += align256(chunk * outs[i].bpu);
+            if (pg_out[i]) {
+                hout[i] = hcur;
+                hcur += align256(chunk * outs[i].bpu);
+            }
         }
         rc = launch(din, dout, scratch ? static_cast<void*>(cur) : nullptr, n, s.stream);
         if (rc != WG_OK) break;
         for (int i = 0; i < nout; ++i) {
             if (!outs[i].p) continue;
-            cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(outs[i].p) + u0 * outs[i].bpu, dout[i],
-                                            n * outs[i].bpu, cudaMemcpyDeviceToHost, s.stream);
+            void* dst = pg_out[i] ? static_cast<void*>(hout[i])
+                                  : static_cast<void*>(static_cast<uint8_t*>(outs[i].p) + u0 * outs[i].bpu);
+            cudaError_t e = cudaMemcpyAsync(dst, dout[i], n * outs[i].bpu, cudaMemcpyDeviceToHost, s.stream);
             if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemcpyAsync D2H"); break; }
         }
+        if (hneed) pend[si] = {true, u0, n};
     }
-    for (Slot& s : ctx.slots) {
-        cudaError_t e = cudaStreamSynchronize(s.stream);
+    for (int si = 0; si < kSlots; ++si) {
+        const int r = hneed ? drain(si) : WG_OK;
+        if (r != WG_OK && rc == WG_OK) rc = r;
+        cudaError_t e = cudaStreamSynchronize(ctx.slots[si].stream);
         if (e != cudaSuccess && rc == WG_OK) rc = cuda_fail(e, "cudaStreamSynchronize");
     }
     return rc;
@@ -268,6 +374,41 @@ extern "C" int wg_device_count(void) {
 }
 
 extern "C" int wg_sm_count(int device) { return sm_count(device); }
+
+// ====================================================================== host-side container check
+// PlanarImage's validation (core.py:69-80: finite, then inside [0, 1]) over a
+// host float64 array, split over host threads: 0 ok, 1 a non-finite sample,
+// 2 a sample outside [0, 1]. The reference's NumPy checks make three passes
+// over the samples on one core; this is one pass on up to 16.
+extern "C" int wg_host_check_unit_f64(const double* p, int64_t n, int* result) {
+    WG_CHECK_ARGS(check_npix(n) || (n > 0 && (!p || !result)) || !result);
+    constexpr int64_t kPart = int64_t(1) << 20;
+    static const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t nt = std::min<int64_t>({16, static_cast<int64_t>(hw), (n + kPart - 1) / kPart});
+    std::vector<int> bad(static_cast<size_t>(std::max<int64_t>(nt, 1)), 0);  // bit 0 non-finite, bit 1 out of range
+    const auto scan = [&](int64_t t) {
+        const int64_t per = (n + nt - 1) / nt, a = t * per, b = std::min(n, a + per);
+        int f = 0;
+        for (int64_t i = a; i < b; ++i) {
+            const double v = p[i];
+            if (!(v - v == 0.0)) f |= 1;         // NaN or +-inf
+            else if (v < 0.0 || v > 1.0) f |= 2;  // -0.0 passes, as in NumPy
+        }
+        bad[static_cast<size_t>(t)] = f;
+    };
+    if (nt <= 1) {
+        if (n > 0) scan(0);
+    } else {
+        std::vector<std::thread> ts;
+        for (int64_t t = 1; t < nt; ++t) ts.emplace_back(scan, t);
+        scan(0);
+        for (std::thread& t : ts) t.join();
+    }
+    int f = 0;
+    for (int x : bad) f |= x;
+    *result = (f & 1) ? 1 : ((f & 2) ? 2 : 0);
+    return WG_OK;
+}
 
 // ====================================================================== host-buffer entry points
 extern "C" int wg_host_decolor_rows_f64(const double* rgb, double* out, int64_t height, int64_t width,
