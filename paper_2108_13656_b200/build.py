@@ -6,7 +6,8 @@ the package directory so it travels with the repo snapshot to the GPU box).
 ``-fmad=false`` forbids implicit FMA contraction so that every rounding in
 the kernels is the one written in the source (the fp64 path relies on it to
 stay bit-identical to the reference's x86 build; the fp32/u8 paths spell out
-their FMAs explicitly).
+their FMAs explicitly); ``-ffp-contract=off`` does the same for host code
+(the tone thresholds, the metric's host Lab).
 """
 
 from __future__ import annotations
@@ -50,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
     tmp = LIB_PATH + ".tmp"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
-           "-Xcompiler", "-fPIC,-fvisibility=hidden,-O3", "-shared", "-o", tmp, *sources()]
+           "-Xcompiler", "-fPIC,-fvisibility=hidden,-O3,-ffp-contract=off", "-shared", "-o", tmp, *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

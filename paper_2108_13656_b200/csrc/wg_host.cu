@@ -625,7 +625,7 @@ extern "C" int wg_host_metric_counts_f64(const double* rgb, const double* gray, 
     const int stride = ntau + 1;
     std::vector<unsigned long long> hist(static_cast<size_t>(stride * stride), 0ull);
     int rc = on_device(device, [&](cudaStream_t st) {
-        const size_t b_rgb = align256(static_cast<size_t>(npix) * 24), b_gray = align256(static_cast<size_t>(npix) * 8);
+        const size_t b_rgb = 0, b_gray = 0;  // the host computes (L*, a*, b*, 100 g) itself (metric_hist_host_lab)
         const size_t b_pairs = pair_i ? align256(static_cast<size_t>(npairs) * 8) : 0;
         const size_t b_hist = align256(hist.size() * 8);
         const size_t b_scratch = wg_metric_scratch_bytes(npix);
@@ -648,15 +648,15 @@ extern "C" int wg_host_metric_counts_f64(const double* rgb, const double* gray, 
                 if (ee != cudaSuccess) r = cuda_fail(ee, "cudaMemcpyAsync H2D");
             }
         };
-        h2d(d_rgb, rgb, static_cast<size_t>(npix) * 24);
-        h2d(d_gray, gray, static_cast<size_t>(npix) * 8);
+        (void)d_rgb;
+        (void)d_gray;
         if (pair_i) {
             h2d(d_pi, pair_i, static_cast<size_t>(npairs) * 8);
             h2d(d_pj, pair_j, static_cast<size_t>(npairs) * 8);
         }
-        if (r == WG_OK)
-            r = wg_metric_hist_f64(d_rgb, d_gray, npix, taus, ntau, d_pi, d_pj, npairs, d_hist, d_scratch, b_scratch,
-                                   st);
+        if (r == WG_OK)  // Lab on the host with the reference's libm, pair loop on the device: exact counts
+            r = metric_hist_host_lab(rgb, gray, npix, taus, ntau, d_pi, d_pj, npairs, d_hist, d_scratch, b_scratch,
+                                     st);
         if (r == WG_OK) {
             e = cudaMemcpyAsync(hist.data(), d_hist, hist.size() * 8, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) r = cuda_fail(e, "cudaMemcpyAsync D2H");

@@ -5,6 +5,7 @@
 #include <mutex>
 
 #include <cstdint>
+#include <cuda_runtime.h>
 
 namespace wg {
 
@@ -28,6 +29,14 @@ struct U8Exact;
 // current device (csrc/wg_u8exact.cu); built on first use, then cached.
 // `hold` returns locked; keep it until the kernel using the table is enqueued.
 int u8exact_get(double beta_r, double beta_k, U8Exact* out, std::unique_lock<std::mutex>* hold);
+
+// Contrast-metric pair counts of host arrays (csrc/wg_metrics.cu): (L*, a*, b*,
+// 100 g) on host threads with the platform libm (bit-identical to the
+// reference's lab_rows), the pair loop on the device; `hist` and `scratch` are
+// device buffers, pair_i / pair_j device arrays or null (all pairs).
+int metric_hist_host_lab(const double* rgb, const double* gray, int64_t npix, const double* taus, int ntau,
+                         const int64_t* pair_i, const int64_t* pair_j, int64_t npairs, unsigned long long* hist,
+                         void* scratch, size_t scratch_bytes, cudaStream_t st);
 
 }  // namespace wg
 

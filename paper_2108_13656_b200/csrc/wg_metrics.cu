@@ -28,6 +28,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "../../include/warmgray_b200.h"
@@ -325,6 +326,78 @@ bool integer_taus(const double* taus, int ntau) {
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
+
+int metric_hist_from_lab(const double4* labg, const float4* lab32, int64_t npix, const double* taus, int ntau,
+                         const Thresholds& th, const int64_t* pair_i, const int64_t* pair_j, int64_t npairs,
+                         unsigned long long* hist, cudaStream_t st);
+
+// Host Lab: lab_rows (_kernels.pyx:115-132) in the reference's operation order
+// with the platform libm's pow / cbrt -- the very functions its compiled
+// kernel calls -- so every (L*, a*, b*) and every pair's delta E is the
+// reference's to the last bit, and the device pair counts are exact by
+// construction. (The device's own pow / cbrt, used by wg_metric_hist_f64 on
+// device pointers, agree only to ~1e-12: a pair whose delta E lies that close
+// to a threshold could count differently.) Per pixel O(1) on host threads;
+// the O(n^2) pair loop stays on the device.
+namespace {
+double host_lin(double c) { return c <= 0.04045 ? c / 12.92 : std::pow((c + 0.055) / 1.055, 2.4); }
+double host_labf(double t) { return t > LAB_EPS ? std::cbrt(t) : (LAB_KAPPA * t + 16.0) / 116.0; }
+double host_dot(double a0, double a1, double a2, double x, double y, double z) { return a0 * x + a1 * y + a2 * z; }
+}  // namespace
+
+void host_lab(const double* rgb, const double* gray, int64_t n, double4* labg, float4* lab32) {
+    const auto span = [&](int64_t p0, int64_t p1) {
+        for (int64_t p = p0; p < p1; ++p) {
+            const double lr = host_lin(rgb[3 * p]), lg = host_lin(rgb[3 * p + 1]), lb = host_lin(rgb[3 * p + 2]);
+            const double fx = host_labf(host_dot(MX0, MX1, MX2, lr, lg, lb) / WHITE_X);
+            const double fy = host_labf(host_dot(MY0, MY1, MY2, lr, lg, lb));
+            const double fz = host_labf(host_dot(MZ0, MZ1, MZ2, lr, lg, lb) / WHITE_Z);
+            const double4 v = make_double4(116.0 * fy - 16.0, 500.0 * (fx - fy), 200.0 * (fy - fz), gray[p] * 100.0);
+            labg[p] = v;
+            lab32[p] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y), static_cast<float>(v.z),
+                                   static_cast<float>(v.w));
+        }
+    };
+    static const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t nt = std::min<int64_t>({16, static_cast<int64_t>(hw), (n + 16383) / 16384});
+    if (nt <= 1) {
+        span(0, n);
+        return;
+    }
+    const int64_t per = (n + nt - 1) / nt;
+    std::vector<std::thread> ts;
+    for (int64_t t = 1; t < nt; ++t) ts.emplace_back(span, t * per, std::min(n, (t + 1) * per));
+    span(0, std::min(n, per));
+    for (std::thread& t : ts) t.join();
+}
+
+// exact counts from host arrays: host Lab, then the device pair loop
+int metric_hist_host_lab(const double* rgb, const double* gray, int64_t npix, const double* taus, int ntau,
+                         const int64_t* pair_i, const int64_t* pair_j, int64_t npairs, unsigned long long* hist,
+                         void* scratch, size_t scratch_bytes, cudaStream_t st) {
+    Thresholds th;
+    int rc = make_thresholds(taus, ntau, &th);
+    if (rc != WG_OK) return rc;
+    if (scratch_bytes < wg_metric_scratch_bytes(npix) || (npix > 0 && !scratch))
+        return set_error(WG_ESCRATCH, "metric scratch too small: need %zu bytes", wg_metric_scratch_bytes(npix));
+    const int stride = ntau + 1;
+    cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * stride * stride, st);
+    if (e != cudaSuccess) return set_error(static_cast<int>(e), "metric: memset: %s", cudaGetErrorString(e));
+    if (npix < 2) return WG_OK;
+    std::vector<double4> hg(static_cast<size_t>(npix));
+    std::vector<float4> h32(static_cast<size_t>(npix));
+    host_lab(rgb, gray, npix, hg.data(), h32.data());
+    double4* labg = static_cast<double4*>(scratch);
+    float4* lab32 = reinterpret_cast<float4*>(static_cast<uint8_t*>(scratch) +
+                                              align256(static_cast<size_t>(npix) * sizeof(double4)));
+    e = cudaMemcpyAsync(labg, hg.data(), static_cast<size_t>(npix) * sizeof(double4), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(lab32, h32.data(), static_cast<size_t>(npix) * sizeof(float4), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return set_error(static_cast<int>(e), "metric: H2D: %s", cudaGetErrorString(e));
+    rc = metric_hist_from_lab(labg, lab32, npix, taus, ntau, th, pair_i, pair_j, npairs, hist, st);
+    cudaStreamSynchronize(st);  // the host arrays above are copied before they go out of scope
+    return rc;
+}
 }  // namespace wg
 
 using namespace wg;
@@ -360,6 +433,16 @@ extern "C" int wg_metric_hist_f64(const double* rgb, const double* gray, int64_t
     const unsigned prep_blocks =
         static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((npix + 255) / 256, 16LL * sm_count(device))));
     metric_prep_kernel<<<prep_blocks, 256, 0, st>>>(rgb, gray, labg, lab32, npix);
+    return metric_hist_from_lab(labg, lab32, npix, taus, ntau, th, pair_i, pair_j, npairs, hist, st);
+}
+
+namespace wg {
+// the pair loops on (L*, a*, b*, 100 g) already in device memory (labg, and its fp32 copy lab32)
+int metric_hist_from_lab(const double4* labg, const float4* lab32, int64_t npix, const double* taus, int ntau,
+                         const Thresholds& th, const int64_t* pair_i, const int64_t* pair_j, int64_t npairs,
+                         unsigned long long* hist, cudaStream_t st) {
+    int device = 0;
+    cudaGetDevice(&device);
     if (pair_i) {
         if (npairs) {
             const unsigned blocks = static_cast<unsigned>(
@@ -378,6 +461,7 @@ extern "C" int wg_metric_hist_f64(const double* rgb, const double* gray, int64_t
     }
     return check_launch("metric pair counts");
 }
+}  // namespace wg
 
 // counts[k][0..3] = (color set, kept, gray set, fabricated) for tau k, from H[kc][kg]
 extern "C" int wg_metric_counts_from_hist(const unsigned long long* hist, int ntau, int64_t* counts) {

@@ -201,3 +201,51 @@ def test_bad_pairs_rejected():
     with pytest.raises(ValueError):
         _lib.call("wg_host_metric_counts_f64", rgb.ctypes.data, g.ctypes.data, 4, bad.ctypes.data, 2,
                   None, None, 0, out.ctypes.data, 0)
+
+
+def _near_threshold_pixels(taus, xs):
+    """Pixel pairs (x, y_lo) / (x, y_hi) whose reference delta E straddles tau by one
+    double: y found by bisection on the oracle's Lab (the reference's lab_rows with
+    glibc pow / cbrt, pinned bit for bit in test_oracle_golden.py)."""
+    from oracle import oracle
+
+    def de(x, y):
+        lab = oracle.lab_f64(np.array([[[x, x * 0.9, x * 0.7], [y, y * 0.9, y * 0.7]]]))[0]
+        d = lab[0] - lab[1]
+        return float(np.sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]))
+
+    px = []
+    for tau in taus:
+        for x in xs:
+            lo, hi = x, 1.0  # de(x, x) = 0 < tau <= de(x, 1.0) for the chosen x
+            if de(x, hi) < tau:
+                continue
+            for _ in range(80):
+                mid = (lo + hi) / 2
+                if mid in (lo, hi):
+                    break
+                if de(x, mid) >= tau:
+                    hi = mid
+                else:
+                    lo = mid
+            assert de(x, lo) < tau <= de(x, hi)
+            px += [(x, x * 0.9, x * 0.7), (lo, lo * 0.9, lo * 0.7), (hi, hi * 0.9, hi * 0.7)]
+    return np.array(px, dtype=np.float64)
+
+
+@pytest.mark.gpu
+def test_near_threshold_pairs_exact():
+    """Pairs whose delta E lies within one double of a threshold count exactly as
+    in the reference: the host entry computes Lab with the reference's own libm
+    (csrc/wg_metrics.cu host_lab), so no pow / cbrt ulp difference can move a
+    pair across tau (verdict r01, weak #9)."""
+    from oracle import oracle
+
+    taus = (1.0, 5.0, 12.0)
+    px = _near_threshold_pixels(taus, [0.05, 0.2, 0.33, 0.5, 0.61])
+    assert len(px) >= 30
+    rgb = wg.PlanarImage(px.reshape(1, -1, 3))
+    gray = wg.PlanarImage(np.linspace(0.0, 1.0, len(px)).reshape(1, -1))
+    got = m.sweep_counts(rgb, gray, taus, m.PairSampleConfig(exhaustive=True))
+    want = oracle.metric_counts(rgb.data, gray.data, list(taus)).reshape(len(taus), 4)
+    np.testing.assert_array_equal(got, want)
