@@ -55,6 +55,13 @@ struct GridPerSm : std::integral_constant<int, 40> {};
 template <class T>
 struct GridPerSm<T, std::void_t<decltype(T::kGridPerSm)>> : std::integral_constant<int, T::kGridPerSm> {};
 
+// An Op may define `epilogue()`: it runs in every thread of ldg_stream_kernel
+// after its last tile, before the tail (e.g. draining per-warp queues).
+template <class T, class = void>
+struct HasEpilogue : std::false_type {};
+template <class T>
+struct HasEpilogue<T, std::void_t<decltype(&T::epilogue)>> : std::true_type {};
+
 template <class Op>
 __device__ __forceinline__ void run_prologue(const Op& op) {
     if constexpr (HasPrologue<Op>::value) {
@@ -178,6 +185,7 @@ __global__ void __launch_bounds__(kBlock, kBlock == kThreads ? MinBlocks<Op>::va
             if (t >= ntiles) break;
         }
     }
+    if constexpr (HasEpilogue<Op>::value) op.epilogue();
     if (blockIdx.x == gridDim.x - 1) {
         for (int64_t p = ntiles * kTilePx + tid; p < npix; p += kBlock) op.scalar(p);
     }

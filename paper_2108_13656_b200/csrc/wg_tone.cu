@@ -1098,6 +1098,118 @@ __global__ void __launch_bounds__(256, kGray ? 3 : 4)
     }
 }
 
+// The toned-only exact route as an Op of the streaming skeleton (default;
+// WG_TONE_EXACT_KERNEL=1 selects tone_sq_exact_kernel, which also serves the
+// gray output): the same arithmetic and proof as tone_sq_exact_kernel, 955
+// vs 897 Gpix/s on C3; the per-warp queues live in
+// shared memory with their length (warp-uniform), the skeleton's epilogue
+// drains what is left. An entry is (tile iteration << 12 | pixel in tile).
+struct OpToneSqExactU8 {
+    static constexpr bool kLdg = true;
+    static constexpr bool kPingPong = false;  // one register buffer ...
+    static constexpr int kMinBlocks = 4;      // ... at 4 CTAs/SM (64 registers): 955 Gpix/s on C3;
+    // two buffers spill at 48 or 64 registers (624 / 875), one buffer at 48 spills too (559)
+    static constexpr int kPx = 16;
+    const uint8_t* in;
+    uint8_t* toned;
+    U8Consts k;
+    const ToneTable* tab;
+    uint32_t M;
+    double br, bk;
+    SigD sig;
+    SqWeights w;
+
+    __device__ __forceinline__ static uint32_t* s_step() {
+        __shared__ __align__(16) uint32_t t[kSqBins];
+        return t;
+    }
+    __device__ __forceinline__ static float* s_w() {
+        __shared__ __align__(16) float t[kSqW];
+        return t;
+    }
+    __device__ __forceinline__ static uint32_t* s_queue() {
+        __shared__ uint32_t q[8 * kExactQueue];
+        return q;
+    }
+    __device__ __forceinline__ static int* s_qn() {
+        __shared__ int n[8];
+        return n;
+    }
+    __device__ __forceinline__ void prologue() const {
+        const uint4* src = reinterpret_cast<const uint4*>(tab->sq_step);
+        for (int i = threadIdx.x; i < kSqBins / 4; i += blockDim.x) reinterpret_cast<uint4*>(s_step())[i] = src[i];
+        for (int i = threadIdx.x; i < kSqW; i += blockDim.x) s_w()[i] = w.w[i];
+        if (threadIdx.x < 8) s_qn()[threadIdx.x] = 0;
+    }
+    __device__ __forceinline__ void fix(int64_t p) const {
+        tone_rgb_px(in, nullptr, toned, nullptr, p, br, bk, sig.m, sig.k, sig.lo, sig.hi);
+    }
+    __device__ __forceinline__ int64_t entry_px(uint32_t e) const {
+        const int64_t tpx = static_cast<int64_t>(blockDim.x) * kPx;
+        return (static_cast<int64_t>(blockIdx.x) + static_cast<int64_t>(e >> 12) * gridDim.x) * tpx + (e & 4095u);
+    }
+    __device__ __forceinline__ void drain(uint32_t* q, int qn) const {
+        for (int j = threadIdx.x & 31; j < qn; j += 32) fix(entry_px(q[j]));
+    }
+    __device__ __forceinline__ void vec(const uint4 (&v)[3], int64_t px0) const {
+        const uint32_t wd[12] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y,
+                                 v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
+        const uint32_t wb = smem_addr(s_w()) + w.ofs;
+        const uint32_t twoM = 2 * M;
+        uint32_t ot[4], mask = 0;
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+            uint32_t tt[4];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = 2 * qd + h;
+                uint32_t t2[2], g2[2];
+                sq_pair_words<false>(wd, j, k, s_step(), nullptr, wb, t2, g2);
+                tt[2 * h] = t2[0];
+                tt[2 * h + 1] = t2[1];
+                // |bits(u) - bits(anchor)| <= M  <=>  ((word + M) mod 2^24) <= 2M
+                mask |= ((((t2[0] + M) & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j);
+                mask |= ((((t2[1] + M) & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j + 1);
+            }
+            ot[qd] = __byte_perm(__byte_perm(tt[0], tt[1], 0x0073u), __byte_perm(tt[2], tt[3], 0x0073u), 0x5410u);
+        }
+        st_global_cs_v4(toned + px0, make_uint4(ot[0], ot[1], ot[2], ot[3]));
+        if (__any_sync(0xFFFFFFFFu, mask != 0u)) {  // rare: queue the pixels for the fp64 chain
+            const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+            uint32_t* q = s_queue() + wid * kExactQueue;
+            int qn = s_qn()[wid];
+            const int cnt = __popc(mask);
+            int pre = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int x = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+                if (lane >= d) pre += x;
+            }
+            int slot = qn + pre - cnt;
+            const int64_t tpx = static_cast<int64_t>(blockDim.x) * kPx;
+            const int64_t tile = px0 / tpx;
+            const uint32_t e0 = (static_cast<uint32_t>((tile - blockIdx.x) / gridDim.x) << 12) |
+                                static_cast<uint32_t>(px0 - tile * tpx);
+            for (uint32_t mm = mask; mm; mm &= mm - 1) q[slot++] = e0 + (__ffs(mm) - 1);
+            qn += __shfl_sync(0xFFFFFFFFu, pre, 31);
+            __syncwarp();  // appends and this tile's provisional stores before the drain
+            if (qn >= kQueueDrain) {
+                drain(q, qn);
+                qn = 0;
+                __syncwarp();
+            }
+            if (lane == 0) s_qn()[wid] = qn;
+            __syncwarp();
+        }
+    }
+    __device__ __forceinline__ void epilogue() const {
+        const int wid = threadIdx.x >> 5;
+        __syncwarp();
+        drain(s_queue() + wid * kExactQueue, s_qn()[wid]);
+    }
+    __device__ __forceinline__ void scalar(int64_t p) const { fix(p); }
+};
+
 // fp32 constants and error budget of the fast kernel; false if the curve is
 // outside its range (then the fp64 kernel runs every pixel)
 bool make_tone_rgb_consts(double br, double bk, double m, double k, ToneRgbF* c, bool* two_ex2) {
@@ -1208,6 +1320,12 @@ extern "C" int wg_decolor_tone_rgb_u8(const uint8_t* rgb, uint8_t* rgb_out, uint
             const size_t smem = ((gray_or_null ? 2 : 1) * kSqBins + kSqW + 8 * kExactQueue) * sizeof(uint32_t);
             const unsigned grid =
                 static_cast<unsigned>(std::min<int64_t>(ntiles, (gray_or_null ? 3LL : 4LL) * sm_count(device)));
+            if (!gray_or_null && !std::getenv("WG_TONE_EXACT_KERNEL")) {
+                // toned only: the Op on the streaming skeleton (pingpong, 5 CTAs/SM)
+                const void* outs[1] = {toned_or_null};
+                return launch_stream(OpToneSqExactU8{rgb, toned_or_null, k, tab, Msq, beta_r, beta_k, sig, w}, rgb,
+                                     outs, 1, npix, st);
+            }
             auto kern = gray_or_null ? tone_sq_exact_kernel<true> : tone_sq_exact_kernel<false>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             kern<<<grid, 256, smem, st>>>(rgb, toned_or_null, gray_or_null, ntiles, npix, tab, k, w, Msq, beta_r,

@@ -25,7 +25,7 @@ import torch  # noqa: E402
 import paper_2108_13656_b200 as wg  # noqa: E402
 from paper_2108_13656_b200 import synth  # noqa: E402
 
-KEYS = {"GRID": "WG_LDG_GRID_PER_SM", "ROUTE": "WG_TONE_ROUTE"}
+KEYS = {"GRID": "WG_LDG_GRID_PER_SM", "ROUTE": "WG_TONE_ROUTE", "XK": "WG_TONE_EXACT_KERNEL"}
 
 
 def main():

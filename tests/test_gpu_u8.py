@@ -403,6 +403,9 @@ def test_exact_tone_routes_agree(torch_dev, cube, monkeypatch):
             b, gb, _ = wg.decolor_tone(t, curve, return_gray=True, exact=True)
             monkeypatch.delenv(env)
             assert torch.equal(a, b) and torch.equal(ga, gb), (curve, env)
+        monkeypatch.setenv("WG_TONE_EXACT_KERNEL", "1")  # toned only through the standalone kernel
+        assert torch.equal(wg.decolor_tone(t, curve, exact=True), a)
+        monkeypatch.delenv("WG_TONE_EXACT_KERNEL")
 
 
 def test_exact_tone_voronoi_frames(torch_dev):
