@@ -197,18 +197,20 @@ def _nhw(shape):
 
 
 def decolor_tone_local(rgb, grid=None, params: DecolorParams = DEFAULT_PARAMS, return_gray: bool = False,
-                       scratch=None, stream=None):
+                       scratch=None, stream=None, out=None):
     """Fused decolor + local tone map of a device uint8 (N, H, W, 3) / (H, W, 3) batch.
 
     Per image: toned = quantize_u8(apply_local_lhe(decolor_image(rgb / 255), grid)),
     bit-identical to the fp64 reference; ``return_gray`` adds quantize_u8 of the
-    gray. ``grid`` defaults to LocalHistogramGrid.for_image(W, H).
+    gray. ``grid`` defaults to LocalHistogramGrid.for_image(W, H); ``out``: optional
+    destination for the toned batch (contiguous uint8, rgb.shape[:-1]).
     """
     torch = _torch()
     _check_rgb_tensor(rgb, ("uint8",))
     n, h, w = _nhw(rgb.shape)
     g = _grid_for(h, w, grid)
-    toned = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=rgb.device)
+    toned = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=rgb.device) if out is None \
+        else _check_out(out, rgb.shape[:-1], rgb)
     gray = torch.empty_like(toned) if return_gray else None
     need = int(_lib.load().wg_lhe_scratch_bytes(n, h, w, g.tile_w, g.tile_h, g.bins))
     if scratch is None or scratch.numel() < need:

@@ -35,7 +35,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/warmgray_b200.h"
 #include "wg_device.cuh"
@@ -79,6 +81,11 @@ struct LheBufs {
     double* yf;
     float* yff;
     float* gray255;  // [nimg][h][w] uint8 route: the hist pass's 255 * gray estimate, reused by apply
+    // uint8 route (bins <= 65536), built once per call for the apply blocks:
+    float4* qtab;    // [nimg][nband][nx * nb] blend table of each row band (lhe_table_kernel)
+    uint8_t* qident; // [nimg][nband] the band's table holds an identity tile (raw curves)
+    float* colf;     // [wpad] per-column blend fraction, apply's interleaved order
+    uint32_t* colo;  // [wpad] per-column byte offset of the left tile's table, same order
 };
 
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -104,6 +111,12 @@ size_t layout(const LheGeom& g, uint8_t* base, LheBufs* b) {
     t.yf = reinterpret_cast<double*>(take(g.h * 8));
     t.yff = reinterpret_cast<float*>(take(g.h * 4));
     t.gray255 = reinterpret_cast<float*>(take(static_cast<size_t>(g.nimg) * g.h * g.w * 4));
+    const bool u8 = g.nb <= 65536;
+    const size_t nband = g.ny > 1 ? g.ny - 1 : 1, wpad = (g.w + 15) / 16 * 16;
+    t.qtab = reinterpret_cast<float4*>(take(u8 ? static_cast<size_t>(g.nimg) * nband * g.nx * g.nb * 16 : 0));
+    t.qident = take(u8 ? static_cast<size_t>(g.nimg) * nband : 0);
+    t.colf = reinterpret_cast<float*>(take(u8 ? wpad * 4 : 0));
+    t.colo = reinterpret_cast<uint32_t*>(take(u8 ? wpad * 4 : 0));
     if (b) *b = t;
     return off;
 }
@@ -468,13 +481,21 @@ struct U8Lhe {
     float nb_over_255;  // fl(nb / 255)
     float half_m;       // 0.5 - m, m = 1e-6 nb the margin in t = v * nb
     float t_hi;         // nb - 0.5
+    // 16-bit plane word u = floor(t * 2^F) (t = v nb unclamped, F = 16 - ceil(log2 nb)):
+    // bin = u >> F, v = (u + 1/2) 2^-F / nb to within qhalf = 2^-F / (2 nb)
+    float u_magic;  // 2^(7 + ceil(log2 nb)): fl_rd(t + u_magic) holds floor(t 2^F) in its low bits
+    int ufrac;      // F
+    uint32_t umax;  // nb 2^F - 1
 
     // bin from the 0..255-domain estimate g255: t = g255 * nb/255 with
     // |t - v nb| <= (2.4e-7 + 6e-8 + 6e-8) nb < m. t is clamped to [0.5, nb - 0.5]
     // (0 and nb are not bin edges), floor(t) taken as the low bits of
     // fl_rd(t + 2^23) (no F2I); `sure` is false within m of an inner edge.
     __device__ __forceinline__ int bin_fast(float g255, bool& sure) const {
-        const float t = fminf(fmaxf(__fmul_rn(g255, nb_over_255), 0.5f), t_hi);
+        return bin_fast_t(__fmul_rn(g255, nb_over_255), sure);
+    }
+    __device__ __forceinline__ int bin_fast_t(float tu, bool& sure) const {
+        const float t = fminf(fmaxf(tu, 0.5f), t_hi);
         const float tf = __fadd_rd(t, 8388608.0f);
         sure = fabsf(__fsub_rn(__fsub_rn(t, __fsub_rn(tf, 8388608.0f)), 0.5f)) < half_m;
         return static_cast<int>(__float_as_uint(tf) & 0x7fffffu);
@@ -482,37 +503,39 @@ struct U8Lhe {
 };
 
 // Per-warp queue of the rare pixels that need the reference's fp64 chain
-// (entry = group index * 16 + pixel): lanes append their flagged pixels at a
-// shuffle prefix sum and the warp drains the queue through `fix` 32 at a time
-// (all lanes busy) instead of each flagged lane running the long fp64 chain
-// while its warp waits. Capacity: < 32 carried + one group per lane.
-constexpr int kWq = 32 + 32 * kGrp;
+// (entry = group index * 16 + pixel): each round every lane with flagged pixels
+// appends one at its ballot rank, and once 32 are queued the warp drains them
+// through `fix` with all lanes busy (instead of each flagged lane running the
+// long fp64 chain while its warp waits). Capacity: < 32 carried + 32 appended.
+constexpr int kWq = 64;
 constexpr size_t kWqBytes = static_cast<size_t>(kBlock / 32) * kWq * 4;
 template <class F>
 __device__ __forceinline__ void wq_push(uint32_t* q, int& qn, uint32_t mask, uint32_t gi, F&& fix) {
-    if (!__any_sync(0xFFFFFFFFu, mask != 0u)) return;
-    const int lane = threadIdx.x & 31;
-    const int cnt = __popc(mask);
-    int pre = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const int x = __shfl_up_sync(0xFFFFFFFFu, pre, d);
-        if (lane >= d) pre += x;
-    }
-    int slot = qn + pre - cnt;
-    for (uint32_t mm = mask; mm; mm &= mm - 1) q[slot++] = gi * kGrp + static_cast<uint32_t>(__ffs(mm) - 1);
-    qn += __shfl_sync(0xFFFFFFFFu, pre, 31);
-    __syncwarp();  // appends (and the callers' provisional stores) before the drain
-    if (qn >= 32) {
-        for (int j = lane; j < qn; j += 32) fix(q[j]);
-        qn = 0;
-        __syncwarp();  // queue reads before the next appends
+    const uint32_t lane = threadIdx.x & 31u;
+    for (;;) {
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mask != 0u);
+        if (!bal) return;
+        if (mask) {
+            q[qn + __popc(bal & ((1u << lane) - 1u))] = gi * kGrp + static_cast<uint32_t>(__ffs(mask) - 1);
+            mask &= mask - 1u;
+        }
+        qn += __popc(bal);
+        __syncwarp();  // appends (and the callers' provisional stores) before the drain
+        if (qn >= 32) {
+            const uint32_t e = q[lane];
+            const uint32_t rest = static_cast<int>(lane) + 32 < qn ? q[lane + 32] : 0u;
+            __syncwarp();
+            if (static_cast<int>(lane) + 32 < qn) q[lane] = rest;
+            qn -= 32;
+            fix(e);
+            __syncwarp();  // queue moves before the next appends
+        }
     }
 }
 template <class F>
 __device__ __forceinline__ void wq_flush(const uint32_t* q, int qn, F&& fix) {
     __syncwarp();
-    for (int j = static_cast<int>(threadIdx.x & 31); j < qn; j += 32) fix(q[j]);
+    if (static_cast<int>(threadIdx.x & 31u) < qn) fix(q[threadIdx.x & 31u]);
 }
 
 // predicated shared-memory add without the compiler's warp-aggregation scaffolding
@@ -530,9 +553,22 @@ __device__ __forceinline__ void red_shared_add(uint32_t* p, uint32_t v, bool pre
 __device__ __forceinline__ uint32_t plane_word(float g255, int bin) {
     return (__float_as_uint(__fadd_rn(g255, 256.0f)) & 0x7FFFFFu) | (static_cast<uint32_t>(bin) << 23);
 }
+// kMode 2: the 16-bit plane word of t = v nb (unclamped, t >= 0): floor(t 2^F), capped
+// at nb 2^F - 1 (v = 1 gives t = nb, bin nb - 1). For a pixel whose bin is sure,
+// u >> F is that bin (the same fp32 t floored); the others are patched by the fix.
+__device__ __forceinline__ uint32_t plane_u16(const U8Lhe& L, float tu) {
+    return min(__float_as_uint(__fadd_rd(fmaxf(tu, 0.0f), L.u_magic)) & 0x7FFFFFu, L.umax);
+}
+// a plane word whose bin (u >> F) must be b: the nearest word of bin b
+__device__ __forceinline__ uint32_t plane_u16_fix(uint32_t u, int b, int F) {
+    const int cb = static_cast<int>(u >> F);
+    return cb == b ? u : (b < cb ? ((static_cast<uint32_t>(b) << F) | ((1u << F) - 1u)) : (static_cast<uint32_t>(b) << F));
+}
 
-template <bool kPacked>
-__global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
+// kMode: 0 fp32 estimate plane, 1 packed 32-bit plane (bin << 23 | estimate), 2 the
+// 16-bit plane (plane_u16)
+template <int kMode>
+__global__ void __launch_bounds__(kBlock, 4) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
                                                               float* __restrict__ gplane, int rows_per_chunk,
                                                               bool vec) {
     extern __shared__ uint32_t sh[];  // [nx * nb] + one dummy cell, then the warp queues
@@ -565,9 +601,12 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
         L.src.load(p0 + p, cr, cg, cb);
         const int b = bin_d(L.src.gray_d(cr, cg, cb), g.nb);
         atomicAdd(&sh[((x0 + p) / g.tw) * g.nb + b], 1u);
-        if constexpr (kPacked) {  // the exact bin into the plane word (after the warp's stores)
+        if constexpr (kMode == 1) {  // the exact bin into the plane word (after the warp's stores)
             uint32_t* wp = reinterpret_cast<uint32_t*>(gplane) + p0 + p;
             *wp = (*wp & 0x7FFFFFu) | (static_cast<uint32_t>(b) << 23);
+        } else if constexpr (kMode == 2) {
+            uint16_t* wp = reinterpret_cast<uint16_t*>(gplane) + p0 + p;
+            *wp = static_cast<uint16_t>(plane_u16_fix(*wp, b, L.ufrac));
         }
     };
     const uint32_t lane = threadIdx.x & 31u;
@@ -603,9 +642,11 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
             uint32_t run = 0;
             const auto px = [&](int p, int cbase) {
                 bool sure;
-                const int b = L.bin_fast(g255[p], sure);
+                const float tu = __fmul_rn(g255[p], L.nb_over_255);
+                const int b = L.bin_fast_t(tu, sure);
                 const int cell = cbase + b;
-                if constexpr (kPacked) words[p] = plane_word(g255[p], b);  // unsure bins are patched below
+                if constexpr (kMode == 2) words[p] = plane_u16(L, tu);  // unsure bins are patched below
+                else if constexpr (kMode == 1) words[p] = plane_word(g255[p], b);
                 else words[p] = __float_as_uint(g255[p]);
                 slow |= static_cast<uint32_t>(!sure) << p;
                 const bool same = cell == run_cell;
@@ -629,7 +670,21 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
             red_shared_add(&sh[run_cell], run, true);
             // keep the estimate for the apply pass (4 B/px instead of recomputing the gray)
             uint32_t* wplane = reinterpret_cast<uint32_t*>(gplane);
-            if (vec) {
+            if constexpr (kMode == 2) {
+                uint16_t* hplane = reinterpret_cast<uint16_t*>(gplane);
+                if (vec) {
+#pragma unroll
+                    for (int q = 0; q < kGrp / 8; ++q)
+                        reinterpret_cast<uint4*>(hplane + p0)[q] = make_uint4(
+                            __byte_perm(words[8 * q], words[8 * q + 1], 0x5410),
+                            __byte_perm(words[8 * q + 2], words[8 * q + 3], 0x5410),
+                            __byte_perm(words[8 * q + 4], words[8 * q + 5], 0x5410),
+                            __byte_perm(words[8 * q + 6], words[8 * q + 7], 0x5410));
+                } else {
+#pragma unroll
+                    for (int q = 0; q < kGrp; ++q) hplane[p0 + q] = static_cast<uint16_t>(words[q]);
+                }
+            } else if (vec) {
 #pragma unroll
                 for (int q = 0; q < kGrp / 4; ++q)
                     reinterpret_cast<uint4*>(wplane + p0)[q] =
@@ -650,9 +705,167 @@ __global__ void __launch_bounds__(kBlock) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g
                 const float g255 = decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
                                                    static_cast<float>(cb), L.k8);
                 bool sure;
-                const int b = L.bin_fast(g255, sure);
-                if constexpr (kPacked) reinterpret_cast<uint32_t*>(gplane)[p0 + p] = plane_word(g255, b);
+                const float tu = __fmul_rn(g255, L.nb_over_255);
+                const int b = L.bin_fast_t(tu, sure);
+                if constexpr (kMode == 2) reinterpret_cast<uint16_t*>(gplane)[p0 + p] = static_cast<uint16_t>(plane_u16(L, tu));
+                else if constexpr (kMode == 1) reinterpret_cast<uint32_t*>(gplane)[p0 + p] = plane_word(g255, b);
                 else gplane[p0 + p] = g255;
+                if (sure) atomicAdd(&sh[tx * g.nb + b], 1u);
+                else slow |= 1u << p;
+            }
+        }
+        }
+        wq_push(wq, qn, slow, gi, fix);  // rare: pixels next to a bin edge
+    }
+    wq_flush(wq, qn, fix);
+    __syncthreads();
+    uint32_t* gh = hist + (img * g.ntile + static_cast<int64_t>(ty) * g.nx) * g.nb;
+    for (int i = threadIdx.x; i < cells; i += blockDim.x)
+        if (sh[i]) atomicAdd(&gh[i], sh[i]);
+}
+
+// predicated shared-memory add at a shared-window address
+__device__ __forceinline__ void red_shared_at(uint32_t addr, uint32_t v, bool pred) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.add.u32 [%0], %1;\n}" ::"r"(addr),
+                 "r"(v), "r"(static_cast<uint32_t>(pred))
+                 : "memory");
+}
+
+// Histogram pass of the 16-bit plane route. Per pixel: t = v nb from the gray
+// estimate, the bin test on t clamped to [1/2, nb - 1/2] (0 and nb are not bin
+// edges), the plane word from the unclamped t, and the run-merged count: the
+// cell's shared-memory address is formed straight from the bits of
+// fl_rd(t + 2^23) (one LEA; unsure pixels go to a dummy cell and the fp64
+// queue), a run is flushed with one predicated red.shared when the address
+// changes. Group coordinates advance incrementally and a per-column-group table
+// (tile column, "group inside one tile") replaces the divisions per group.
+__global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
+                                                            uint16_t* __restrict__ plane, int rows_per_chunk,
+                                                            bool vec) {
+    extern __shared__ uint32_t sh[];  // [nx * nb] + one dummy cell, the warp queues, the column-group table
+    const int64_t img = blockIdx.z;
+    const int ty = blockIdx.y;
+    const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
+    const int64_t y1 = imin64(imin64(y0 + rows_per_chunk, static_cast<int64_t>(ty + 1) * g.th), g.h);
+    if (y0 >= y1) return;
+    const int cells = g.nx * g.nb;
+    const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
+    uint32_t* wq = sh + cells + 1 + (threadIdx.x >> 5) * kWq;
+    uint32_t* ctab = sh + cells + 1 + (kBlock / 32) * kWq;  // [gpr]: tile column | whole-group flag << 31
+    for (int i = threadIdx.x; i <= cells; i += blockDim.x) sh[i] = 0;
+    for (uint32_t c = threadIdx.x; c < gpr; c += blockDim.x) {
+        const int64_t x0 = static_cast<int64_t>(c) * kGrp;
+        const int64_t tx = x0 / g.tw;
+        ctab[c] = static_cast<uint32_t>(tx) | (x0 + kGrp <= (tx + 1) * g.tw ? 0x80000000u : 0u);
+    }
+    int qn = 0;
+    __syncthreads();
+    const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
+    const int64_t row0 = (img * g.h + y0) * g.w;
+    const uint32_t sh_base = smem_addr(sh);
+    const uint32_t dummy = sh_base + 4u * static_cast<uint32_t>(cells);
+    // address of cell (tx, bin) from bits(fl_rd(t + 2^23)) = 0x4B000000 + bin: LEA(bits, base, 2)
+    const uint32_t nb4 = 4u * static_cast<uint32_t>(g.nb);
+    const uint32_t lea_base = sh_base - (0x4B000000u << 2);
+    const auto fix = [&](uint32_t e) {  // the reference's fp64 bin for a pixel next to a bin edge (rare)
+        const uint32_t gi = e / kGrp, gy = gi / gpr;
+        const int x = static_cast<int>(gi - gy * gpr) * kGrp + static_cast<int>(e % kGrp);
+        const int64_t pp = row0 + static_cast<int64_t>(gy) * g.w + x;
+        uint32_t cr, cg, cb;
+        L.src.load(pp, cr, cg, cb);
+        const int b = bin_d(L.src.gray_d(cr, cg, cb), g.nb);
+        atomicAdd(&sh[(x / g.tw) * g.nb + b], 1u);
+        plane[pp] = static_cast<uint16_t>(plane_u16_fix(plane[pp], b, L.ufrac));  // after the warp's stores
+    };
+    const uint32_t dq = blockDim.x / gpr, dr = blockDim.x - dq * gpr;
+    uint32_t ny_ = threadIdx.x / gpr, nx_ = threadIdx.x - ny_ * gpr;  // the next group
+    const uint32_t lane = threadIdx.x & 31u;
+    U8Group nxt;
+    if (threadIdx.x < ngroups)
+        nxt.load(L.src.rgb, row0 + static_cast<int64_t>(ny_) * g.w + nx_ * kGrp,
+                 static_cast<int>(imin64(kGrp, g.w - static_cast<int64_t>(nx_) * kGrp)), vec);
+    // warp-uniform trip count (the queue uses warp collectives)
+    for (uint32_t gb = threadIdx.x - lane; gb < ngroups; gb += blockDim.x) {
+        const uint32_t gi = gb + lane;
+        uint32_t slow = 0;
+        if (gi < ngroups) {
+        const U8Group grp = nxt;
+        const uint32_t gy = ny_, gx = nx_;
+        nx_ += dr;
+        ny_ += dq;
+        if (nx_ >= gpr) {
+            nx_ -= gpr;
+            ++ny_;
+        }
+        if (gi + blockDim.x < ngroups)  // register prefetch of this thread's next group
+            nxt.load(L.src.rgb, row0 + static_cast<int64_t>(ny_) * g.w + nx_ * kGrp,
+                     static_cast<int>(imin64(kGrp, g.w - static_cast<int64_t>(nx_) * kGrp)), vec);
+        const int x0 = static_cast<int>(gx) * kGrp;
+        const int n = static_cast<int>(imin64(kGrp, g.w - x0));
+        const int64_t p0 = row0 + static_cast<int64_t>(gy) * g.w + x0;
+        const uint32_t ct = ctab[gx];
+        uint32_t tx = ct & 0x7FFFFFFFu;
+        if (n == kGrp) {
+            float g255[kGrp];
+            grp.gray255(L.k8, g255);
+            uint32_t words[kGrp];
+            uint32_t run_addr = dummy, run = 0;
+            const auto px = [&](int p, uint32_t base) {
+                const float tu = __fmul_rn(g255[p], L.nb_over_255);
+                const float t = fminf(fmaxf(tu, 0.5f), L.t_hi);
+                const float tf = __fadd_rd(t, 8388608.0f);
+                const bool sure = fabsf(__fsub_rn(__fsub_rn(t, __fsub_rn(tf, 8388608.0f)), 0.5f)) < L.half_m;
+                words[p] = plane_u16(L, tu);  // unsure bins are patched by the fix
+                slow |= static_cast<uint32_t>(!sure) << p;
+                const uint32_t addr = sure ? base + (__float_as_uint(tf) << 2) : dummy;
+                const bool flush = addr != run_addr;
+                red_shared_at(run_addr, run, flush);
+                run = (flush ? 0u : run) + 1u;
+                run_addr = addr;
+            };
+            if (ct & 0x80000000u) {  // the whole group inside one tile column
+                const uint32_t base = lea_base + tx * nb4;
+#pragma unroll
+                for (int p = 0; p < kGrp; ++p) px(p, base);
+            } else {
+                int next = static_cast<int>(tx + 1) * g.tw;
+#pragma unroll
+                for (int p = 0; p < kGrp; ++p) {
+                    const bool stp = x0 + p >= next;
+                    tx += stp;
+                    next += stp ? g.tw : 0;
+                    px(p, lea_base + tx * nb4);
+                }
+            }
+            red_shared_at(run_addr, run, true);
+            if (vec) {
+#pragma unroll
+                for (int q = 0; q < kGrp / 8; ++q)
+                    reinterpret_cast<uint4*>(plane + p0)[q] =
+                        make_uint4(__byte_perm(words[8 * q], words[8 * q + 1], 0x5410),
+                                   __byte_perm(words[8 * q + 2], words[8 * q + 3], 0x5410),
+                                   __byte_perm(words[8 * q + 4], words[8 * q + 5], 0x5410),
+                                   __byte_perm(words[8 * q + 6], words[8 * q + 7], 0x5410));
+            } else {
+#pragma unroll
+                for (int q = 0; q < kGrp; ++q) plane[p0 + q] = static_cast<uint16_t>(words[q]);
+            }
+        } else {  // row tail of a width that is not a multiple of 16
+            int next = static_cast<int>(tx + 1) * g.tw;
+#pragma unroll 1
+            for (int p = 0; p < n; ++p) {
+                if (x0 + p >= next) {
+                    ++tx;
+                    next += g.tw;
+                }
+                uint32_t cr, cg, cb;  // (a dynamic index into grp.w would spill it to local memory)
+                L.src.load(p0 + p, cr, cg, cb);
+                const float g255 = decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
+                                                   static_cast<float>(cb), L.k8);
+                bool sure;
+                const float tu = __fmul_rn(g255, L.nb_over_255);
+                const int b = L.bin_fast_t(tu, sure);
+                plane[p0 + p] = static_cast<uint16_t>(plane_u16(L, tu));
                 if (sure) atomicAdd(&sh[tx * g.nb + b], 1u);
                 else slow |= 1u << p;
             }
@@ -881,7 +1094,299 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8
         apply_groups<kGray, false, kPacked>(L, toned, gray, g, s, y0, y1, img, quad, sxf, sxo, G, vec, wq);
 }
 
+
+// ------------------------------------------------------------------ apply on the 16-bit plane
+// The hist pass writes u = floor(v nb 2^F) per pixel (2 B/px, plane_u16); the
+// apply pass reads it back instead of 4 B/px of fp32 estimates: 3 + 2 + 2 + 1 =
+// 8 B/px of traffic. v is known to within uhalf = 2^-F / (2 nb) (255 domain:
+// <= 255 / 2^16), which the quantization margins below absorb; the pixels inside
+// them take the fp64 queue. Bands without identity tiles get a blend table
+// pre-scaled by the strength s, offset by 256.5 + (1 - s) uhalf, with the
+// column differences: (s c00 + off, s c01 - s c00, s c10 + off, s c11 - s c10),
+// so per pixel T = fma(wx, d0, a0), B = fma(wx, d1, a1), E = fma(wy, B - T, T)
+// and r' = fma((1 - s) uscale, u, E) = 256.5 + v + s (eq - v): the rounded byte and
+// its distance to the rounding boundary are integer fields of r''s bits.
+struct Apply16 {
+    float uscale, uhalf;  // v255 = (u + 1/2) uscale
+    float oms_us;         // fl((1 - s) uscale)
+    float off;            // 256.5 + (1 - s) uhalf
+    uint32_t mq, mq_ident, mg;  // margins of the toned / identity-tile / gray byte, units of 2^-15
+};
+
+struct Apply16Smem {
+    static __host__ __device__ size_t bytes(int nx, int nb, int64_t w) {
+        return static_cast<size_t>(nx) * nb * 16 + static_cast<size_t>(ApplySmem::wpad(w)) * 8 + kWqBytes;
+    }
+};
+
+// per (image, row band) the table of the band's tile-row pair (j0, j1) = (band,
+// band + 1), or (0, 0) for a single tile row: entry [i0][b] covers the tiles
+// (j0, i0), (j0, i1), (j1, i0), (j1, i1), i1 = min(i0 + 1, nx - 1). One block
+// per (tile column i0, band, image).
+__global__ void __launch_bounds__(kBlock) lhe_table_kernel(LheGeom g, LheBufs s, Apply16 A) {
+    const int col = blockIdx.x, band = blockIdx.y, nband = g.ny > 1 ? g.ny - 1 : 1;
+    const int64_t img = blockIdx.z;
+    const int jrow = g.ny > 1 ? 1 : 0;
+    const float* cf = s.curvef + (img * g.ntile + static_cast<int64_t>(g.ny > 1 ? band : 0) * g.nx) * g.nb;
+    const int rowoff = jrow * g.nx * g.nb;
+    bool any_ident = false;
+    for (int i = threadIdx.x; i < (1 + jrow) * g.nx; i += blockDim.x) any_ident |= cf[i * g.nb] != cf[i * g.nb];
+    const bool ident = __syncthreads_or(any_ident);
+    float4* qt = s.qtab + (img * nband + band) * static_cast<int64_t>(g.nx) * g.nb;
+    const float sf = static_cast<float>(g.strength);
+    const int i0 = col, i1 = g.nx > 1 ? min(i0 + 1, g.nx - 1) : i0;
+    for (int b = threadIdx.x; b < g.nb; b += blockDim.x) {
+        const int i = i0 * g.nb + b;
+        const float c00 = cf[i0 * g.nb + b], c01 = cf[i1 * g.nb + b];
+        const float c10 = cf[rowoff + i0 * g.nb + b], c11 = cf[rowoff + i1 * g.nb + b];
+        if (ident) {
+            qt[i] = make_float4(c00, c01, c10, c11);
+        } else {
+            const float a0 = __fmul_rn(sf, c00), a1 = __fmul_rn(sf, c01);
+            const float b0 = __fmul_rn(sf, c10), b1 = __fmul_rn(sf, c11);
+            qt[i] = make_float4(__fadd_rn(a0, A.off), __fsub_rn(a1, a0), __fadd_rn(b0, A.off), __fsub_rn(b1, b0));
+        }
+    }
+    if (threadIdx.x == 0 && col == 0) s.qident[img * nband + band] = ident;
+    // the per-column tables (image-independent): column x = 16 gc + 4 q + r is
+    // stored at ((q * G + gc) * 4 + r), G = wpad / 16, so the lanes of a warp
+    // (consecutive groups gc) read consecutive 16-byte vectors
+    if (band == 0 && img == 0) {  // split over the nx blocks of (band 0, image 0)
+        const int64_t wp = ApplySmem::wpad(g.w), G = wp / kGrp;
+        for (int64_t x = threadIdx.x + static_cast<int64_t>(col) * blockDim.x; x < wp;
+             x += static_cast<int64_t>(blockDim.x) * g.nx) {
+            const int64_t xc = imin64(x, g.w - 1);
+            const int64_t gc = x / kGrp, q = (x % kGrp) >> 2, r = x & 3;
+            const int64_t at = (q * G + gc) * 4 + r;
+            s.colf[at] = s.xff[xc];
+            s.colo[at] = static_cast<uint32_t>(s.xi[xc]) * static_cast<uint32_t>(g.nb) * 16u;
+        }
+    }
+}
+
+// byte of r' (in [256, 512): mantissa bits 22..15 = floor(r + 1/2)) and the
+// flag "within m of a rounding boundary", from e = bits(r') + m
+__device__ __forceinline__ uint32_t q_byte(uint32_t e) { return (e >> 15) & 255u; }
+__device__ __forceinline__ bool q_unsure(uint32_t e, uint32_t m) { return (e & 0x7FFFu) < 2u * m; }
+
+// kF: the plane's fraction bits when fixed at compile time (8: bins 129..256), else -1
+template <bool kGray, bool kIdent, int kF>
+__device__ __forceinline__ void apply16_groups(const U8Lhe& L, const Apply16& A, uint8_t* __restrict__ toned,
+                                               uint8_t* __restrict__ gray, const LheGeom& g, const LheBufs& s,
+                                               int64_t y0, int64_t y1, int64_t img, const uint8_t* quadb,
+                                               const float* sxf, const uint32_t* sxo, int64_t G, bool vec,
+                                               uint32_t* wq) {
+    const float sf = static_cast<float>(g.strength);
+    const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
+    const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
+    const uint16_t* plane = reinterpret_cast<const uint16_t*>(s.gray255);
+    const int F = kF >= 0 ? kF : L.ufrac;
+    const int64_t rowbase = (img * g.h + y0) * g.w;
+    // group gi = (row gy, column group gx); the thread's groups advance by
+    // blockDim.x: gx += dr, gy += dq (+1 on wrap) instead of a division per group
+    const uint32_t dq = blockDim.x / gpr, dr = blockDim.x - dq * gpr;
+    const auto step = [&](uint32_t& gy, uint32_t& gx) {
+        gx += dr;
+        gy += dq;
+        if (gx >= gpr) {
+            gx -= gpr;
+            ++gy;
+        }
+    };
+    auto load_w = [&](uint32_t gy, uint32_t gx, uint4 (&e)[2]) {
+        const int x0 = static_cast<int>(gx) * kGrp;
+        const uint16_t* src = plane + rowbase + static_cast<int64_t>(gy) * g.w + x0;
+        if (vec) {  // (w % 16 == 0: every group is whole)
+            e[0] = __ldcs(reinterpret_cast<const uint4*>(src));
+            e[1] = __ldcs(reinterpret_cast<const uint4*>(src) + 1);
+        } else {
+            const int n = static_cast<int>(imin64(kGrp, g.w - x0));
+            uint32_t t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                t[q] = (2 * q < n ? static_cast<uint32_t>(src[2 * q]) : 0u) |
+                       (2 * q + 1 < n ? static_cast<uint32_t>(src[2 * q + 1]) << 16 : 0u);
+            e[0] = make_uint4(t[0], t[1], t[2], t[3]);
+            e[1] = make_uint4(t[4], t[5], t[6], t[7]);
+        }
+    };
+    // the reference's fp64 chain for a pixel within a margin (queued, rare):
+    // overwrites the provisional bytes the warp stored
+    const auto fix = [&](uint32_t e) {
+        const uint32_t gi = e / kGrp, gy = gi / gpr;
+        const int p = static_cast<int>(e % kGrp);
+        const int64_t y = y0 + gy;
+        const int x = static_cast<int>(gi - gy * gpr) * kGrp + p;
+        const int64_t pp = (img * g.h + y) * g.w + x;
+        const int j0 = s.yi[y], j1 = g.ny > 1 ? j0 + 1 : 0;
+        uint32_t cr, cg, cb;
+        L.src.load(pp, cr, cg, cb);
+        const double vd = L.src.gray_d(cr, cg, cb);
+        const int b = bin_d(vd, g.nb);
+        const int i0 = s.xi[x], i1 = g.nx > 1 ? i0 + 1 : 0;
+        const int64_t t00 = img * g.ntile + static_cast<int64_t>(j0) * g.nx + i0, t01 = t00 - i0 + i1;
+        const int64_t t10 = img * g.ntile + static_cast<int64_t>(j1) * g.nx + i0, t11 = t10 - i0 + i1;
+        const double c00 = s.ident[t00] ? vd : s.curve[t00 * g.nb + b];
+        const double c01 = s.ident[t01] ? vd : s.curve[t01 * g.nb + b];
+        const double c10 = s.ident[t10] ? vd : s.curve[t10 * g.nb + b];
+        const double c11 = s.ident[t11] ? vd : s.curve[t11 * g.nb + b];
+        toned[pp] = static_cast<uint8_t>(quantize_d(blend_d(vd, c00, c01, c10, c11, s.xf[x], s.yf[y], g.strength)));
+        if constexpr (kGray) gray[pp] = static_cast<uint8_t>(quantize_d(vd));
+    };
+    const uint32_t lane = threadIdx.x & 31u;
+    int qn = 0;
+    uint4 nxt[2];
+    uint32_t ny_ = threadIdx.x / gpr, nx_ = threadIdx.x - ny_ * gpr;  // the next group
+    if (threadIdx.x < ngroups) load_w(ny_, nx_, nxt);
+    // warp-uniform trip count (the queue uses warp collectives)
+    for (uint32_t gb = threadIdx.x - lane; gb < ngroups; gb += blockDim.x) {
+        const uint32_t gi = gb + lane;
+        uint32_t slow = 0;
+        if (gi < ngroups) {
+        const uint32_t gy = ny_, gx = nx_;
+        const uint32_t wd[8] = {nxt[0].x, nxt[0].y, nxt[0].z, nxt[0].w, nxt[1].x, nxt[1].y, nxt[1].z, nxt[1].w};
+        step(ny_, nx_);
+        if (gi + blockDim.x < ngroups) load_w(ny_, nx_, nxt);
+        const int x0 = static_cast<int>(gx) * kGrp;
+        const int64_t p0 = rowbase + static_cast<int64_t>(gy) * g.w + x0;
+        const float wy = s.yff[y0 + gy];  // every row of the block blends the same tile-row pair
+        float wxs[kGrp];
+        uint32_t xos[kGrp];
+#pragma unroll
+        for (int q = 0; q < kGrp / 4; ++q) {
+            const float4 f = reinterpret_cast<const float4*>(sxf)[q * G + gx];
+            const uint4 o = reinterpret_cast<const uint4*>(sxo)[q * G + gx];
+            wxs[4 * q] = f.x;
+            wxs[4 * q + 1] = f.y;
+            wxs[4 * q + 2] = f.z;
+            wxs[4 * q + 3] = f.w;
+            xos[4 * q] = o.x;
+            xos[4 * q + 1] = o.y;
+            xos[4 * q + 2] = o.z;
+            xos[4 * q + 3] = o.w;
+        }
+        uint32_t ot[4] = {0u, 0u, 0u, 0u}, og[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int p = 0; p < kGrp; ++p) {
+            const uint32_t w = wd[p >> 1];
+            // 2^23 + u as a float (u exactly after one FADD) and the table entry's address
+            uint32_t fb, boff;
+            if constexpr (kF == 8) {
+                fb = (p & 1) ? (w >> 16) | 0x4B000000u : (w & 0xFFFFu) | 0x4B000000u;
+                boff = xos[p] + ((p & 1) ? ((w >> 20) & 0xFF0u) : ((w & 0xFF00u) >> 4));
+            } else {
+                const uint32_t u = (p & 1) ? w >> 16 : w & 0xFFFFu;
+                fb = u | 0x4B000000u;
+                boff = xos[p] + ((u >> F) << 4);
+            }
+            const float uf = __fsub_rn(__uint_as_float(fb), 8388608.0f);
+            const float4 cq = *reinterpret_cast<const float4*>(quadb + boff);
+            const float wx = wxs[p];
+            uint32_t e;
+            bool uns;
+            if constexpr (kIdent) {  // raw curves, NaN = identity tile (the pixel's own value)
+                const float v = __fmaf_rn(uf, A.uscale, A.uhalf);
+                const float c00 = cq.x != cq.x ? v : cq.x, c01 = cq.y != cq.y ? v : cq.y;
+                const float c10 = cq.z != cq.z ? v : cq.z, c11 = cq.w != cq.w ? v : cq.w;
+                const float top = __fmaf_rn(wx, __fsub_rn(c01, c00), c00);
+                const float bottom = __fmaf_rn(wx, __fsub_rn(c11, c10), c10);
+                const float eq = __fmaf_rn(wy, __fsub_rn(bottom, top), top);
+                e = __float_as_uint(__fadd_rn(__fmaf_rn(sf, __fsub_rn(eq, v), v), 256.5f)) + A.mq_ident;
+                uns = q_unsure(e, A.mq_ident);
+            } else {
+                const float T = __fmaf_rn(wx, cq.y, cq.x), B = __fmaf_rn(wx, cq.w, cq.z);
+                const float E = __fmaf_rn(wy, __fsub_rn(B, T), T);
+                e = __float_as_uint(__fmaf_rn(A.oms_us, uf, E)) + A.mq;
+                uns = q_unsure(e, A.mq);
+            }
+            ot[p >> 2] |= q_byte(e) << (8 * (p & 3));
+            if constexpr (kGray) {
+                const uint32_t eg = __float_as_uint(__fadd_rn(__fmaf_rn(uf, A.uscale, A.uhalf), 256.5f)) + A.mg;
+                uns = uns || q_unsure(eg, A.mg);
+                og[p >> 2] |= q_byte(eg) << (8 * (p & 3));
+            }
+            slow |= static_cast<uint32_t>(uns) << p;
+        }
+        if (vec) {
+            st_global_cs_v4(toned + p0, make_uint4(ot[0], ot[1], ot[2], ot[3]));
+            if constexpr (kGray) st_global_cs_v4(gray + p0, make_uint4(og[0], og[1], og[2], og[3]));
+        } else {
+            const int n = static_cast<int>(imin64(kGrp, g.w - x0));
+            slow &= (1u << n) - 1u;
+#pragma unroll
+            for (int p = 0; p < kGrp; ++p) {
+                if (p < n) {
+                    toned[p0 + p] = static_cast<uint8_t>(ot[p >> 2] >> (8 * (p & 3)));
+                    if constexpr (kGray) gray[p0 + p] = static_cast<uint8_t>(og[p >> 2] >> (8 * (p & 3)));
+                }
+            }
+        }
+        }
+        wq_push(wq, qn, slow, gi, fix);
+    }
+    wq_flush(wq, qn, fix);
+}
+
+template <bool kGray, int kF>
+__global__ void __launch_bounds__(kBlock, 3) lhe_apply16_kernel(U8Lhe L, Apply16 A, uint8_t* __restrict__ toned,
+                                                             uint8_t* __restrict__ gray, LheGeom g, LheBufs s,
+                                                             int rows_per_chunk, bool vec) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int64_t img = blockIdx.z;
+    // row bands between tile-row centres, as lhe_apply_u8g_kernel
+    const int band = blockIdx.y, nband = g.ny > 1 ? g.ny - 1 : 1;
+    const int64_t lo = band == 0 ? 0 : static_cast<int64_t>(ceil(centre(band, g.th, g.h)));
+    const int64_t hi = band == nband - 1 ? g.h : static_cast<int64_t>(ceil(centre(band + 1, g.th, g.h)));
+    const int64_t y0 = lo + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
+    const int64_t y1 = imin64(y0 + rows_per_chunk, hi);
+    if (y0 >= y1) return;
+    const int64_t wp = ApplySmem::wpad(g.w);
+    const int nq = g.nx * g.nb;
+    uint4* quad = reinterpret_cast<uint4*>(smem);                              // [nx][nb] (lhe_table_kernel)
+    float* sxf = reinterpret_cast<float*>(quad + nq);                          // [wp]
+    uint32_t* sxo = reinterpret_cast<uint32_t*>(sxf + wp);                     // [wp] byte offsets
+    uint32_t* wq = sxo + wp + (threadIdx.x >> 5) * kWq;                        // per-warp queues
+    const uint4* qt = reinterpret_cast<const uint4*>(s.qtab + (img * nband + band) * static_cast<int64_t>(nq));
+    for (int i = threadIdx.x; i < nq; i += blockDim.x) quad[i] = __ldg(qt + i);
+    const int64_t wv = wp / 4;  // 16-byte vectors of each column table
+    for (int64_t i = threadIdx.x; i < wv; i += blockDim.x) {
+        reinterpret_cast<uint4*>(sxf)[i] = __ldg(reinterpret_cast<const uint4*>(s.colf) + i);
+        reinterpret_cast<uint4*>(sxo)[i] = __ldg(reinterpret_cast<const uint4*>(s.colo) + i);
+    }
+    const bool ident = s.qident[img * nband + band] != 0;
+    __syncthreads();
+    const uint8_t* quadb = reinterpret_cast<const uint8_t*>(quad);
+    const int64_t G = wp / kGrp;
+    if (ident)
+        apply16_groups<kGray, true, kF>(L, A, toned, gray, g, s, y0, y1, img, quadb, sxf, sxo, G, vec, wq);
+    else
+        apply16_groups<kGray, false, kF>(L, A, toned, gray, g, s, y0, y1, img, quadb, sxf, sxo, G, vec, wq);
+}
+
 // ------------------------------------------------------------------ driver
+// WG_LHE_PLANE=32: the 4 B/px plane (fp32 estimates / packed words) instead of
+// the 16-bit plane (A/B of the two)
+bool lhe_plane32() {
+    const char* e = std::getenv("WG_LHE_PLANE");
+    return e && e[0] == '3';
+}
+
+Apply16 make_apply16(int nb, int F, double strength) {
+    Apply16 a;
+    const double us = 255.0 / (static_cast<double>(nb) * static_cast<double>(1u << F)), uh = 0.5 * us;
+    a.uscale = static_cast<float>(us);
+    a.uhalf = static_cast<float>(uh);
+    a.oms_us = static_cast<float>((1.0 - strength) * us);
+    a.off = static_cast<float>(256.5 + (1.0 - strength) * uh);
+    // |v_recon - v| <= uh + 1e-4 (estimate 6.1e-5, t rounding, reconstruction);
+    // the blend's own fp32 roundings, curve and weight errors < 4e-4 (255 domain)
+    const double ev = uh + 1e-4;
+    a.mq = static_cast<uint32_t>(std::ceil((4e-4 + (1.0 - strength) * ev) * 32768.0)) + 1;
+    a.mq_ident = static_cast<uint32_t>(std::ceil((4.2e-4 + ev) * 32768.0)) + 1;
+    a.mg = static_cast<uint32_t>(std::ceil((ev + 3e-5) * 32768.0)) + 1;
+    return a;
+}
+
 struct Chunking {
     int rows_per_chunk, chunks;
 };
@@ -1046,8 +1551,17 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
                     static_cast<float>(bins),
                     1.0f / static_cast<float>(bins)};
     const float m = static_cast<float>(kGrayMargin * static_cast<double>(bins));
-    const U8Lhe L{src, make_u8_consts(static_cast<float>(beta_r), static_cast<float>(beta_k)),
-                  static_cast<float>(bins) / 255.0f, 0.5f - m, static_cast<float>(bins) - 0.5f};
+    int kb = 1;
+    while ((int64_t(1) << kb) < bins) ++kb;  // 2^kb >= bins
+    const int F = kb <= 16 ? 16 - kb : 0;
+    const U8Lhe L{src,
+                  make_u8_consts(static_cast<float>(beta_r), static_cast<float>(beta_k)),
+                  static_cast<float>(bins) / 255.0f,
+                  0.5f - m,
+                  static_cast<float>(bins) - 0.5f,
+                  std::ldexp(1.0f, 7 + kb),
+                  F,
+                  static_cast<uint32_t>(bins) * (1u << F) - 1u};
     // 16-pixel groups load/store 16-byte vectors when every row starts aligned
     const bool vec = width % 16 == 0 && (reinterpret_cast<uintptr_t>(rgb) & 15) == 0 &&
                      (reinterpret_cast<uintptr_t>(toned) & 15) == 0 &&
@@ -1055,24 +1569,36 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     rc = lhe_begin(g, b, st);
     if (rc != WG_OK) return rc;
     const Chunking c = chunking(g);
-    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4 + kWqBytes;  // + the dummy cell, warp queues
-    const size_t asmem = ApplySmem::bytes(g.nx, g.nb, g.w);
+    // + the dummy cell, warp queues, column-group table
+    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4 + kWqBytes + ApplySmem::wpad(g.w) / kGrp * 4;
+    const bool p32 = lhe_plane32();
+    const size_t asmem = p32 ? ApplySmem::bytes(g.nx, g.nb, g.w) : Apply16Smem::bytes(g.nx, g.nb, g.w);
     // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact); the
     // group apply reads the gray plane the group hist writes, so both or neither
     // (the per-warp queue entries are group * 16 + pixel within one row chunk: < 2^32)
     const bool group_ok = bins <= 65536 && hsmem <= kHistSmemCap && asmem <= kApplySmemCap &&
+                          g.ny <= 65535 && g.nx <= 65535 &&  // grid dimensions of the hist / table / apply grids
                           static_cast<int64_t>(c.rows_per_chunk) * ApplySmem::wpad(g.w) < (int64_t(1) << 32) &&
-                          static_cast<int64_t>(g.nx) * g.nb <= 65536;  // u16 column offsets i0 * nb
+                          (!p32 || static_cast<int64_t>(g.nx) * g.nb <= 65536);  // u16 column offsets i0 * nb
     const bool packed = bins <= 512;  // the plane word carries the bin (9 bits)
     if (group_ok) {
-        auto hk = packed ? lhe_hist_u8g_kernel<true> : lhe_hist_u8g_kernel<false>;
-        if (hsmem > 48 * 1024)
+        auto hk = packed ? lhe_hist_u8g_kernel<1> : lhe_hist_u8g_kernel<0>;
+        if (hsmem > 48 * 1024) {
             cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hsmem));
+            cudaFuncSetAttribute(lhe_hist16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(hsmem));
+        }
         per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
             U8Lhe Li = L;
             Li.src.advance(i0 * g.h * g.w);
-            hk<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, hsmem, st>>>(
-                Li, gi, b.hist + i0 * g.ntile * g.nb, b.gray255 + i0 * g.h * g.w, c.rows_per_chunk, vec);
+            const dim3 hgrid(c.chunks, g.ny, static_cast<unsigned>(gi.nimg));
+            if (p32)
+                hk<<<hgrid, kBlock, hsmem, st>>>(Li, gi, b.hist + i0 * g.ntile * g.nb, b.gray255 + i0 * g.h * g.w,
+                                                 c.rows_per_chunk, vec);
+            else
+                lhe_hist16_kernel<<<hgrid, kBlock, hsmem, st>>>(
+                    Li, gi, b.hist + i0 * g.ntile * g.nb, reinterpret_cast<uint16_t*>(b.gray255 + i0 * g.h * g.w),
+                    c.rows_per_chunk, vec);
         });
     } else {
         lhe_hist(src, g, b, st);
@@ -1081,8 +1607,14 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     if (group_ok) {
         auto kern = gray_or_null ? (packed ? lhe_apply_u8g_kernel<true, true> : lhe_apply_u8g_kernel<true, false>)
                                  : (packed ? lhe_apply_u8g_kernel<false, true> : lhe_apply_u8g_kernel<false, false>);
-        if (asmem > 48 * 1024)
+        auto kern16 = F == 8 ? (gray_or_null ? lhe_apply16_kernel<true, 8> : lhe_apply16_kernel<false, 8>)
+                             : (gray_or_null ? lhe_apply16_kernel<true, -1> : lhe_apply16_kernel<false, -1>);
+        const Apply16 A16 = make_apply16(static_cast<int>(bins), F, strength);
+        const int nband = g.ny > 1 ? g.ny - 1 : 1;
+        if (asmem > 48 * 1024) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(asmem));
+            cudaFuncSetAttribute(kern16, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(asmem));
+        }
         per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
             U8Lhe Li = L;
             Li.src.advance(i0 * g.h * g.w);
@@ -1092,10 +1624,18 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
             bi.ident += i0 * g.ntile;
             const int64_t off = i0 * g.h * g.w;
             bi.gray255 += off;
+            bi.qtab += i0 * nband * static_cast<int64_t>(g.nx) * g.nb;
+            bi.qident += i0 * nband;
+            if (!p32) lhe_table_kernel<<<dim3(g.nx, nband, static_cast<unsigned>(gi.nimg)), kBlock, 0, st>>>(gi, bi, A16);
             // row bands between tile-row centres are at most ~1.5 tile heights (+2 rows)
             const int achunks = static_cast<int>((2LL * g.th + 2 + c.rows_per_chunk - 1) / c.rows_per_chunk);
-            kern<<<dim3(achunks, g.ny > 1 ? g.ny - 1 : 1, static_cast<unsigned>(gi.nimg)), kBlock, asmem, st>>>(
-                Li, toned + off, gray_or_null ? gray_or_null + off : nullptr, gi, bi, c.rows_per_chunk, vec);
+            const dim3 agrid(achunks, g.ny > 1 ? g.ny - 1 : 1, static_cast<unsigned>(gi.nimg));
+            if (p32)
+                kern<<<agrid, kBlock, asmem, st>>>(Li, toned + off, gray_or_null ? gray_or_null + off : nullptr, gi,
+                                                   bi, c.rows_per_chunk, vec);
+            else
+                kern16<<<agrid, kBlock, asmem, st>>>(Li, A16, toned + off, gray_or_null ? gray_or_null + off : nullptr,
+                                                     gi, bi, c.rows_per_chunk, vec);
         });
     } else {
         lhe_apply_u8_kernel<<<apply_grid(g), kBlock, 0, st>>>(src, toned, gray_or_null, g, b);

@@ -2,7 +2,7 @@
 against the default decolor kernel on the C3 batch (256 Voronoi 4K frames,
 device-generated), CUDA events.
 
-    python scripts/ab_tone.py [--op tone|decolor] [--images 256] [--iters 20] [--rounds 3]
+    python scripts/ab_tone.py [--op tone|decolor|tone_exact|local] [--images 256] [--iters 20] [--rounds 3]
         [--sleep 2] [--configs "ROUTE=linear;GRID=20"]
 
 Each config sets WG_TONE_ROUTE / WG_LDG_GRID_PER_SM for
@@ -25,7 +25,8 @@ import torch  # noqa: E402
 import paper_2108_13656_b200 as wg  # noqa: E402
 from paper_2108_13656_b200 import synth  # noqa: E402
 
-KEYS = {"GRID": "WG_LDG_GRID_PER_SM", "ROUTE": "WG_TONE_ROUTE", "XK": "WG_TONE_EXACT_KERNEL"}
+KEYS = {"GRID": "WG_LDG_GRID_PER_SM", "ROUTE": "WG_TONE_ROUTE", "XK": "WG_TONE_EXACT_KERNEL",
+        "LP": "WG_LHE_PLANE"}
 
 
 def main():
@@ -35,15 +36,24 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--configs", default="ROUTE=linear")
-    ap.add_argument("--op", default="tone", choices=("tone", "decolor", "tone_exact"))
+    ap.add_argument("--op", default="tone", choices=("tone", "decolor", "tone_exact", "local"))
     ap.add_argument("--sleep", type=float, default=0.0)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     wl = synth.WORKLOADS[args.workload]
     rgb = synth.make_batch(wl, dev, n_images=args.images)
     out = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=dev)
+    img4 = rgb.view(args.images, wl.height, wl.width, 3)
+    grid = wg.LocalHistogramGrid.for_image(wl.width, wl.height)
+    scratch = None
+    if args.op == "local":
+        scratch = torch.empty(int(wg._lib.load().wg_lhe_scratch_bytes(args.images, wl.height, wl.width, grid.tile_w,
+                                                                      grid.tile_h, grid.bins)),
+                              dtype=torch.uint8, device=dev)
     op = {"tone": lambda: wg.decolor_tone(rgb, out=out), "decolor": lambda: wg.decolor(rgb, out=out),
-          "tone_exact": lambda: wg.decolor_tone(rgb, out=out, exact=True)}[args.op]
+          "tone_exact": lambda: wg.decolor_tone(rgb, out=out, exact=True),
+          "local": lambda: wg.decolor_tone_local(img4, grid=grid, scratch=scratch,
+                                                 out=out.view(args.images, wl.height, wl.width))}[args.op]
     tone_ref = op().clone()
     npx = out.numel()
     configs = [dict(kv.split("=") for kv in c.split(",") if kv) for c in args.configs.split(";")]
