@@ -724,11 +724,11 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist_u8g_kernel(U8Lhe L, LheGeo
         if (sh[i]) atomicAdd(&gh[i], sh[i]);
 }
 
-// predicated shared-memory add at a shared-window address
-__device__ __forceinline__ void red_shared_at(uint32_t addr, uint32_t v, bool pred) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.add.u32 [%0], %1;\n}" ::"r"(addr),
-                 "r"(v), "r"(static_cast<uint32_t>(pred))
-                 : "memory");
+// shared-memory add at a shared-window address (unconditional: the caller
+// points the adds it does not want at a per-lane scratch cell, which costs less
+// than the branch ptxas builds around a predicated atomic)
+__device__ __forceinline__ void red_shared_at(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 
 // Histogram pass of the 16-bit plane route. Per pixel: t = v nb from the gray
@@ -742,7 +742,8 @@ __device__ __forceinline__ void red_shared_at(uint32_t addr, uint32_t v, bool pr
 __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
                                                             uint16_t* __restrict__ plane, int rows_per_chunk,
                                                             bool vec) {
-    extern __shared__ uint32_t sh[];  // [nx * nb] + one dummy cell, the warp queues, the column-group table
+    // [nx * nb] + one dummy cell, the warp queues, the column-group table, 32 per-lane scratch cells
+    extern __shared__ uint32_t sh[];
     const int64_t img = blockIdx.z;
     const int ty = blockIdx.y;
     const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
@@ -752,6 +753,7 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
     const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
     uint32_t* wq = sh + cells + 1 + (threadIdx.x >> 5) * kWq;
     uint32_t* ctab = sh + cells + 1 + (kBlock / 32) * kWq;  // [gpr]: tile column | whole-group flag << 31
+    const uint32_t lane_cell = smem_addr(ctab + gpr + (threadIdx.x & 31u));
     for (int i = threadIdx.x; i <= cells; i += blockDim.x) sh[i] = 0;
     for (uint32_t c = threadIdx.x; c < gpr; c += blockDim.x) {
         const int64_t x0 = static_cast<int64_t>(c) * kGrp;
@@ -819,8 +821,8 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
                 slow |= static_cast<uint32_t>(!sure) << p;
                 const uint32_t addr = sure ? base + (__float_as_uint(tf) << 2) : dummy;
                 const bool flush = addr != run_addr;
-                red_shared_at(run_addr, run, flush);
-                run = (flush ? 0u : run) + 1u;
+                red_shared_at(flush ? run_addr : lane_cell, run);
+                run = flush ? 1u : run + 1u;
                 run_addr = addr;
             };
             if (ct & 0x80000000u) {  // the whole group inside one tile column
@@ -837,7 +839,7 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
                     px(p, lea_base + tx * nb4);
                 }
             }
-            red_shared_at(run_addr, run, true);
+            red_shared_at(run_addr, run);
             if (vec) {
 #pragma unroll
                 for (int q = 0; q < kGrp / 8; ++q)
@@ -1115,7 +1117,7 @@ struct Apply16 {
 
 struct Apply16Smem {
     static __host__ __device__ size_t bytes(int nx, int nb, int64_t w) {
-        return static_cast<size_t>(nx) * nb * 16 + static_cast<size_t>(ApplySmem::wpad(w)) * 8 + kWqBytes;
+        return static_cast<size_t>(nx) * nb * 16 + static_cast<size_t>(ApplySmem::wpad(w)) * 8 + kWqBytes + 16;
     }
 };
 
@@ -1162,6 +1164,12 @@ __global__ void __launch_bounds__(kBlock) lhe_table_kernel(LheGeom g, LheBufs s,
             s.colo[at] = static_cast<uint32_t>(s.xi[xc]) * static_cast<uint32_t>(g.nb) * 16u;
         }
     }
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_last_lhe() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 
 // byte of r' (in [256, 512): mantissa bits 22..15 = floor(r + 1/2)) and the
@@ -1236,8 +1244,12 @@ __device__ __forceinline__ void apply16_groups(const U8Lhe& L, const Apply16& A,
     const uint32_t lane = threadIdx.x & 31u;
     int qn = 0;
     uint4 nxt[2];
+    float wyn = 0.0f;  // the next group's row weight
     uint32_t ny_ = threadIdx.x / gpr, nx_ = threadIdx.x - ny_ * gpr;  // the next group
-    if (threadIdx.x < ngroups) load_w(ny_, nx_, nxt);
+    if (threadIdx.x < ngroups) {
+        load_w(ny_, nx_, nxt);
+        wyn = s.yff[y0 + ny_];
+    }
     // warp-uniform trip count (the queue uses warp collectives)
     for (uint32_t gb = threadIdx.x - lane; gb < ngroups; gb += blockDim.x) {
         const uint32_t gi = gb + lane;
@@ -1245,43 +1257,38 @@ __device__ __forceinline__ void apply16_groups(const U8Lhe& L, const Apply16& A,
         if (gi < ngroups) {
         const uint32_t gy = ny_, gx = nx_;
         const uint32_t wd[8] = {nxt[0].x, nxt[0].y, nxt[0].z, nxt[0].w, nxt[1].x, nxt[1].y, nxt[1].z, nxt[1].w};
+        const float wy = wyn;  // every row of the block blends the same tile-row pair
         step(ny_, nx_);
-        if (gi + blockDim.x < ngroups) load_w(ny_, nx_, nxt);
+        if (gi + blockDim.x < ngroups) {
+            load_w(ny_, nx_, nxt);
+            wyn = s.yff[y0 + ny_];
+        }
         const int x0 = static_cast<int>(gx) * kGrp;
         const int64_t p0 = rowbase + static_cast<int64_t>(gy) * g.w + x0;
-        const float wy = s.yff[y0 + gy];  // every row of the block blends the same tile-row pair
-        float wxs[kGrp];
-        uint32_t xos[kGrp];
-#pragma unroll
-        for (int q = 0; q < kGrp / 4; ++q) {
-            const float4 f = reinterpret_cast<const float4*>(sxf)[q * G + gx];
-            const uint4 o = reinterpret_cast<const uint4*>(sxo)[q * G + gx];
-            wxs[4 * q] = f.x;
-            wxs[4 * q + 1] = f.y;
-            wxs[4 * q + 2] = f.z;
-            wxs[4 * q + 3] = f.w;
-            xos[4 * q] = o.x;
-            xos[4 * q + 1] = o.y;
-            xos[4 * q + 2] = o.z;
-            xos[4 * q + 3] = o.w;
-        }
         uint32_t ot[4] = {0u, 0u, 0u, 0u}, og[4] = {0u, 0u, 0u, 0u};
+        float4 f;
+        uint4 o;
 #pragma unroll
         for (int p = 0; p < kGrp; ++p) {
+            if ((p & 3) == 0) {  // the quad's blend fractions and table offsets, loaded where used
+                f = reinterpret_cast<const float4*>(sxf)[(p >> 2) * G + gx];
+                o = reinterpret_cast<const uint4*>(sxo)[(p >> 2) * G + gx];
+            }
+            const uint32_t xo = (p & 3) == 0 ? o.x : (p & 3) == 1 ? o.y : (p & 3) == 2 ? o.z : o.w;
+            const float wx = (p & 3) == 0 ? f.x : (p & 3) == 1 ? f.y : (p & 3) == 2 ? f.z : f.w;
             const uint32_t w = wd[p >> 1];
             // 2^23 + u as a float (u exactly after one FADD) and the table entry's address
             uint32_t fb, boff;
             if constexpr (kF == 8) {
                 fb = (p & 1) ? (w >> 16) | 0x4B000000u : (w & 0xFFFFu) | 0x4B000000u;
-                boff = xos[p] + ((p & 1) ? ((w >> 20) & 0xFF0u) : ((w & 0xFF00u) >> 4));
+                boff = xo + ((p & 1) ? ((w >> 20) & 0xFF0u) : ((w & 0xFF00u) >> 4));
             } else {
                 const uint32_t u = (p & 1) ? w >> 16 : w & 0xFFFFu;
                 fb = u | 0x4B000000u;
-                boff = xos[p] + ((u >> F) << 4);
+                boff = xo + ((u >> F) << 4);
             }
             const float uf = __fsub_rn(__uint_as_float(fb), 8388608.0f);
             const float4 cq = *reinterpret_cast<const float4*>(quadb + boff);
-            const float wx = wxs[p];
             uint32_t e;
             bool uns;
             if constexpr (kIdent) {  // raw curves, NaN = identity tile (the pixel's own value)
@@ -1346,15 +1353,22 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply16_kernel(U8Lhe L, Apply16
     float* sxf = reinterpret_cast<float*>(quad + nq);                          // [wp]
     uint32_t* sxo = reinterpret_cast<uint32_t*>(sxf + wp);                     // [wp] byte offsets
     uint32_t* wq = sxo + wp + (threadIdx.x >> 5) * kWq;                        // per-warp queues
-    const uint4* qt = reinterpret_cast<const uint4*>(s.qtab + (img * nband + band) * static_cast<int64_t>(nq));
-    for (int i = threadIdx.x; i < nq; i += blockDim.x) quad[i] = __ldg(qt + i);
-    const int64_t wv = wp / 4;  // 16-byte vectors of each column table
-    for (int64_t i = threadIdx.x; i < wv; i += blockDim.x) {
-        reinterpret_cast<uint4*>(sxf)[i] = __ldg(reinterpret_cast<const uint4*>(s.colf) + i);
-        reinterpret_cast<uint4*>(sxo)[i] = __ldg(reinterpret_cast<const uint4*>(s.colo) + i);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sxo + wp + (kBlock / 32) * kWq);
+    // the band's blend table and the column tables: three bulk copies (TMA), no
+    // register round trip (the register-staged copy was ~11% of the kernel's stalls)
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+        const uint32_t tb = static_cast<uint32_t>(nq) * 16u, cb = static_cast<uint32_t>(wp) * 4u;
+        const uint64_t pol = l2_policy_evict_last_lhe();
+        mbar_arrive_expect_tx(bar, tb + 2u * cb);
+        bulk_g2s(quad, s.qtab + (img * nband + band) * static_cast<int64_t>(nq), tb, bar, pol);
+        bulk_g2s(sxf, s.colf, cb, bar, pol);
+        bulk_g2s(sxo, s.colo, cb, bar, pol);
     }
     const bool ident = s.qident[img * nband + band] != 0;
-    __syncthreads();
+    __syncthreads();  // the barrier's initialisation before anyone waits on it
+    mbar_wait(bar, 0);
     const uint8_t* quadb = reinterpret_cast<const uint8_t*>(quad);
     const int64_t G = wp / kGrp;
     if (ident)
@@ -1570,7 +1584,7 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     if (rc != WG_OK) return rc;
     const Chunking c = chunking(g);
     // + the dummy cell, warp queues, column-group table
-    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4 + kWqBytes + ApplySmem::wpad(g.w) / kGrp * 4;
+    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4 + kWqBytes + ApplySmem::wpad(g.w) / kGrp * 4 + 128;
     const bool p32 = lhe_plane32();
     const size_t asmem = p32 ? ApplySmem::bytes(g.nx, g.nb, g.w) : Apply16Smem::bytes(g.nx, g.nb, g.w);
     // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact); the

@@ -38,7 +38,10 @@ def main():
     ap.add_argument("--configs", default="ROUTE=linear")
     ap.add_argument("--op", default="tone", choices=("tone", "decolor", "tone_exact", "local"))
     ap.add_argument("--sleep", type=float, default=0.0)
+    ap.add_argument("--lib", default=None, help="load this build of the library (cross-build A/B)")
     args = ap.parse_args()
+    if args.lib:
+        wg._lib.load(args.lib)
     dev = torch.device("cuda", 0)
     wl = synth.WORKLOADS[args.workload]
     rgb = synth.make_batch(wl, dev, n_images=args.images)
