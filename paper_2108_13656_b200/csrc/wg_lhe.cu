@@ -478,6 +478,7 @@ struct U8Group {
 struct U8Lhe {
     SrcU8 src;
     U8Consts k8;
+    U8Consts kt;  // k8 with inv_c4sq scaled by (255 / nb)^2: the same estimate times nb / 255, i.e. t = v nb
     float nb_over_255;  // fl(nb / 255)
     float half_m;       // 0.5 - m, m = 1e-6 nb the margin in t = v * nb
     float t_hi;         // nb - 0.5
@@ -558,6 +559,10 @@ __device__ __forceinline__ uint32_t plane_word(float g255, int bin) {
 // u >> F is that bin (the same fp32 t floored); the others are patched by the fix.
 __device__ __forceinline__ uint32_t plane_u16(const U8Lhe& L, float tu) {
     return min(__float_as_uint(__fadd_rd(fmaxf(tu, 0.0f), L.u_magic)) & 0x7FFFFFu, L.umax);
+}
+// the same for an estimate known to be >= 0 (decolor_fast of bytes: T >= 0, rsqrt > 0)
+__device__ __forceinline__ uint32_t plane_u16_nn(const U8Lhe& L, float tu) {
+    return min(__float_as_uint(__fadd_rd(tu, L.u_magic)) & 0x7FFFFFu, L.umax);
 }
 // a plane word whose bin (u >> F) must be b: the nearest word of bin b
 __device__ __forceinline__ uint32_t plane_u16_fix(uint32_t u, int b, int F) {
@@ -808,16 +813,16 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
         const uint32_t ct = ctab[gx];
         uint32_t tx = ct & 0x7FFFFFFFu;
         if (n == kGrp) {
-            float g255[kGrp];
-            grp.gray255(L.k8, g255);
+            float tv[kGrp];
+            grp.gray255(L.kt, tv);  // t = v nb directly (the scale folded into the constants)
             uint32_t words[kGrp];
             uint32_t run_addr = dummy, run = 0;
             const auto px = [&](int p, uint32_t base) {
-                const float tu = __fmul_rn(g255[p], L.nb_over_255);
+                const float tu = tv[p];
                 const float t = fminf(fmaxf(tu, 0.5f), L.t_hi);
                 const float tf = __fadd_rd(t, 8388608.0f);
                 const bool sure = fabsf(__fsub_rn(__fsub_rn(t, __fsub_rn(tf, 8388608.0f)), 0.5f)) < L.half_m;
-                words[p] = plane_u16(L, tu);  // unsure bins are patched by the fix
+                words[p] = plane_u16_nn(L, tu);  // unsure bins are patched by the fix
                 slow |= static_cast<uint32_t>(!sure) << p;
                 const uint32_t addr = sure ? base + (__float_as_uint(tf) << 2) : dummy;
                 const bool flush = addr != run_addr;
@@ -1392,9 +1397,10 @@ Apply16 make_apply16(int nb, int F, double strength) {
     a.uhalf = static_cast<float>(uh);
     a.oms_us = static_cast<float>((1.0 - strength) * us);
     a.off = static_cast<float>(256.5 + (1.0 - strength) * uh);
-    // |v_recon - v| <= uh + 1e-4 (estimate 6.1e-5, t rounding, reconstruction);
-    // the blend's own fp32 roundings, curve and weight errors < 4e-4 (255 domain)
-    const double ev = uh + 1e-4;
+    // |v_recon - v| <= uh + 1.5e-4 (estimate <= 255 * 3.6e-7 = 9.2e-5 with the t scale
+    // folded into its constants, reconstruction 1.5e-5); the blend's own fp32
+    // roundings, curve and weight errors < 4e-4 (255 domain)
+    const double ev = uh + 1.5e-4;
     a.mq = static_cast<uint32_t>(std::ceil((4e-4 + (1.0 - strength) * ev) * 32768.0)) + 1;
     a.mq_ident = static_cast<uint32_t>(std::ceil((4.2e-4 + ev) * 32768.0)) + 1;
     a.mg = static_cast<uint32_t>(std::ceil((ev + 3e-5) * 32768.0)) + 1;
@@ -1568,8 +1574,12 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     int kb = 1;
     while ((int64_t(1) << kb) < bins) ++kb;  // 2^kb >= bins
     const int F = kb <= 16 ? 16 - kb : 0;
+    U8Consts kt = make_u8_consts(static_cast<float>(beta_r), static_cast<float>(beta_k));
+    kt.inv_c4sq = static_cast<float>(3.0 / static_cast<double>(static_cast<float>(beta_k)) * (255.0 / bins) *
+                                     (255.0 / bins));
     const U8Lhe L{src,
                   make_u8_consts(static_cast<float>(beta_r), static_cast<float>(beta_k)),
+                  kt,
                   static_cast<float>(bins) / 255.0f,
                   0.5f - m,
                   static_cast<float>(bins) - 0.5f,
