@@ -719,7 +719,7 @@ def run_methods(wg, torch, rgb, out, n_img, wl, stream, iters: int = 5):
     """
     grid = wg.LocalHistogramGrid.for_image(wl.width, wl.height)
     # at most ~2.2 Gpx (all of C3; 66 frames of C5): the local tone map's scratch
-    # holds a 4 B/px gray plane and the extractors allocate their outputs
+    # holds a 2 B/px plane and the extractors allocate their outputs
     n_img = min(n_img, max(1, 2_200_000_000 // wl.pix_per_image))
     rgb = rgb[:n_img]
     out = out[:n_img]

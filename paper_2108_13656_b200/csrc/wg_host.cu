@@ -625,18 +625,16 @@ extern "C" int wg_host_metric_counts_f64(const double* rgb, const double* gray, 
     const int stride = ntau + 1;
     std::vector<unsigned long long> hist(static_cast<size_t>(stride * stride), 0ull);
     int rc = on_device(device, [&](cudaStream_t st) {
-        const size_t b_rgb = 0, b_gray = 0;  // the host computes (L*, a*, b*, 100 g) itself (metric_hist_host_lab)
+        // (the host computes (L*, a*, b*, 100 g) itself: metric_hist_host_lab)
         const size_t b_pairs = pair_i ? align256(static_cast<size_t>(npairs) * 8) : 0;
         const size_t b_hist = align256(hist.size() * 8);
         const size_t b_scratch = wg_metric_scratch_bytes(npix);
         const size_t b_taus = 256;
         uint8_t* d = nullptr;
-        const size_t total = b_rgb + b_gray + 2 * b_pairs + b_hist + b_scratch + b_taus;
+        const size_t total = 2 * b_pairs + b_hist + b_scratch + b_taus;
         cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d), total, st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(metric)");
         uint8_t* p = d;
-        double* d_rgb = reinterpret_cast<double*>(p); p += b_rgb;
-        double* d_gray = reinterpret_cast<double*>(p); p += b_gray;
         int64_t* d_pi = pair_i ? reinterpret_cast<int64_t*>(p) : nullptr; p += b_pairs;
         int64_t* d_pj = pair_i ? reinterpret_cast<int64_t*>(p) : nullptr; p += b_pairs;
         unsigned long long* d_hist = reinterpret_cast<unsigned long long*>(p); p += b_hist;
@@ -648,8 +646,6 @@ extern "C" int wg_host_metric_counts_f64(const double* rgb, const double* gray, 
                 if (ee != cudaSuccess) r = cuda_fail(ee, "cudaMemcpyAsync H2D");
             }
         };
-        (void)d_rgb;
-        (void)d_gray;
         if (pair_i) {
             h2d(d_pi, pair_i, static_cast<size_t>(npairs) * 8);
             h2d(d_pj, pair_j, static_cast<size_t>(npairs) * 8);

@@ -18,12 +18,17 @@
 //   4. apply   per pixel the four neighbouring tile curves at the pixel's bin,
 //              blended bilinearly and mixed with the identity by `strength`.
 //
-// uint8 kernels work on 16-pixel groups inside one row (three 128-bit loads
-// when rows are 16-byte aligned) with the packed MUFU gray estimate of the
-// decolor kernel (decolor_fast_x2, |error| <= 2.4e-7 over all byte colours:
-// scripts/margin_probe.cu); the histogram merges runs of equal cells before
-// its shared-memory atomics, and the apply pass stages the (at most three)
-// tile rows of fp32 curves and the per-column tables in shared memory.
+// The fused uint8 route (bins <= 65536) runs five kernels per batch:
+// lhe_axis_kernel, lhe_hist16_kernel (RGB -> per-tile counts + a 16-bit plane
+// word per pixel, 3 + 2 B/px), lhe_curve_kernel, lhe_table_kernel (one blend
+// table per image x row band: the four tile curves each pixel of the band
+// blends, pre-scaled) and lhe_apply16_kernel (plane -> toned byte, 2 + 1 B/px):
+// 8 B/px of HBM traffic. Both per-pixel kernels work on 16-pixel groups inside
+// one row (128-bit loads when rows are 16-byte aligned); the hist uses the
+// packed MUFU gray estimate of the decolor kernel (decolor_fast_x2, |error| <=
+// 2.4e-7 over all byte colours: scripts/margin_probe.cu) and merges runs of
+// equal cells before its shared-memory adds; the apply stages its band's table
+// with bulk copies (TMA) and does one 128-bit shared load per pixel.
 //
 // The fp64 drop-in evaluates every step with the reference's operations and
 // order (no contraction), so it is bit-identical to the NumPy code. The fused
@@ -50,7 +55,6 @@ constexpr int kBlock = 256;
 // |decolor_acc(k/255) - decolor_f64(k/255)| over all 2^24 byte colours is
 // < 2.5e-7 (tests/test_gpu_lhe.py pins it); margins below leave >= 4x headroom.
 constexpr float kGrayMargin = 1e-6f;  // bin edges (gray domain)
-constexpr float kGray255Margin = 255.0f * kGrayMargin;  // the same in the 0..255 domain
 // (bins of the uint8 route need margin_t = kGrayMargin * nb < 0.5, i.e. nb < 500000)
 constexpr int kGrp = 16;                                // pixels per thread group (48 input bytes)
 // quantization margin in the x = 255 v + 0.5 domain. Error budget of the uint8
@@ -80,7 +84,7 @@ struct LheBufs {
     int32_t* yi;  // [h]
     double* yf;
     float* yff;
-    float* gray255;  // [nimg][h][w] uint8 route: the hist pass's 255 * gray estimate, reused by apply
+    uint16_t* plane;  // [nimg][h][w] uint8 route: the hist pass's 16-bit plane words (plane_u16), read by apply
     // uint8 route (bins <= 65536), built once per call for the apply blocks:
     float4* qtab;    // [nimg][nband][nx * nb] blend table of each row band (lhe_table_kernel)
     uint8_t* qident; // [nimg][nband] the band's table holds an identity tile (raw curves)
@@ -110,8 +114,8 @@ size_t layout(const LheGeom& g, uint8_t* base, LheBufs* b) {
     t.yi = reinterpret_cast<int32_t*>(take(g.h * 4));
     t.yf = reinterpret_cast<double*>(take(g.h * 8));
     t.yff = reinterpret_cast<float*>(take(g.h * 4));
-    t.gray255 = reinterpret_cast<float*>(take(static_cast<size_t>(g.nimg) * g.h * g.w * 4));
     const bool u8 = g.nb <= 65536;
+    t.plane = reinterpret_cast<uint16_t*>(take(u8 ? static_cast<size_t>(g.nimg) * g.h * g.w * 2 : 0));
     const size_t nband = g.ny > 1 ? g.ny - 1 : 1, wpad = (g.w + 15) / 16 * 16;
     t.qtab = reinterpret_cast<float4*>(take(u8 ? static_cast<size_t>(g.nimg) * nband * g.nx * g.nb * 16 : 0));
     t.qident = take(u8 ? static_cast<size_t>(g.nimg) * nband : 0);
@@ -492,9 +496,6 @@ struct U8Lhe {
     // |t - v nb| <= (2.4e-7 + 6e-8 + 6e-8) nb < m. t is clamped to [0.5, nb - 0.5]
     // (0 and nb are not bin edges), floor(t) taken as the low bits of
     // fl_rd(t + 2^23) (no F2I); `sure` is false within m of an inner edge.
-    __device__ __forceinline__ int bin_fast(float g255, bool& sure) const {
-        return bin_fast_t(__fmul_rn(g255, nb_over_255), sure);
-    }
     __device__ __forceinline__ int bin_fast_t(float tu, bool& sure) const {
         const float t = fminf(fmaxf(tu, 0.5f), t_hi);
         const float tf = __fadd_rd(t, 8388608.0f);
@@ -539,194 +540,16 @@ __device__ __forceinline__ void wq_flush(const uint32_t* q, int qn, F&& fix) {
     if (static_cast<int>(threadIdx.x & 31u) < qn) fix(q[threadIdx.x & 31u]);
 }
 
-// predicated shared-memory add without the compiler's warp-aggregation scaffolding
-__device__ __forceinline__ void red_shared_add(uint32_t* p, uint32_t v, bool pred) {
-    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.shared.add.u32 [%0], %1;\n}" ::"r"(
-                     smem_addr(p)),
-                 "r"(v), "r"(static_cast<uint32_t>(pred))
-                 : "memory");
-}
-
-// kPacked (nb <= 512): the plane word carries the pixel's exact bin next to the
-// estimate, bin << 23 | the 23 fraction bits of 256 + g255 (ulp 2^-15), so the
-// apply pass neither recomputes the bin nor re-tests its edges; else the plane
-// holds the fp32 estimate.
-__device__ __forceinline__ uint32_t plane_word(float g255, int bin) {
-    return (__float_as_uint(__fadd_rn(g255, 256.0f)) & 0x7FFFFFu) | (static_cast<uint32_t>(bin) << 23);
-}
-// kMode 2: the 16-bit plane word of t = v nb (unclamped, t >= 0): floor(t 2^F), capped
+// the 16-bit plane word of t = v nb (unclamped, t >= 0): floor(t 2^F), capped
 // at nb 2^F - 1 (v = 1 gives t = nb, bin nb - 1). For a pixel whose bin is sure,
 // u >> F is that bin (the same fp32 t floored); the others are patched by the fix.
 __device__ __forceinline__ uint32_t plane_u16(const U8Lhe& L, float tu) {
-    return min(__float_as_uint(__fadd_rd(fmaxf(tu, 0.0f), L.u_magic)) & 0x7FFFFFu, L.umax);
-}
-// the same for an estimate known to be >= 0 (decolor_fast of bytes: T >= 0, rsqrt > 0)
-__device__ __forceinline__ uint32_t plane_u16_nn(const U8Lhe& L, float tu) {
     return min(__float_as_uint(__fadd_rd(tu, L.u_magic)) & 0x7FFFFFu, L.umax);
 }
 // a plane word whose bin (u >> F) must be b: the nearest word of bin b
 __device__ __forceinline__ uint32_t plane_u16_fix(uint32_t u, int b, int F) {
     const int cb = static_cast<int>(u >> F);
     return cb == b ? u : (b < cb ? ((static_cast<uint32_t>(b) << F) | ((1u << F) - 1u)) : (static_cast<uint32_t>(b) << F));
-}
-
-// kMode: 0 fp32 estimate plane, 1 packed 32-bit plane (bin << 23 | estimate), 2 the
-// 16-bit plane (plane_u16)
-template <int kMode>
-__global__ void __launch_bounds__(kBlock, 4) lhe_hist_u8g_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
-                                                              float* __restrict__ gplane, int rows_per_chunk,
-                                                              bool vec) {
-    extern __shared__ uint32_t sh[];  // [nx * nb] + one dummy cell, then the warp queues
-    const int64_t img = blockIdx.z;
-    const int ty = blockIdx.y;
-    const int64_t y0 = static_cast<int64_t>(ty) * g.th + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
-    const int64_t y1 = imin64(imin64(y0 + rows_per_chunk, static_cast<int64_t>(ty + 1) * g.th), g.h);
-    if (y0 >= y1) return;
-    const int cells = g.nx * g.nb;
-    for (int i = threadIdx.x; i <= cells; i += blockDim.x) sh[i] = 0;
-    uint32_t* wq = sh + cells + 1 + (threadIdx.x >> 5) * kWq;
-    int qn = 0;
-    __syncthreads();
-    const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
-    const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
-    const int64_t row0 = (img * g.h + y0) * g.w;
-    auto group_at = [&](uint32_t gi, int& x0, int& n, int64_t& p0) {
-        const uint32_t gy = gi / gpr;
-        x0 = static_cast<int>(gi - gy * gpr) * kGrp;
-        n = static_cast<int>(imin64(kGrp, g.w - x0));
-        p0 = row0 + static_cast<int64_t>(gy) * g.w + x0;
-    };
-    // the reference's fp64 bin for a pixel next to a bin edge (queued, rare)
-    const auto fix = [&](uint32_t e) {
-        int x0, n;
-        int64_t p0;
-        group_at(e / kGrp, x0, n, p0);
-        const int p = static_cast<int>(e % kGrp);
-        uint32_t cr, cg, cb;
-        L.src.load(p0 + p, cr, cg, cb);
-        const int b = bin_d(L.src.gray_d(cr, cg, cb), g.nb);
-        atomicAdd(&sh[((x0 + p) / g.tw) * g.nb + b], 1u);
-        if constexpr (kMode == 1) {  // the exact bin into the plane word (after the warp's stores)
-            uint32_t* wp = reinterpret_cast<uint32_t*>(gplane) + p0 + p;
-            *wp = (*wp & 0x7FFFFFu) | (static_cast<uint32_t>(b) << 23);
-        } else if constexpr (kMode == 2) {
-            uint16_t* wp = reinterpret_cast<uint16_t*>(gplane) + p0 + p;
-            *wp = static_cast<uint16_t>(plane_u16_fix(*wp, b, L.ufrac));
-        }
-    };
-    const uint32_t lane = threadIdx.x & 31u;
-    U8Group nxt;
-    int x0n = 0, nn = 0;
-    int64_t p0n = 0;
-    if (threadIdx.x < ngroups) {
-        group_at(threadIdx.x, x0n, nn, p0n);
-        nxt.load(L.src.rgb, p0n, nn, vec);
-    }
-    // warp-uniform trip count (the queue uses warp collectives)
-    for (uint32_t gb = threadIdx.x - lane; gb < ngroups; gb += blockDim.x) {
-        const uint32_t gi = gb + lane;
-        uint32_t slow = 0;
-        if (gi < ngroups) {
-        const U8Group grp = nxt;
-        const int x0 = x0n, n = nn;
-        const int64_t p0 = p0n;
-        if (gi + blockDim.x < ngroups) {  // register prefetch of this thread's next group
-            group_at(gi + blockDim.x, x0n, nn, p0n);
-            nxt.load(L.src.rgb, p0n, nn, vec);
-        }
-        int tx = x0 / g.tw, next = (tx + 1) * g.tw;
-        if (n == kGrp) {
-            float g255[kGrp];
-            grp.gray255(L.k8, g255);
-            uint32_t words[kGrp];
-            // runs of equal cells are merged before the shared-memory add (a
-            // predicated red.shared: no branch per pixel); the first flush goes to
-            // the dummy cell. Groups inside one tile (all but one in tw / 16 when
-            // tw >= 16) skip the per-pixel tile stepping.
-            int run_cell = cells;
-            uint32_t run = 0;
-            const auto px = [&](int p, int cbase) {
-                bool sure;
-                const float tu = __fmul_rn(g255[p], L.nb_over_255);
-                const int b = L.bin_fast_t(tu, sure);
-                const int cell = cbase + b;
-                if constexpr (kMode == 2) words[p] = plane_u16(L, tu);  // unsure bins are patched below
-                else if constexpr (kMode == 1) words[p] = plane_word(g255[p], b);
-                else words[p] = __float_as_uint(g255[p]);
-                slow |= static_cast<uint32_t>(!sure) << p;
-                const bool same = cell == run_cell;
-                red_shared_add(&sh[run_cell], run, sure && !same);
-                run = sure ? (same ? run + 1 : 1u) : run;
-                run_cell = sure ? cell : run_cell;
-            };
-            if (x0 + kGrp <= next) {
-                const int cbase = tx * g.nb;
-#pragma unroll
-                for (int p = 0; p < kGrp; ++p) px(p, cbase);
-            } else {
-#pragma unroll
-                for (int p = 0; p < kGrp; ++p) {
-                    const bool step = x0 + p >= next;
-                    tx += step;
-                    next += step ? g.tw : 0;
-                    px(p, tx * g.nb);
-                }
-            }
-            red_shared_add(&sh[run_cell], run, true);
-            // keep the estimate for the apply pass (4 B/px instead of recomputing the gray)
-            uint32_t* wplane = reinterpret_cast<uint32_t*>(gplane);
-            if constexpr (kMode == 2) {
-                uint16_t* hplane = reinterpret_cast<uint16_t*>(gplane);
-                if (vec) {
-#pragma unroll
-                    for (int q = 0; q < kGrp / 8; ++q)
-                        reinterpret_cast<uint4*>(hplane + p0)[q] = make_uint4(
-                            __byte_perm(words[8 * q], words[8 * q + 1], 0x5410),
-                            __byte_perm(words[8 * q + 2], words[8 * q + 3], 0x5410),
-                            __byte_perm(words[8 * q + 4], words[8 * q + 5], 0x5410),
-                            __byte_perm(words[8 * q + 6], words[8 * q + 7], 0x5410));
-                } else {
-#pragma unroll
-                    for (int q = 0; q < kGrp; ++q) hplane[p0 + q] = static_cast<uint16_t>(words[q]);
-                }
-            } else if (vec) {
-#pragma unroll
-                for (int q = 0; q < kGrp / 4; ++q)
-                    reinterpret_cast<uint4*>(wplane + p0)[q] =
-                        make_uint4(words[4 * q], words[4 * q + 1], words[4 * q + 2], words[4 * q + 3]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < kGrp; ++q) wplane[p0 + q] = words[q];
-            }
-        } else {  // row tail of a width that is not a multiple of 16
-#pragma unroll 1
-            for (int p = 0; p < n; ++p) {
-                if (x0 + p >= next) {
-                    ++tx;
-                    next += g.tw;
-                }
-                uint32_t cr, cg, cb;  // (a dynamic index into grp.w would spill it to local memory)
-                L.src.load(p0 + p, cr, cg, cb);
-                const float g255 = decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
-                                                   static_cast<float>(cb), L.k8);
-                bool sure;
-                const float tu = __fmul_rn(g255, L.nb_over_255);
-                const int b = L.bin_fast_t(tu, sure);
-                if constexpr (kMode == 2) reinterpret_cast<uint16_t*>(gplane)[p0 + p] = static_cast<uint16_t>(plane_u16(L, tu));
-                else if constexpr (kMode == 1) reinterpret_cast<uint32_t*>(gplane)[p0 + p] = plane_word(g255, b);
-                else gplane[p0 + p] = g255;
-                if (sure) atomicAdd(&sh[tx * g.nb + b], 1u);
-                else slow |= 1u << p;
-            }
-        }
-        }
-        wq_push(wq, qn, slow, gi, fix);  // rare: pixels next to a bin edge
-    }
-    wq_flush(wq, qn, fix);
-    __syncthreads();
-    uint32_t* gh = hist + (img * g.ntile + static_cast<int64_t>(ty) * g.nx) * g.nb;
-    for (int i = threadIdx.x; i < cells; i += blockDim.x)
-        if (sh[i]) atomicAdd(&gh[i], sh[i]);
 }
 
 // shared-memory add at a shared-window address (unconditional: the caller
@@ -740,9 +563,10 @@ __device__ __forceinline__ void red_shared_at(uint32_t addr, uint32_t v) {
 // estimate, the bin test on t clamped to [1/2, nb - 1/2] (0 and nb are not bin
 // edges), the plane word from the unclamped t, and the run-merged count: the
 // cell's shared-memory address is formed straight from the bits of
-// fl_rd(t + 2^23) (one LEA; unsure pixels go to a dummy cell and the fp64
-// queue), a run is flushed with one predicated red.shared when the address
-// changes. Group coordinates advance incrementally and a per-column-group table
+// fl_rd(t + 2^23) (one LEA; an unsure pixel is counted in its fp32 bin and
+// queued: the fix moves the count if the fp64 bin differs), a run is flushed
+// with one red.shared when the address changes (otherwise the add goes to a
+// per-lane scratch cell). Group coordinates advance incrementally and a per-column-group table
 // (tile column, "group inside one tile") replaces the divisions per group.
 __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom g, uint32_t* __restrict__ hist,
                                                             uint16_t* __restrict__ plane, int rows_per_chunk,
@@ -774,14 +598,23 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
     // address of cell (tx, bin) from bits(fl_rd(t + 2^23)) = 0x4B000000 + bin: LEA(bits, base, 2)
     const uint32_t nb4 = 4u * static_cast<uint32_t>(g.nb);
     const uint32_t lea_base = sh_base - (0x4B000000u << 2);
-    const auto fix = [&](uint32_t e) {  // the reference's fp64 bin for a pixel next to a bin edge (rare)
+    // the reference's fp64 bin for a pixel next to a bin edge (rare); the pixel
+    // was counted in its fp32 bin, which is moved if the two differ
+    const auto fix = [&](uint32_t e) {
         const uint32_t gi = e / kGrp, gy = gi / gpr;
         const int x = static_cast<int>(gi - gy * gpr) * kGrp + static_cast<int>(e % kGrp);
         const int64_t pp = row0 + static_cast<int64_t>(gy) * g.w + x;
         uint32_t cr, cg, cb;
         L.src.load(pp, cr, cg, cb);
         const int b = bin_d(L.src.gray_d(cr, cg, cb), g.nb);
-        atomicAdd(&sh[(x / g.tw) * g.nb + b], 1u);
+        bool sure;
+        const int b32 = L.bin_fast_t(decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
+                                                     static_cast<float>(cb), L.kt), sure);
+        if (b32 != b) {
+            const int c0 = (x / g.tw) * g.nb;
+            atomicSub(&sh[c0 + b32], 1u);
+            atomicAdd(&sh[c0 + b], 1u);
+        }
         plane[pp] = static_cast<uint16_t>(plane_u16_fix(plane[pp], b, L.ufrac));  // after the warp's stores
     };
     const uint32_t dq = blockDim.x / gpr, dr = blockDim.x - dq * gpr;
@@ -822,9 +655,9 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
                 const float t = fminf(fmaxf(tu, 0.5f), L.t_hi);
                 const float tf = __fadd_rd(t, 8388608.0f);
                 const bool sure = fabsf(__fsub_rn(__fsub_rn(t, __fsub_rn(tf, 8388608.0f)), 0.5f)) < L.half_m;
-                words[p] = plane_u16_nn(L, tu);  // unsure bins are patched by the fix
+                words[p] = plane_u16(L, tu);  // unsure bins are patched by the fix
                 slow |= static_cast<uint32_t>(!sure) << p;
-                const uint32_t addr = sure ? base + (__float_as_uint(tf) << 2) : dummy;
+                const uint32_t addr = base + (__float_as_uint(tf) << 2);  // unsure: moved by the fix
                 const bool flush = addr != run_addr;
                 red_shared_at(flush ? run_addr : lane_cell, run);
                 run = flush ? 1u : run + 1u;
@@ -867,14 +700,14 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
                 }
                 uint32_t cr, cg, cb;  // (a dynamic index into grp.w would spill it to local memory)
                 L.src.load(p0 + p, cr, cg, cb);
-                const float g255 = decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
-                                                   static_cast<float>(cb), L.k8);
+                // (decolor_fast_x1 with kt: the same t as a lane of the group path, and as the fix)
+                const float tu = decolor_fast_x1(static_cast<float>(cr), static_cast<float>(cg),
+                                                 static_cast<float>(cb), L.kt);
                 bool sure;
-                const float tu = __fmul_rn(g255, L.nb_over_255);
                 const int b = L.bin_fast_t(tu, sure);
                 plane[p0 + p] = static_cast<uint16_t>(plane_u16(L, tu));
-                if (sure) atomicAdd(&sh[tx * g.nb + b], 1u);
-                else slow |= 1u << p;
+                atomicAdd(&sh[tx * g.nb + b], 1u);  // unsure: moved by the fix
+                if (!sure) slow |= 1u << p;
             }
         }
         }
@@ -887,220 +720,8 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
         if (sh[i]) atomicAdd(&gh[i], sh[i]);
 }
 
-// shared-memory layout of the apply kernel: curves of <= 3 tile rows, then per
-// column the blend fraction (fp32) and the left tile's curve offset i0 * nb
-// (u32), padded to a multiple of 16 columns so a group reads its 16 entries as
-// 128-bit vectors, then the per-warp fp64 queues
-struct ApplySmem {
-    static __host__ __device__ int64_t wpad(int64_t w) { return (w + kGrp - 1) / kGrp * kGrp; }
-    static __host__ __device__ size_t bytes(int nx, int nb, int64_t w) {
-        return static_cast<size_t>(nx) * nb * 16 + static_cast<size_t>(wpad(w)) * 6 + 16 + kWqBytes;
-    }
-};
-
-template <bool kGray, bool kIdent, bool kPacked>
-__device__ __forceinline__ void apply_groups(const U8Lhe& L, uint8_t* __restrict__ toned, uint8_t* __restrict__ gray,
-                                             const LheGeom& g, const LheBufs& s, int64_t y0, int64_t y1, int64_t img,
-                                             const float4* quad, const float* sxf, const uint16_t* sxo,
-                                             int64_t G, bool vec, uint32_t* wq) {
-    const float sf = static_cast<float>(g.strength);
-    const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
-    const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
-    // the hist pass's gray estimates (identical to recomputing them), one group of
-    // register prefetch ahead
-    auto load_est = [&](uint32_t gi, float4 (&e)[kGrp / 4]) {
-        const uint32_t gy = gi / gpr;
-        const int x0 = static_cast<int>(gi - gy * gpr) * kGrp;
-        const int n = static_cast<int>(imin64(kGrp, g.w - x0));
-        const float* src = s.gray255 + (img * g.h + y0 + gy) * g.w + x0;
-        if (vec && n == kGrp) {
-#pragma unroll
-            for (int q = 0; q < kGrp / 4; ++q) e[q] = __ldcs(reinterpret_cast<const float4*>(src) + q);
-        } else {
-            float t[kGrp];
-#pragma unroll
-            for (int q = 0; q < kGrp; ++q) t[q] = q < n ? src[q] : 0.0f;
-#pragma unroll
-            for (int q = 0; q < kGrp / 4; ++q) e[q] = make_float4(t[4 * q], t[4 * q + 1], t[4 * q + 2], t[4 * q + 3]);
-        }
-    };
-    // the reference's fp64 chain for a pixel within the quantization margin
-    // (queued, rare): overwrites the provisional bytes the warp stored
-    const auto fix = [&](uint32_t e) {
-        const uint32_t gi = e / kGrp, gy = gi / gpr;
-        const int p = static_cast<int>(e % kGrp);
-        const int64_t y = y0 + gy;
-        const int x = static_cast<int>(gi - gy * gpr) * kGrp + p;
-        const int64_t pp = (img * g.h + y) * g.w + x;
-        const int j0 = s.yi[y], j1 = g.ny > 1 ? j0 + 1 : 0;
-        uint32_t cr, cg, cb;
-        L.src.load(pp, cr, cg, cb);
-        const double vd = L.src.gray_d(cr, cg, cb);
-        const int b = bin_d(vd, g.nb);
-        const int i0 = s.xi[x], i1 = g.nx > 1 ? i0 + 1 : 0;
-        const int64_t t00 = img * g.ntile + static_cast<int64_t>(j0) * g.nx + i0, t01 = t00 - i0 + i1;
-        const int64_t t10 = img * g.ntile + static_cast<int64_t>(j1) * g.nx + i0, t11 = t10 - i0 + i1;
-        const double c00 = s.ident[t00] ? vd : s.curve[t00 * g.nb + b];
-        const double c01 = s.ident[t01] ? vd : s.curve[t01 * g.nb + b];
-        const double c10 = s.ident[t10] ? vd : s.curve[t10 * g.nb + b];
-        const double c11 = s.ident[t11] ? vd : s.curve[t11 * g.nb + b];
-        toned[pp] = static_cast<uint8_t>(quantize_d(blend_d(vd, c00, c01, c10, c11, s.xf[x], s.yf[y], g.strength)));
-        if constexpr (kGray) gray[pp] = static_cast<uint8_t>(quantize_d(vd));
-    };
-    const uint32_t lane = threadIdx.x & 31u;
-    int qn = 0;
-    float4 nxt[kGrp / 4];
-    if (threadIdx.x < ngroups) load_est(threadIdx.x, nxt);
-    // warp-uniform trip count (the queue uses warp collectives)
-    for (uint32_t gb = threadIdx.x - lane; gb < ngroups; gb += blockDim.x) {
-        const uint32_t gi = gb + lane;
-        uint32_t slow = 0;
-        if (gi < ngroups) {
-        const uint32_t gy = gi / gpr;
-        const int64_t y = y0 + gy;
-        const int x0 = static_cast<int>(gi - gy * gpr) * kGrp;
-        const int n = static_cast<int>(imin64(kGrp, g.w - x0));
-        const int64_t p0 = (img * g.h + y) * g.w + x0;
-        float g255[kGrp];
-#pragma unroll
-        for (int q = 0; q < kGrp / 4; ++q) {
-            g255[4 * q] = nxt[q].x;
-            g255[4 * q + 1] = nxt[q].y;
-            g255[4 * q + 2] = nxt[q].z;
-            g255[4 * q + 3] = nxt[q].w;
-        }
-        if (gi + blockDim.x < ngroups) load_est(gi + blockDim.x, nxt);
-        const float wy = s.yff[y];  // every row of the block blends the same tile-row pair
-        // the group's 16 blend fractions and curve offsets as 128-bit shared loads
-        float wxs[kGrp];
-        uint32_t xos[kGrp];
-        const int64_t gcol = x0 / kGrp;
-#pragma unroll
-        for (int q = 0; q < kGrp / 4; ++q) {
-            const float4 f = reinterpret_cast<const float4*>(sxf)[q * G + gcol];
-            const uint2 o = reinterpret_cast<const uint2*>(sxo)[q * G + gcol];
-            wxs[4 * q] = f.x;
-            wxs[4 * q + 1] = f.y;
-            wxs[4 * q + 2] = f.z;
-            wxs[4 * q + 3] = f.w;
-            xos[4 * q] = o.x & 0xFFFFu;
-            xos[4 * q + 1] = o.x >> 16;
-            xos[4 * q + 2] = o.y & 0xFFFFu;
-            xos[4 * q + 3] = o.y >> 16;
-        }
-        uint32_t ot[4] = {0u, 0u, 0u, 0u}, og[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-        for (int p = 0; p < kGrp; ++p) {
-            float v;  // everything below is in the 0..255 domain
-            bool sure;
-            int b;
-            if constexpr (kPacked) {  // estimate (ulp 2^-15) and exact bin from the hist pass
-                const uint32_t wd = __float_as_uint(g255[p]);
-                v = __fsub_rn(__uint_as_float((wd & 0x7FFFFFu) | 0x43800000u), 256.0f);
-                b = static_cast<int>(wd >> 23);
-                sure = true;
-            } else {
-                v = g255[p];
-                b = L.bin_fast(v, sure);
-            }
-            const float4 cq = quad[static_cast<int>(xos[p]) + b];  // the four curves: one LDS.128
-            float c00 = cq.x, c01 = cq.y, c10 = cq.z, c11 = cq.w;
-            if constexpr (kIdent) {
-                c00 = c00 != c00 ? v : c00;  // NaN: identity tile (the pixel's own value)
-                c01 = c01 != c01 ? v : c01;
-                c10 = c10 != c10 ? v : c10;
-                c11 = c11 != c11 ? v : c11;
-            }
-            const float wx = wxs[p];
-            const float top = __fmaf_rn(wx, __fsub_rn(c01, c00), c00);
-            const float bottom = __fmaf_rn(wx, __fsub_rn(c11, c10), c10);
-            const float eq = __fmaf_rn(wy, __fsub_rn(bottom, top), top);
-            // res = v + s (eq - v) is a convex combination of values in [0, 255]: no
-            // clamp; x = res + 0.5, floor(x) as the low byte of fl_rd(x + 2^23),
-            // x - floor(x) must clear the margin (x = 0.5 and 255.5 give exactly 0.5)
-            const float xq = __fadd_rn(__fmaf_rn(sf, __fsub_rn(eq, v), v), 0.5f);
-            const float tq = __fadd_rd(xq, 8388608.0f);
-            sure = sure && fabsf(__fsub_rn(__fsub_rn(xq, __fsub_rn(tq, 8388608.0f)), 0.5f)) < 0.5f - kQuantMargin;
-            ot[p >> 2] |= (__float_as_uint(tq) & 255u) << (8 * (p & 3));
-            if constexpr (kGray) {
-                const float xg = __fadd_rn(v, 0.5f);
-                const float tg = __fadd_rd(xg, 8388608.0f);
-                sure = sure && fabsf(__fsub_rn(__fsub_rn(xg, __fsub_rn(tg, 8388608.0f)), 0.5f)) < 0.5f - kGray255Margin;
-                og[p >> 2] |= (__float_as_uint(tg) & 255u) << (8 * (p & 3));
-            }
-            slow |= static_cast<uint32_t>(!sure && p < n) << p;
-        }
-        if (vec && n == kGrp) {
-            st_global_cs_v4(toned + p0, make_uint4(ot[0], ot[1], ot[2], ot[3]));
-            if constexpr (kGray) st_global_cs_v4(gray + p0, make_uint4(og[0], og[1], og[2], og[3]));
-        } else {
-#pragma unroll
-            for (int p = 0; p < kGrp; ++p) {
-                if (p < n) {
-                    toned[p0 + p] = static_cast<uint8_t>(ot[p >> 2] >> (8 * (p & 3)));
-                    if constexpr (kGray) gray[p0 + p] = static_cast<uint8_t>(og[p >> 2] >> (8 * (p & 3)));
-                }
-            }
-        }
-        }
-        wq_push(wq, qn, slow, gi, fix);
-    }
-    wq_flush(wq, qn, fix);
-}
-
-template <bool kGray, bool kPacked>
-__global__ void __launch_bounds__(kBlock, 3) lhe_apply_u8g_kernel(U8Lhe L, uint8_t* __restrict__ toned,
-                                                               uint8_t* __restrict__ gray, LheGeom g, LheBufs s,
-                                                               int rows_per_chunk, bool vec) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int64_t img = blockIdx.z;
-    // Blocks cover bands of rows between consecutive tile-row centres (yi[y] ==
-    // band for every row of band `band`, lhe_axis_kernel), so all rows of a
-    // block blend the same pair of tile rows (j0, j1) = (band, band + 1), or
-    // (0, 0) for a single tile row.
-    const int band = blockIdx.y, nband = g.ny > 1 ? g.ny - 1 : 1;
-    const int64_t lo = band == 0 ? 0 : static_cast<int64_t>(ceil(centre(band, g.th, g.h)));
-    const int64_t hi = band == nband - 1 ? g.h : static_cast<int64_t>(ceil(centre(band + 1, g.th, g.h)));
-    const int64_t y0 = lo + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
-    const int64_t y1 = imin64(y0 + rows_per_chunk, hi);
-    if (y0 >= y1) return;
-    const int jbase = g.ny > 1 ? band : 0, jrow = g.ny > 1 ? 1 : 0;  // j0 and j1 - j0
-    const int64_t wp = ApplySmem::wpad(g.w);
-    // quad[i0][b] = the four curves (j0,i0), (j0,i1), (j1,i0), (j1,i1) at bin b
-    // (255 * curve, NaN = identity tile; i1 = i0 + 1, or i0 for a single tile
-    // column): one 128-bit shared load per pixel instead of four random 32-bit ones
-    float4* quad = reinterpret_cast<float4*>(smem);                                 // [nx][nb]
-    float* sxf = reinterpret_cast<float*>(quad + static_cast<size_t>(g.nx) * g.nb);  // [wp]
-    uint16_t* sxo = reinterpret_cast<uint16_t*>(sxf + wp);                          // [wp] i0 * nb
-    uint32_t* wq = reinterpret_cast<uint32_t*>(sxo + wp) + 4 + (threadIdx.x >> 5) * kWq;  // per-warp queues
-    const float* cf = s.curvef + (img * g.ntile + static_cast<int64_t>(jbase) * g.nx) * g.nb;
-    const int rowoff = jrow * g.nx * g.nb;
-    for (int i = threadIdx.x; i < g.nx * g.nb; i += blockDim.x) {
-        const int b = i % g.nb, i0 = i / g.nb, i1 = g.nx > 1 ? min(i0 + 1, g.nx - 1) : i0;
-        quad[i] = make_float4(cf[i0 * g.nb + b], cf[i1 * g.nb + b], cf[rowoff + i0 * g.nb + b],
-                              cf[rowoff + i1 * g.nb + b]);
-    }
-    // column x = 16 gc + 4 q + r is stored at ((q * G + gc) * 4 + r), G = wp / 16: the
-    // lanes of a warp (consecutive groups gc) then read consecutive 16-byte vectors
-    const int64_t G = wp / kGrp;
-    for (int64_t x = threadIdx.x; x < wp; x += blockDim.x) {
-        const int64_t xc = imin64(x, g.w - 1);
-        const int64_t gc = x / kGrp, q = (x % kGrp) >> 2, r = x & 3;
-        const int64_t at = (q * G + gc) * 4 + r;
-        sxf[at] = s.xff[xc];
-        sxo[at] = static_cast<uint16_t>(s.xi[xc] * g.nb);  // < 2^16 (checked by the launcher)
-    }
-    __syncthreads();
-    // identity tiles (NaN curves) are rare: the per-pixel NaN selects only run in
-    // blocks whose staged curve rows contain one
-    bool any_ident = false;
-    for (int i = threadIdx.x; i < (1 + jrow) * g.nx; i += blockDim.x) any_ident |= cf[i * g.nb] != cf[i * g.nb];
-    if (__syncthreads_or(any_ident))
-        apply_groups<kGray, true, kPacked>(L, toned, gray, g, s, y0, y1, img, quad, sxf, sxo, G, vec, wq);
-    else
-        apply_groups<kGray, false, kPacked>(L, toned, gray, g, s, y0, y1, img, quad, sxf, sxo, G, vec, wq);
-}
-
+// row width padded to whole 16-pixel groups (the per-column tables)
+__host__ __device__ inline int64_t wpad16(int64_t w) { return (w + kGrp - 1) / kGrp * kGrp; }
 
 // ------------------------------------------------------------------ apply on the 16-bit plane
 // The hist pass writes u = floor(v nb 2^F) per pixel (2 B/px, plane_u16); the
@@ -1120,9 +741,12 @@ struct Apply16 {
     uint32_t mq, mq_ident, mg;  // margins of the toned / identity-tile / gray byte, units of 2^-15
 };
 
+// shared memory of the apply kernel: the band's blend table [nx][nb] (16 B
+// entries), the per-column blend fractions and table offsets (interleaved, see
+// lhe_table_kernel), the per-warp fp64 queues, one mbarrier
 struct Apply16Smem {
     static __host__ __device__ size_t bytes(int nx, int nb, int64_t w) {
-        return static_cast<size_t>(nx) * nb * 16 + static_cast<size_t>(ApplySmem::wpad(w)) * 8 + kWqBytes + 16;
+        return static_cast<size_t>(nx) * nb * 16 + static_cast<size_t>(wpad16(w)) * 8 + kWqBytes + 16;
     }
 };
 
@@ -1159,7 +783,7 @@ __global__ void __launch_bounds__(kBlock) lhe_table_kernel(LheGeom g, LheBufs s,
     // stored at ((q * G + gc) * 4 + r), G = wpad / 16, so the lanes of a warp
     // (consecutive groups gc) read consecutive 16-byte vectors
     if (band == 0 && img == 0) {  // split over the nx blocks of (band 0, image 0)
-        const int64_t wp = ApplySmem::wpad(g.w), G = wp / kGrp;
+        const int64_t wp = wpad16(g.w), G = wp / kGrp;
         for (int64_t x = threadIdx.x + static_cast<int64_t>(col) * blockDim.x; x < wp;
              x += static_cast<int64_t>(blockDim.x) * g.nx) {
             const int64_t xc = imin64(x, g.w - 1);
@@ -1192,7 +816,7 @@ __device__ __forceinline__ void apply16_groups(const U8Lhe& L, const Apply16& A,
     const float sf = static_cast<float>(g.strength);
     const uint32_t gpr = static_cast<uint32_t>((g.w + kGrp - 1) / kGrp);
     const uint32_t ngroups = static_cast<uint32_t>(y1 - y0) * gpr;  // < 2^31: rows of one tile row
-    const uint16_t* plane = reinterpret_cast<const uint16_t*>(s.gray255);
+    const uint16_t* plane = s.plane;
     const int F = kF >= 0 ? kF : L.ufrac;
     const int64_t rowbase = (img * g.h + y0) * g.w;
     // group gi = (row gy, column group gx); the thread's groups advance by
@@ -1352,7 +976,7 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply16_kernel(U8Lhe L, Apply16
     const int64_t y0 = lo + static_cast<int64_t>(blockIdx.x) * rows_per_chunk;
     const int64_t y1 = imin64(y0 + rows_per_chunk, hi);
     if (y0 >= y1) return;
-    const int64_t wp = ApplySmem::wpad(g.w);
+    const int64_t wp = wpad16(g.w);
     const int nq = g.nx * g.nb;
     uint4* quad = reinterpret_cast<uint4*>(smem);                              // [nx][nb] (lhe_table_kernel)
     float* sxf = reinterpret_cast<float*>(quad + nq);                          // [wp]
@@ -1383,12 +1007,6 @@ __global__ void __launch_bounds__(kBlock, 3) lhe_apply16_kernel(U8Lhe L, Apply16
 }
 
 // ------------------------------------------------------------------ driver
-// WG_LHE_PLANE=32: the 4 B/px plane (fp32 estimates / packed words) instead of
-// the 16-bit plane (A/B of the two)
-bool lhe_plane32() {
-    const char* e = std::getenv("WG_LHE_PLANE");
-    return e && e[0] == '3';
-}
 
 Apply16 make_apply16(int nb, int F, double strength) {
     Apply16 a;
@@ -1594,72 +1212,52 @@ extern "C" int wg_decolor_tone_local_u8(const uint8_t* rgb, uint8_t* toned, uint
     if (rc != WG_OK) return rc;
     const Chunking c = chunking(g);
     // + the dummy cell, warp queues, column-group table
-    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4 + kWqBytes + ApplySmem::wpad(g.w) / kGrp * 4 + 128;
-    const bool p32 = lhe_plane32();
-    const size_t asmem = p32 ? ApplySmem::bytes(g.nx, g.nb, g.w) : Apply16Smem::bytes(g.nx, g.nb, g.w);
-    // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact); the
-    // group apply reads the gray plane the group hist writes, so both or neither
-    // (the per-warp queue entries are group * 16 + pixel within one row chunk: < 2^32)
+    const size_t hsmem = static_cast<size_t>(g.nx) * g.nb * 4 + 4 + kWqBytes + wpad16(g.w) / kGrp * 4 + 128;
+    const size_t asmem = Apply16Smem::bytes(g.nx, g.nb, g.w);
+    // the group kernels' t-domain bin test needs nb <= 65536 (t + 2^23 exact, and
+    // the 16-bit plane word); the group apply reads the plane the group hist
+    // writes, so both or neither (the per-warp queue entries are group * 16 +
+    // pixel within one row chunk: < 2^32)
     const bool group_ok = bins <= 65536 && hsmem <= kHistSmemCap && asmem <= kApplySmemCap &&
                           g.ny <= 65535 && g.nx <= 65535 &&  // grid dimensions of the hist / table / apply grids
-                          static_cast<int64_t>(c.rows_per_chunk) * ApplySmem::wpad(g.w) < (int64_t(1) << 32) &&
-                          (!p32 || static_cast<int64_t>(g.nx) * g.nb <= 65536);  // u16 column offsets i0 * nb
-    const bool packed = bins <= 512;  // the plane word carries the bin (9 bits)
+                          static_cast<int64_t>(c.rows_per_chunk) * wpad16(g.w) < (int64_t(1) << 32);
     if (group_ok) {
-        auto hk = packed ? lhe_hist_u8g_kernel<1> : lhe_hist_u8g_kernel<0>;
-        if (hsmem > 48 * 1024) {
-            cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hsmem));
+        if (hsmem > 48 * 1024)
             cudaFuncSetAttribute(lhe_hist16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(hsmem));
-        }
         per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
             U8Lhe Li = L;
             Li.src.advance(i0 * g.h * g.w);
-            const dim3 hgrid(c.chunks, g.ny, static_cast<unsigned>(gi.nimg));
-            if (p32)
-                hk<<<hgrid, kBlock, hsmem, st>>>(Li, gi, b.hist + i0 * g.ntile * g.nb, b.gray255 + i0 * g.h * g.w,
-                                                 c.rows_per_chunk, vec);
-            else
-                lhe_hist16_kernel<<<hgrid, kBlock, hsmem, st>>>(
-                    Li, gi, b.hist + i0 * g.ntile * g.nb, reinterpret_cast<uint16_t*>(b.gray255 + i0 * g.h * g.w),
-                    c.rows_per_chunk, vec);
+            lhe_hist16_kernel<<<dim3(c.chunks, g.ny, static_cast<unsigned>(gi.nimg)), kBlock, hsmem, st>>>(
+                Li, gi, b.hist + i0 * g.ntile * g.nb, b.plane + i0 * g.h * g.w, c.rows_per_chunk, vec);
         });
     } else {
         lhe_hist(src, g, b, st);
     }
     lhe_curves(g, b, st);
     if (group_ok) {
-        auto kern = gray_or_null ? (packed ? lhe_apply_u8g_kernel<true, true> : lhe_apply_u8g_kernel<true, false>)
-                                 : (packed ? lhe_apply_u8g_kernel<false, true> : lhe_apply_u8g_kernel<false, false>);
-        auto kern16 = F == 8 ? (gray_or_null ? lhe_apply16_kernel<true, 8> : lhe_apply16_kernel<false, 8>)
-                             : (gray_or_null ? lhe_apply16_kernel<true, -1> : lhe_apply16_kernel<false, -1>);
+        auto kern = F == 8 ? (gray_or_null ? lhe_apply16_kernel<true, 8> : lhe_apply16_kernel<false, 8>)
+                           : (gray_or_null ? lhe_apply16_kernel<true, -1> : lhe_apply16_kernel<false, -1>);
         const Apply16 A16 = make_apply16(static_cast<int>(bins), F, strength);
         const int nband = g.ny > 1 ? g.ny - 1 : 1;
-        if (asmem > 48 * 1024) {
+        if (asmem > 48 * 1024)
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(asmem));
-            cudaFuncSetAttribute(kern16, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(asmem));
-        }
         per_image_slice(g, [&](int64_t i0, const LheGeom& gi) {
             U8Lhe Li = L;
             Li.src.advance(i0 * g.h * g.w);
-            LheBufs bi = b;  // the kernel indexes tiles per image slice
+            LheBufs bi = b;  // the kernels index tiles per image slice
             bi.curve += i0 * g.ntile * g.nb;
             bi.curvef += i0 * g.ntile * g.nb;
             bi.ident += i0 * g.ntile;
             const int64_t off = i0 * g.h * g.w;
-            bi.gray255 += off;
+            bi.plane += off;
             bi.qtab += i0 * nband * static_cast<int64_t>(g.nx) * g.nb;
             bi.qident += i0 * nband;
-            if (!p32) lhe_table_kernel<<<dim3(g.nx, nband, static_cast<unsigned>(gi.nimg)), kBlock, 0, st>>>(gi, bi, A16);
+            lhe_table_kernel<<<dim3(g.nx, nband, static_cast<unsigned>(gi.nimg)), kBlock, 0, st>>>(gi, bi, A16);
             // row bands between tile-row centres are at most ~1.5 tile heights (+2 rows)
             const int achunks = static_cast<int>((2LL * g.th + 2 + c.rows_per_chunk - 1) / c.rows_per_chunk);
-            const dim3 agrid(achunks, g.ny > 1 ? g.ny - 1 : 1, static_cast<unsigned>(gi.nimg));
-            if (p32)
-                kern<<<agrid, kBlock, asmem, st>>>(Li, toned + off, gray_or_null ? gray_or_null + off : nullptr, gi,
-                                                   bi, c.rows_per_chunk, vec);
-            else
-                kern16<<<agrid, kBlock, asmem, st>>>(Li, A16, toned + off, gray_or_null ? gray_or_null + off : nullptr,
-                                                     gi, bi, c.rows_per_chunk, vec);
+            kern<<<dim3(achunks, nband, static_cast<unsigned>(gi.nimg)), kBlock, asmem, st>>>(
+                Li, A16, toned + off, gray_or_null ? gray_or_null + off : nullptr, gi, bi, c.rows_per_chunk, vec);
         });
     } else {
         lhe_apply_u8_kernel<<<apply_grid(g), kBlock, 0, st>>>(src, toned, gray_or_null, g, b);
