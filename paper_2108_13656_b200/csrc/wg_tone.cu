@@ -1135,9 +1135,16 @@ struct OpToneSqExactU8 {
         __shared__ int n[8];
         return n;
     }
+    // the staged step words carry + M: word' = word + M, so the flag test is
+    // (word' mod 2^24) <= 2M without a per-pixel add; byte 3 of word' differs from
+    // byte 3 of word only when the low 24 bits wrap, i.e. for flagged pixels,
+    // whose bytes the fp64 queue rewrites
     __device__ __forceinline__ void prologue() const {
         const uint4* src = reinterpret_cast<const uint4*>(tab->sq_step);
-        for (int i = threadIdx.x; i < kSqBins / 4; i += blockDim.x) reinterpret_cast<uint4*>(s_step())[i] = src[i];
+        for (int i = threadIdx.x; i < kSqBins / 4; i += blockDim.x) {
+            const uint4 v = src[i];
+            reinterpret_cast<uint4*>(s_step())[i] = make_uint4(v.x + M, v.y + M, v.z + M, v.w + M);
+        }
         for (int i = threadIdx.x; i < kSqW; i += blockDim.x) s_w()[i] = w.w[i];
         if (threadIdx.x < 8) s_qn()[threadIdx.x] = 0;
     }
@@ -1156,7 +1163,10 @@ struct OpToneSqExactU8 {
                                  v[1].z, v[1].w, v[2].x, v[2].y, v[2].z, v[2].w};
         const uint32_t wb = smem_addr(s_w()) + w.ofs;
         const uint32_t twoM = 2 * M;
-        uint32_t ot[4], mask = 0;
+        // |bits(u) - bits(anchor)| <= M  <=>  ((word + M) mod 2^24) <= 2M (+ M staged):
+        // the group keeps only the minimum of the low 24 bits (one VIMNMX per pixel);
+        // the rare group with a flagged pixel recomputes its words for the mask
+        uint32_t ot[4], lo24 = 0xFFFFFFFFu;
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
             uint32_t tt[4];
@@ -1167,14 +1177,22 @@ struct OpToneSqExactU8 {
                 sq_pair_words<false>(wd, j, k, s_step(), nullptr, wb, t2, g2);
                 tt[2 * h] = t2[0];
                 tt[2 * h + 1] = t2[1];
-                // |bits(u) - bits(anchor)| <= M  <=>  ((word + M) mod 2^24) <= 2M
-                mask |= ((((t2[0] + M) & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j);
-                mask |= ((((t2[1] + M) & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j + 1);
+                lo24 = min(lo24, min(t2[0] & 0xFFFFFFu, t2[1] & 0xFFFFFFu));
             }
             ot[qd] = __byte_perm(__byte_perm(tt[0], tt[1], 0x0073u), __byte_perm(tt[2], tt[3], 0x0073u), 0x5410u);
         }
         st_global_cs_v4(toned + px0, make_uint4(ot[0], ot[1], ot[2], ot[3]));
-        if (__any_sync(0xFFFFFFFFu, mask != 0u)) {  // rare: queue the pixels for the fp64 chain
+        if (__any_sync(0xFFFFFFFFu, lo24 <= twoM)) {  // rare: queue the pixels for the fp64 chain
+            uint32_t mask = 0;
+            if (lo24 <= twoM) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {  // (static indices keep wd[] in registers)
+                    uint32_t t2[2], g2[2];
+                    sq_pair_words<false>(wd, j, k, s_step(), nullptr, wb, t2, g2);
+                    mask |= (((t2[0] & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j);
+                    mask |= (((t2[1] & 0xFFFFFFu) <= twoM) ? 1u : 0u) << (2 * j + 1);
+                }
+            }
             const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
             uint32_t* q = s_queue() + wid * kExactQueue;
             int qn = s_qn()[wid];
