@@ -38,3 +38,13 @@ H="python bench.py --workload C4 --steps 2 --warmup 3 --no-e2e --no-cpu --no-sus
 $H > $OUT/ncu_plain4.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"hdr_ws_kernel" -s 3 -c 1 -o $OUT/prof_c4_hdr $H > $OUT/ncu_full_hdr.log 2>&1
 echo "ncu_full_hdr=$?"
+# local tone map (C3 frames): per-kernel split and full captures of its two per-pixel kernels
+timeout 300 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.per_cycle_active \
+  --clock-control none -k regex:lhe_ --csv python scripts/ab_tone.py --op local --images 16 --iters 1 --rounds 1 --configs "" \
+  > $OUT/lhe_split.csv 2> $OUT/lhe_split.err; echo "lhe_split=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"lhe_hist16|lhe_apply16" -c 2 -o $OUT/prof_c3_lhe \
+  python scripts/ab_tone.py --op local --images 16 --iters 1 --rounds 1 --configs "" > $OUT/ncu_full_lhe.log 2>&1
+echo "ncu_full_lhe=$?"
+timeout 600 python scripts/ab_tone.py --op local --images 64 --iters 10 --rounds 3 --sleep 2 --configs "" > $OUT/ab_local.log 2>&1
+timeout 600 python scripts/ab_tone.py --op tone_exact --images 256 --iters 20 --rounds 3 --sleep 2 --configs "" > $OUT/ab_tone_exact.log 2>&1
+echo "ab=$?"
