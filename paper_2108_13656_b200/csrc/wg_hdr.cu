@@ -500,7 +500,12 @@ constexpr int kWsT = 1024;   // one CTA per SM
 constexpr int kWsLinePx = 32;    // partition unit: one 128 B gray line
 constexpr int kWsMaxGrid = 1024;  // partial slots per image
 constexpr int kWsMaxRing = 4;
-constexpr size_t kWsRingBudget = size_t(56) << 20;  // gray ring bytes kept L2-resident
+// gray ring bytes kept L2-resident: 2 slots (C4: 2 slots 322.6, 3 slots 310.8,
+// 4 slots 294 Gpix/s -- the ring competes with the RGB stream for L2)
+constexpr size_t kWsRingBudget = 0;
+// producer L2 prefetch distance in waves of the CTA's range (C4, TMEM kernel:
+// 0 -> 320.8, 2 -> 339.5, 3 -> 340.1, 8 -> 336.7 Gpix/s; L2 ring: 0 -> 296, 3 -> 309)
+constexpr int kWsPrefetchWaves = 3;
 
 
 
@@ -529,6 +534,11 @@ __device__ __forceinline__ void st_v4_hint(float* p, float4 v, uint64_t pol) {
     asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y),
                  "f"(v.z), "f"(v.w), "l"(pol)
                  : "memory");
+}
+// bulk L2 prefetch (no registers, no shared memory): the producers' loads then
+// hit L2, so the same registers in flight sustain more HBM bandwidth
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -608,11 +618,14 @@ __device__ __forceinline__ void ws_tone_range(const float* __restrict__ gsl, uin
     }
 }
 
-template <int kCons_>
+// kDbg (timing experiments only, WG_HDR_DBG; output invalid): 1 = consumers do
+// not tone, 2 = producers do not load (synthetic values), 3 = producers do not
+// store the gray and consumers do not tone
+template <int kCons_, int kDbg = 0>
 __global__ void __launch_bounds__(kWsT, 1)
     hdr_ws_kernel(const float* __restrict__ rgb, uint8_t* __restrict__ out, float* __restrict__ ring,
                   float2* __restrict__ parts, unsigned* __restrict__ counts, int64_t nimg, int64_t ppi, int nring,
-                  U8Consts k, float m, float slope, Theta theta) {
+                  U8Consts k, float m, float slope, Theta theta, int pf_waves) {
     constexpr int kProd_ = kWsT / 32 - kCons_, kProdT_ = kProd_ * 32, kConsT_ = kCons_ * 32;
     __shared__ uint32_t s_lut[kLutBins];
     __shared__ int s_cnt[kLutBins];
@@ -620,18 +633,40 @@ __global__ void __launch_bounds__(kWsT, 1)
     __shared__ int s_wsum[kCons_];
     __shared__ int s_conflict;
     __shared__ volatile int s_toned;  // images this CTA's consumers have finished
+    __shared__ int s_pf[2];           // producer thread 0: next (image, wave) to prefetch into L2
     float* s_thr = reinterpret_cast<float*>(s_lut);  // thresholds, then the entries in place
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, c = blockIdx.x;
     const int64_t nlines = ppi / kWsLinePx;
     const WsMap mp{nlines * c / G, nlines * (c + 1) / G};
-    if (tid == 0) s_toned = 0;
+    if (tid == 0) {
+        s_toned = 0;
+        s_pf[0] = s_pf[1] = 0;
+    }
     __syncthreads();
 
     if (warp < kProd_) {
         // ---------------- producers: three 128-bit loads per quad, the next quad in flight
         const uint64_t pol_gray = l2_policy_evict_last();
         const int64_t nq = mp.nquads();  // this CTA's quads (4 px) of every image
+        // L2 prefetch pf_waves waves (kProdT_ quads, 36 KiB) ahead of the loads,
+        // across image boundaries; thread 0 keeps the next (image, wave) in
+        // shared memory (no registers in the other threads)
+        const int nw = static_cast<int>((nq + kProdT_ - 1) / kProdT_);
+        auto prefetch_next = [&]() {
+            const int i2 = s_pf[0], w2 = s_pf[1];
+            if (i2 >= nimg) return;
+            const int64_t q0 = static_cast<int64_t>(w2) * kProdT_, q1 = min(nq, q0 + kProdT_);
+            prefetch_l2_bulk(rgb + i2 * ppi * 3 + 12 * mp.quad(q0), static_cast<uint32_t>((q1 - q0) * 48));
+            if (w2 + 1 == nw) {
+                s_pf[0] = i2 + 1;
+                s_pf[1] = 0;
+            } else {
+                s_pf[1] = w2 + 1;
+            }
+        };
+        if (tid == 0)
+            for (int w = 0; w < pf_waves; ++w) prefetch_next();
         for (int64_t i = 0; i < nimg; ++i) {
             if (i >= nring) {  // slot i % nring: this CTA's consumers are done with image i - nring
                 for (uint32_t spins = 0; s_toned < i - nring + 1; ++spins) {
@@ -644,7 +679,11 @@ __global__ void __launch_bounds__(kWsT, 1)
             float lo = INFINITY, hi = 0.0f;
             int64_t u = tid;
             float4 n0, n1, n2;
-            if (u < nq) {
+            if (kDbg == 2) {
+                n0 = make_float4(float(u) + 1.0f, 2.0f, 3.0f, 4.0f);
+                n1 = make_float4(5.0f, 6.0f, 7.0f, 8.0f);
+                n2 = make_float4(9.0f, 10.0f, 11.0f, float(i));
+            } else if (u < nq) {
                 const float4* src = reinterpret_cast<const float4*>(in + 12 * mp.quad(u));
                 n0 = __ldcs(src);
                 n1 = __ldcs(src + 1);
@@ -653,7 +692,10 @@ __global__ void __launch_bounds__(kWsT, 1)
             for (; u < nq; u += kProdT_) {
                 const int64_t q = mp.quad(u);
                 const float4 v0 = n0, v1 = n1, v2 = n2;
-                if (u + kProdT_ < nq) {
+                if (pf_waves > 0 && tid == 0) prefetch_next();
+                if (kDbg == 2) {
+                    n0.x += 1.0f;
+                } else if (u + kProdT_ < nq) {
                     const float4* src = reinterpret_cast<const float4*>(in + 12 * mp.quad(u + kProdT_));
                     n0 = __ldcs(src);
                     n1 = __ldcs(src + 1);
@@ -667,7 +709,7 @@ __global__ void __launch_bounds__(kWsT, 1)
                 track(a.y, lo, hi);
                 track(b.x, lo, hi);
                 track(b.y, lo, hi);
-                st_v4_hint(g + 4 * q, make_float4(a.x, a.y, b.x, b.y), pol_gray);
+                if (kDbg != 3) st_v4_hint(g + 4 * q, make_float4(a.x, a.y, b.x, b.y), pol_gray);
             }
             warp_minmax(lo, hi);
             if (lane == 0) {
@@ -754,7 +796,8 @@ __global__ void __launch_bounds__(kWsT, 1)
         // tone this CTA's lines (per-image mode hoisted out of the pixel loop)
         const float* gsl = ring + (i % nring) * ppi;
         uint8_t* o = out + i * ppi;
-        if (st.mode == 1 && st.lut) {
+        if (kDbg == 1 || kDbg == 3) {
+        } else if (st.mode == 1 && st.lut) {
             const float inv = st.inv_gmin;
             ws_tone_range<2, kConsT_>(gsl, o, mp, ct, [&](float v) -> uint32_t { return lut_px32(v, inv, s_lut); });
         } else if (st.mode == 2) {
@@ -765,6 +808,270 @@ __global__ void __launch_bounds__(kWsT, 1)
         named_bar(2, kConsT_);  // every consumer is done with the slot and with s_lut
         if (ct == 0) s_toned = static_cast<int>(i + 1);
     }
+}
+
+// ---------------------------------------------------------------- TMEM-staged variant
+// hdr_tm_kernel: the same warp-specialised schedule, but the gray of the CTA's
+// range never leaves the SM: producers tcgen05.st it into tensor memory (256 KiB
+// per SM, otherwise unused by this bandwidth-bound map: 2 slots of 128 lanes x
+// 256 columns = 32768 px each), consumers tcgen05.ld it back. HBM/L2 traffic is
+// the compulsory 12 B/px in + 1 B/px out and no gray line competes with the RGB
+// stream for L2. Fits when a CTA's per-image range is <= 8192 quads (C4: 7085).
+// Quad u of the range lives at TMEM lane u % 128, columns 4 (u / 128) + 0..3:
+// kProdT_ is a multiple of 128, so producer warp w always hits lanes
+// 32 (w % 4) .. + 31 -- the lanes its warp may access -- and a consumer warp
+// reads whole column groups of its own quadrant.
+constexpr int kTmCols = 512, kTmSlotCols = 256, kTmMaxQuads = kTmSlotCols / 4 * 128;
+
+__device__ __forceinline__ void tm_st4(uint32_t taddr, float a, float b, float c, float d) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(__float_as_uint(a)),
+                 "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d))
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// consumer tone of one TMEM slot: warp cw of quadrant cw % 4, half cw / 4 of the
+// column groups, four groups (16 columns) per tcgen05.ld; one 32-bit store per
+// quad (a warp stores 128 contiguous bytes)
+template <int kCons_, class Px>
+__device__ __forceinline__ void tm_tone_slot(uint32_t tslot, uint8_t* __restrict__ o, int64_t nq, int cw, int lane,
+                                             Px px) {
+    const int qd = cw & 3, h = cw >> 2;
+    constexpr int kHalves = kCons_ / 4;
+    const int ncg = static_cast<int>((nq + 127) >> 7);
+    const int per = (((ncg + kHalves - 1) / kHalves) + 3) & ~3;  // groups per warp, a multiple of 4
+    const int g0 = h * per, g1 = min(ncg, g0 + per);
+    const uint32_t tl = tslot + (static_cast<uint32_t>(qd * 32) << 16);
+    for (int g = g0; g < g1; g += 4) {
+        uint32_t r[16];
+        tm_ld16(tl + 4 * g, r);
+        tm_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t u = (static_cast<int64_t>(g + j) << 7) + qd * 32 + lane;
+            if (g + j < g1 && u < nq) {
+                const uint32_t w = px(__uint_as_float(r[4 * j])) | (px(__uint_as_float(r[4 * j + 1])) << 8) |
+                                   (px(__uint_as_float(r[4 * j + 2])) << 16) | (px(__uint_as_float(r[4 * j + 3])) << 24);
+                __stcs(reinterpret_cast<unsigned*>(o) + u, w);
+            }
+        }
+    }
+}
+
+template <int kCons_>
+__global__ void __launch_bounds__(kWsT, 1)
+    hdr_tm_kernel(const float* __restrict__ rgb, uint8_t* __restrict__ out, float2* __restrict__ parts,
+                  unsigned* __restrict__ counts, int64_t nimg, int64_t ppi, U8Consts k, float m, float slope,
+                  Theta theta, int pf_waves) {
+    static_assert(kCons_ % 4 == 0, "consumer warps come in whole quadrant sets");
+    constexpr int kProd_ = kWsT / 32 - kCons_, kProdT_ = kProd_ * 32, kConsT_ = kCons_ * 32;
+    static_assert(kProdT_ % 128 == 0, "producer waves must cover whole TMEM column groups");
+    constexpr int kRing = kTmCols / kTmSlotCols;
+    __shared__ uint32_t s_lut[kLutBins];
+    __shared__ int s_cnt[kLutBins];
+    __shared__ float s_plo[kProd_], s_phi[kProd_], s_clo[kCons_], s_chi[kCons_];
+    __shared__ int s_wsum[kCons_];
+    __shared__ int s_conflict;
+    __shared__ volatile int s_toned;  // images this CTA's consumers have finished
+    __shared__ int s_pf[2];           // producer thread 0: next (image, wave) to prefetch into L2
+    __shared__ uint32_t s_tmem;       // TMEM base address (tcgen05.alloc)
+    float* s_thr = reinterpret_cast<float*>(s_lut);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t nlines = ppi / kWsLinePx;
+    const WsMap mp{nlines * c / G, nlines * (c + 1) / G};
+    const int64_t nq = mp.nquads();  // <= kTmMaxQuads (host check)
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&s_tmem))),
+                     "n"(kTmCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        s_toned = 0;
+        s_pf[0] = s_pf[1] = 0;
+    }
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    const uint32_t tbase = s_tmem;
+
+    if (warp < kProd_) {
+        // ---------------- producers: three 128-bit loads per quad, the next quad in flight
+        const int nw = static_cast<int>((nq + kProdT_ - 1) / kProdT_);
+        auto prefetch_next = [&]() {
+            const int i2 = s_pf[0], w2 = s_pf[1];
+            if (i2 >= nimg) return;
+            const int64_t q0 = static_cast<int64_t>(w2) * kProdT_, q1 = min(nq, q0 + kProdT_);
+            prefetch_l2_bulk(rgb + i2 * ppi * 3 + 12 * mp.quad(q0), static_cast<uint32_t>((q1 - q0) * 48));
+            if (w2 + 1 == nw) {
+                s_pf[0] = i2 + 1;
+                s_pf[1] = 0;
+            } else {
+                s_pf[1] = w2 + 1;
+            }
+        };
+        if (tid == 0)
+            for (int w = 0; w < pf_waves; ++w) prefetch_next();
+        const uint32_t tq = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16);  // this warp's lane quadrant
+        for (int64_t i = 0; i < nimg; ++i) {
+            if (i >= kRing) {  // slot i % kRing: this CTA's consumers are done with image i - kRing
+                for (uint32_t spins = 0; s_toned < i - kRing + 1; ++spins) {
+                    __nanosleep(64);
+                    if (spins > (1u << 26)) __trap();
+                }
+                tm_fence_after();
+            }
+            const float* in = rgb + i * ppi * 3;
+            const uint32_t ts = tq + static_cast<uint32_t>((i % kRing) * kTmSlotCols);
+            float lo = INFINITY, hi = 0.0f;
+            // warp-uniform trip count (tcgen05.st is .aligned): lanes past the range
+            // compute a clamped quad and store into unused cells
+            int64_t u = tid;
+            const int64_t ulast = nq - 1;
+            float4 n0, n1, n2;
+            {
+                const float4* src = reinterpret_cast<const float4*>(in + 12 * mp.quad(min(u, ulast)));
+                n0 = __ldcs(src);
+                n1 = __ldcs(src + 1);
+                n2 = __ldcs(src + 2);
+            }
+            for (; u - lane < nq; u += kProdT_) {
+                const float4 v0 = n0, v1 = n1, v2 = n2;
+                if (pf_waves > 0 && tid == 0) prefetch_next();
+                if (u + kProdT_ - lane < nq) {
+                    const float4* src =
+                        reinterpret_cast<const float4*>(in + 12 * mp.quad(min(u + kProdT_, ulast)));
+                    n0 = __ldcs(src);
+                    n1 = __ldcs(src + 1);
+                    n2 = __ldcs(src + 2);
+                }
+                const float2 a = decolor_fast_x2(make_float2(v0.x, v0.w), make_float2(v0.y, v1.x),
+                                                 make_float2(v0.z, v1.y), k);
+                const float2 b = decolor_fast_x2(make_float2(v1.z, v2.y), make_float2(v1.w, v2.z),
+                                                 make_float2(v2.x, v2.w), k);
+                if (u < nq) {
+                    track(a.x, lo, hi);
+                    track(a.y, lo, hi);
+                    track(b.x, lo, hi);
+                    track(b.y, lo, hi);
+                }
+                tm_st4(ts + static_cast<uint32_t>(4 * (u >> 7)), a.x, a.y, b.x, b.y);
+            }
+            tm_wait_st();
+            tm_fence_before();
+            warp_minmax(lo, hi);
+            if (lane == 0) {
+                s_plo[warp] = lo;
+                s_phi[warp] = hi;
+            }
+            named_bar(1, kProdT_);
+            if (tid == 0) {
+                for (int w = 0; w < kProd_; ++w) {
+                    lo = fminf(lo, s_plo[w]);
+                    hi = fmaxf(hi, s_phi[w]);
+                }
+                __stcg(parts + i * kWsMaxGrid + c, make_float2(lo, hi));
+                __threadfence();
+                atomicAdd(counts + i, 1u);
+            }
+            named_bar(1, kProdT_);  // s_plo / s_phi are rewritten for the next image
+        }
+    } else {
+        // ---------------- consumers
+        const int ct = tid - kProdT_, cw = ct >> 5;
+        const ToneU8 tc = make_tone_u8(m, slope);
+        for (int64_t i = 0; i < nimg; ++i) {
+            if (ct == 0) wait_geq(counts + i, static_cast<unsigned>(G));
+            named_bar(2, kConsT_);
+            tm_fence_after();
+            float lo = INFINITY, hi = 0.0f;
+            for (int q = ct; q < G; q += kConsT_) {
+                const float2 pr = __ldcg(parts + i * kWsMaxGrid + q);
+                lo = fminf(lo, pr.x);
+                hi = fmaxf(hi, pr.y);
+            }
+            warp_minmax(lo, hi);
+            if (lane == 0) {
+                s_clo[cw] = lo;
+                s_chi[cw] = hi;
+            }
+            for (int b = ct; b < kLutBins; b += kConsT_) {
+                s_cnt[b] = 0;
+                s_thr[b] = INFINITY;
+            }
+            if (ct == 0) s_conflict = 0;
+            named_bar(2, kConsT_);
+            lo = s_clo[0];
+            hi = s_chi[0];
+            for (int w = 1; w < kCons_; ++w) {
+                lo = fminf(lo, s_clo[w]);
+                hi = fmaxf(hi, s_chi[w]);
+            }
+            double lr;
+            HdrStat st = hdr_stat_of(lo, hi, &lr);
+            if (st.mode == 1 && lr < kLutOct - 1) {  // uniform over the consumer warps
+                for (int j = ct; j < 255; j += kConsT_) {
+                    const float gam = static_cast<float>(exp2(theta.v[j] * lr));
+                    const int b = lut_bin(gam);
+                    if (atomicAdd(&s_cnt[b], 1) != 0) s_conflict = 1;
+                    s_thr[b] = gam;
+                }
+                named_bar(2, kConsT_);
+                constexpr int kPer = (kLutBins + kConsT_ - 1) / kConsT_;
+                const int b0 = min(ct * kPer, kLutBins), b1 = min(b0 + kPer, kLutBins);
+                int sum = 0;
+                for (int b = b0; b < b1; ++b) sum += s_cnt[b];
+                int incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                if (lane == 31) s_wsum[cw] = incl;
+                named_bar(2, kConsT_);
+                int off = incl - sum;
+                for (int w = 0; w < cw; ++w) off += s_wsum[w];
+                for (int b = b0; b < b1; ++b) {
+                    s_lut[b] = lut_entry(off, s_thr[b]);
+                    off += s_cnt[b];
+                }
+                st.lut = s_conflict ? 0 : 1;
+                named_bar(2, kConsT_);
+            }
+            const uint32_t ts = tbase + static_cast<uint32_t>((i % kRing) * kTmSlotCols);
+            uint8_t* o = out + i * ppi + mp.quad(0) * 4;
+            if (st.mode == 1 && st.lut) {
+                const float inv = st.inv_gmin;
+                tm_tone_slot<kCons_>(ts, o, nq, cw, lane, [&](float v) -> uint32_t { return lut_px32(v, inv, s_lut); });
+            } else if (st.mode == 2) {
+                tm_tone_slot<kCons_>(ts, o, nq, cw, lane, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });
+            } else {
+                tm_tone_slot<kCons_>(ts, o, nq, cw, lane,
+                                     [&](float v) -> uint32_t { return tone_arith_call(v, st, tc); });
+            }
+            tm_fence_before();
+            named_bar(2, kConsT_);  // every consumer is done with the slot and with s_lut
+            if (ct == 0) s_toned = static_cast<int>(i + 1);
+        }
+    }
+    tm_fence_before();
+    __syncthreads();
+    tm_fence_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(kTmCols) : "memory");
 }
 
 // ---------------------------------------------------------------- host helpers
@@ -900,9 +1207,10 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
     const bool ws_ok = (pix_per_img % kWsLinePx) == 0 && (reinterpret_cast<uintptr_t>(rgb) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(out) & 15) == 0 && device >= 0 && device < kMaxDevices;
     // 8 consumer warps of 32 (C4: 4 -> 274, 12 -> 261, 16 -> 270 vs 308 Gpix/s)
-    static std::atomic<int> ws_occ[1][kMaxDevices];  // idempotent lazy cache
-    const int var = 0;
-    const auto ws_kern = hdr_ws_kernel<8>;
+    static std::atomic<int> ws_occ[4][kMaxDevices];  // idempotent lazy cache
+    const char* dbg = getenv("WG_HDR_DBG");  // timing experiments only (output invalid)
+    const int var = dbg ? std::min(std::max(atoi(dbg), 0), 3) : 0;
+    const auto ws_kern = var == 1 ? hdr_ws_kernel<8, 1> : var == 2 ? hdr_ws_kernel<8, 2> : var == 3 ? hdr_ws_kernel<8, 3> : hdr_ws_kernel<8, 0>;
     if (ws_ok && ws_enabled()) {
         if (!ws_occ[var][device]) {
             int coop = 0, occ = 0;
@@ -928,9 +1236,21 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
             U8Consts kk = k;
             float mm = midpoint, ss = slope;
             Theta th = theta;
-            void* args[] = {&rgb, &out, &wring, &wparts, &wcounts, &n, &ppi, &nring, &kk, &mm, &ss, &th};
-            e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(ws_kern), dim3(grid), dim3(kWsT), args,
-                                            0, st);
+            int pf = kWsPrefetchWaves;
+            if (const char* e = getenv("WG_HDR_PF")) pf = atoi(e);  // tuning knob (scripts/ab_tone.py)
+            // TMEM staging when a CTA's per-image range fits one TMEM slot
+            const int64_t max_quads = (lines + grid - 1) / grid * (kWsLinePx / 4);
+            const char* tm_env = getenv("WG_HDR_TMEM");
+            const bool tm = max_quads <= kTmMaxQuads && !(tm_env && std::strcmp(tm_env, "0") == 0) && var == 0;
+            if (tm) {
+                void* targs[] = {&rgb, &out, &wparts, &wcounts, &n, &ppi, &kk, &mm, &ss, &th, &pf};
+                e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(hdr_tm_kernel<8>), dim3(grid),
+                                                dim3(kWsT), targs, 0, st);
+            } else {
+                void* args[] = {&rgb, &out, &wring, &wparts, &wcounts, &n, &ppi, &nring, &kk, &mm, &ss, &th, &pf};
+                e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(ws_kern), dim3(grid), dim3(kWsT),
+                                                args, 0, st);
+            }
             if (e != cudaSuccess) {
                 cudaGetLastError();
                 return set_error(static_cast<int>(e), "hdr: cooperative launch: %s", cudaGetErrorString(e));

@@ -26,7 +26,7 @@ import paper_2108_13656_b200 as wg  # noqa: E402
 from paper_2108_13656_b200 import synth  # noqa: E402
 
 KEYS = {"GRID": "WG_LDG_GRID_PER_SM", "ROUTE": "WG_TONE_ROUTE", "XK": "WG_TONE_EXACT_KERNEL",
-        "LP": "WG_LHE_PLANE"}
+        "LP": "WG_LHE_PLANE", "PF": "WG_HDR_PF", "SCHED": "WG_HDR_SCHEDULE", "RING": "WG_HDR_RING_MB", "DBG": "WG_HDR_DBG", "TM": "WG_HDR_TMEM"}
 
 
 def main():
@@ -36,13 +36,15 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--configs", default="ROUTE=linear")
-    ap.add_argument("--op", default="tone", choices=("tone", "decolor", "tone_exact", "local"))
+    ap.add_argument("--op", default="tone", choices=("tone", "decolor", "tone_exact", "local", "hdr"))
     ap.add_argument("--sleep", type=float, default=0.0)
     ap.add_argument("--lib", default=None, help="load this build of the library (cross-build A/B)")
     args = ap.parse_args()
     if args.lib:
         wg._lib.load(args.lib)
     dev = torch.device("cuda", 0)
+    if args.op == "hdr":
+        args.workload = "C4"
     wl = synth.WORKLOADS[args.workload]
     rgb = synth.make_batch(wl, dev, n_images=args.images)
     out = torch.empty(rgb.shape[:-1], dtype=torch.uint8, device=dev)
@@ -55,6 +57,7 @@ def main():
                               dtype=torch.uint8, device=dev)
     op = {"tone": lambda: wg.decolor_tone(rgb, out=out), "decolor": lambda: wg.decolor(rgb, out=out),
           "tone_exact": lambda: wg.decolor_tone(rgb, out=out, exact=True),
+          "hdr": lambda: wg.hdr_tonemap(rgb, out=out),
           "local": lambda: wg.decolor_tone_local(img4, grid=grid, scratch=scratch,
                                                  out=out.view(args.images, wl.height, wl.width))}[args.op]
     tone_ref = op().clone()
@@ -82,9 +85,10 @@ def main():
             os.environ[KEYS[k]] = v
 
     res = {"decolor": []}
+    gray = torch.empty(rgb.shape[:-1], dtype=rgb.dtype, device=dev) if args.op == "hdr" else out
     for r in range(args.rounds):
         setenv({})
-        res["decolor"].append(timed(lambda: wg.decolor(rgb, out=out)))
+        res["decolor"].append(timed(lambda: wg.decolor(rgb, out=gray)))
         for cfg in configs:
             setenv(cfg)
             name = ",".join(f"{k}={v}" for k, v in cfg.items()) or "default"
@@ -98,7 +102,7 @@ def main():
     for name, v in res.items():
         m = statistics.median(v)
         print(json.dumps({"kernel": name, "gpix_s": round(m, 1), "vs_decolor": round(m / base, 3),
-                          "frac_4Bpx": round(m * 4 / 6545.3, 3), "all": [round(x, 1) for x in v]}))
+                          "frac": round(m * (13 if args.op == "hdr" else 4) / 6545.3, 3), "all": [round(x, 1) for x in v]}))
 
 
 if __name__ == "__main__":
