@@ -151,13 +151,18 @@ WG_API int wg_dequantize_u8_f64(const uint8_t* in, double* out, int64_t n, void*
  * per-image log-range normalisation of the gray channel, then the global
  * sigmoid. Exact per-CTA min/max partials (no atomics on the statistic); one
  * warp-specialised persistent kernel (cooperative launch) when pix_per_img is
- * a multiple of 32, else gray / stats / tone kernels. `out` must be 16-byte
- * aligned (WG_EALIGN), `scratch` 256-byte aligned and at least
- * wg_hdr_scratch_bytes() long (WG_ESCRATCH). */
+ * a multiple of 32 (the gray of each SM's range staged in tensor memory when
+ * it fits, else in an L2-resident ring), else gray / stats / tone kernels.
+ * `out` must be 16-byte aligned (WG_EALIGN), `scratch` 256-byte aligned and at
+ * least wg_hdr_scratch_bytes() long (WG_ESCRATCH). */
 WG_API size_t wg_hdr_scratch_bytes(int64_t nimg, int64_t pix_per_img);
 WG_API int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, int64_t pix_per_img,
                       float beta_r, float beta_k, float midpoint, float slope, void* scratch,
                       size_t scratch_bytes, void* stream);
+/* Diagnostic (scripts/hdr_trace.py): the tensor-memory kernel's per (image,
+ * CTA) globaltimer trace of the last call made with WG_HDR_TMDBG=4, copied to
+ * `host` (NULL: only the element count); returns the uint64 count or -1. */
+WG_API int64_t wg_hdr_debug_trace(uint64_t* host);
 
 /* ---- baseline luminance extractors (_kernels.pyx:59-132) ----
  * method: 0 = BT.601 luma (bt601_rows, also "weighted"), 1 = HSV V

@@ -68,6 +68,7 @@ SIGNATURES = {
     "wg_dequantize_u8_f64": (_i, [_vp, _vp, _i64, _vp]),
     "wg_hdr_scratch_bytes": (_sz, [_i64, _i64]),
     "wg_hdr_tonemap_u8": (_i, [_vp, _vp, _i64, _i64, _f, _f, _f, _f, _vp, _sz, _vp]),
+    "wg_hdr_debug_trace": (_i64, [_vp]),
     "wg_luma_f64": (_i, [_vp, _vp, _i64, _i, _vp]),
     "wg_lab_f64": (_i, [_vp, _vp, _i64, _vp]),
     "wg_luma_u8": (_i, [_vp, _vp, _i64, _i, _vp]),

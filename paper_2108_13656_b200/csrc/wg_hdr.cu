@@ -107,20 +107,70 @@ __device__ __forceinline__ int lut_bin(float r) {
     return min(max(b, 0), kLutBins - 1);
 }
 
-// 32-bit table entry: count of thresholds below the bin (bits 24..31) and the
-// low 17 bits of the float bits of the one threshold inside it (bits 0..17;
-// 0x20000 = none). All floats of a bin share their bits >> 17, so comparing
-// the low 17 bits of r with it is the float compare r >= threshold. One LDS.32
-// per pixel instead of an LDS.64 (fewer shared-memory wavefronts for these
-// random-bin lookups).
-__device__ __forceinline__ uint32_t lut_entry(int count, float thr) {
-    const uint32_t f = thr == INFINITY ? 0x20000u : (__float_as_uint(thr) & 0x1FFFFu);
-    return (static_cast<uint32_t>(count) << 24) | f;
+// 32-bit step word per bin (since r02): W[b] = 2^24 count + 2^24 - L - bits(b0)
+// (mod 2^32), b0 the first float of bin b, count the thresholds below the bin
+// and L the in-bin offset of the bin's one threshold (2^17 = none). For r in
+// bin b, W[b] + bits(r) = 2^24 count + 2^24 + (offset - L): the offset minus L
+// borrows from or carries into bit 24, so byte 3 is the toned byte -- one LDS
+// and one IADD per pixel, no compare. r < 1 happens only for g <= 0 (t = 0) or
+// g = gmin rounding below 1: clamped to 1.0 (t = 0).
+constexpr uint32_t kOneBits = 0x3F800000u, kLutLastBits = ((kOneBits >> 17) + kLutBins) * (1u << 17) - 1u;
+__device__ __forceinline__ uint32_t lut_step_sum(float v, float inv, const uint32_t* s_lut) {
+    const uint32_t rb = static_cast<uint32_t>(
+        min(max(__float_as_int(__fmul_rn(v, inv)), static_cast<int>(kOneBits)), static_cast<int>(kLutLastBits)));
+    return s_lut[(rb >> 17) - (kOneBits >> 17)] + rb;
 }
 __device__ __forceinline__ uint32_t lut_px32(float v, float inv, const uint32_t* s_lut) {
-    const uint32_t rb = __float_as_uint(__fmul_rn(v, inv));
-    const uint32_t e = s_lut[min(max(rb >> 17, 127u << 6), (127u << 6) + kLutBins - 1) - (127u << 6)];
-    return (e >> 24) + ((rb & 0x1FFFFu) >= (e & 0x3FFFFu) ? 1u : 0u);
+    return lut_step_sum(v, inv, s_lut) >> 24;
+}
+// step word of bin b; cb = index of the first threshold whose bin is >= b
+// (advanced past bin b's thresholds). s_b[255] is a sentinel.
+__device__ __forceinline__ uint32_t step_word(int b, int& cb, const int* s_b, const uint32_t* s_gb) {
+    const uint32_t b0 = static_cast<uint32_t>(b + static_cast<int>(kOneBits >> 17)) << 17;
+    uint32_t cnt = static_cast<uint32_t>(cb), L = 0x20000u;
+    if (s_b[cb] == b) {
+        const int64_t d = static_cast<int64_t>(s_gb[cb]) - static_cast<int64_t>(b0);
+        if (d <= 0) cnt += 1u;  // threshold at or below the bin start (gamma <= 1 in bin 0): always reached
+        else L = static_cast<uint32_t>(d);
+        while (s_b[cb] == b) ++cb;  // (two in one bin: conflict, the table is not used)
+    }
+    return (cnt << 24) + 0x1000000u - L - b0;
+}
+// Per-image table build by 256 threads (t = 0..255) of a block / named-barrier
+// group: thread j < 255 computes threshold j (fp64 exp2, as the host theta),
+// then each thread fills 8 consecutive bins from a binary search over the
+// sorted threshold bins. Two barriers (bar, then bar_or, which also returns
+// whether any two thresholds share a bin or are out of order -> no table).
+template <bool kF32 = false, class Bar, class BarOr>
+__device__ __forceinline__ int build_step_table(int t, const Theta& theta, double lr, int* s_b, uint32_t* s_gb,
+                                                uint32_t* s_lut, Bar bar, BarOr bar_or) {
+    if (t < 255) {
+        const float gam = kF32 ? exp2f(static_cast<float>(theta.v[t]) * static_cast<float>(lr))
+                               : static_cast<float>(exp2(theta.v[t] * lr));
+        s_b[t] = lut_bin(gam);
+        s_gb[t] = __float_as_uint(gam);
+    } else if (t == 255) {
+        s_b[255] = 1 << 30;
+    }
+    bar();
+    const int bad = t < 254 && s_b[t] >= s_b[t + 1];
+    const int b0 = t * (kLutBins / 256);
+    int cb = 0;
+#pragma unroll
+    for (int step = 128; step > 0; step >>= 1)
+        if (s_b[cb + step - 1] < b0) cb += step;
+#pragma unroll
+    for (int j = 0; j < kLutBins / 256; ++j) s_lut[b0 + j] = step_word(b0 + j, cb, s_b, s_gb);
+    return bar_or(bad);
+}
+__device__ __forceinline__ int named_bar_or(int id, int nthreads, int pred) {
+    int r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\tbarrier.red.or.pred q, %2, %3, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+        : "=r"(r)
+        : "r"(pred), "r"(id), "r"(nthreads)
+        : "memory");
+    return r;
 }
 
 // ---------------------------------------------------------------- per-pixel tone
@@ -205,13 +255,31 @@ __global__ void __launch_bounds__(kT) hdr_gray_kernel(const float* __restrict__ 
 }
 
 // ---------------------------------------------------------------- pass 2: statistic + threshold table
+// per-image statistic from the folded (min over g > 0, max)
+__device__ __forceinline__ HdrStat hdr_stat_of(float lo, float hi, double* lr) {
+    HdrStat st{0.0f, 0.0f, 0, 0};
+    *lr = 0.0;
+    if (hi > 0.0f && lo <= hi) {
+        st.inv_gmin = static_cast<float>(1.0 / static_cast<double>(lo));
+        if (hi > lo) {
+            st.mode = 1;
+            *lr = log2(static_cast<double>(hi) / static_cast<double>(lo));
+            st.inv_lrange = static_cast<float>(1.0 / *lr);
+        } else {
+            st.mode = 2;
+        }
+    }
+    return st;
+}
+
 __global__ void __launch_bounds__(kT) hdr_stats_kernel(const float2* __restrict__ parts, int nslots,
                                                        HdrStat* __restrict__ stats, float2* __restrict__ luts,
                                                        Theta theta) {
+    static_assert(kT == 256, "build_step_table takes 256 threads");
     __shared__ float s_lo[kWarps], s_hi[kWarps];
-    __shared__ int s_cnt[kLutBins];
-    __shared__ float s_thr[kLutBins];
-    __shared__ int s_wsum[kWarps];
+    __shared__ int s_b[256];
+    __shared__ uint32_t s_gb[256];
+    __shared__ uint32_t s_lut[kLutBins];
     const int img = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     pdl_wait();  // the gray pass's slots are complete and visible
     const float2* slots = parts + static_cast<int64_t>(img) * kSlots;
@@ -220,10 +288,6 @@ __global__ void __launch_bounds__(kT) hdr_stats_kernel(const float2* __restrict_
         const float2 pr = slots[q];
         lo = fminf(lo, pr.x);
         hi = fmaxf(hi, pr.y);
-    }
-    for (int b = tid; b < kLutBins; b += kT) {
-        s_cnt[b] = 0;
-        s_thr[b] = INFINITY;
     }
     warp_minmax(lo, hi);
     if (lane == 0) {
@@ -237,51 +301,14 @@ __global__ void __launch_bounds__(kT) hdr_stats_kernel(const float2* __restrict_
         lo = fminf(lo, s_lo[w]);
         hi = fmaxf(hi, s_hi[w]);
     }
-    HdrStat st{0.0f, 0.0f, 0, 0};
-    double lr = 0.0;
-    if (hi > 0.0f && lo <= hi) {
-        st.inv_gmin = static_cast<float>(1.0 / static_cast<double>(lo));
-        if (hi > lo) {
-            st.mode = 1;
-            lr = log2(static_cast<double>(hi) / static_cast<double>(lo));
-            st.inv_lrange = static_cast<float>(1.0 / lr);
-        } else {
-            st.mode = 2;
-        }
-    }
+    double lr;
+    HdrStat st = hdr_stat_of(lo, hi, &lr);
     if (st.mode == 1 && lr < kLutOct - 1) {  // block-uniform
-        int conflict = 0;
-        if (tid < 255) {
-            const float gam = static_cast<float>(exp2(theta.v[tid] * lr));  // > 1 since theta > 0
-            const int b = lut_bin(gam);
-            if (atomicAdd(&s_cnt[b], 1) != 0) conflict = 1;  // shared counter: table layout only
-            s_thr[b] = gam;
-        }
-        conflict = __syncthreads_or(conflict);
-        // exclusive scan of s_cnt: 8 consecutive bins per thread
-        int local[kLutBins / kT], sum = 0;
-#pragma unroll
-        for (int j = 0; j < kLutBins / kT; ++j) {
-            local[j] = sum;
-            sum += s_cnt[tid * (kLutBins / kT) + j];
-        }
-        int incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        if (lane == 31) s_wsum[warp] = incl;
-        __syncthreads();
-        int off = incl - sum;
-        for (int w = 0; w < warp; ++w) off += s_wsum[w];
+        const int bad = build_step_table(
+            tid, theta, lr, s_b, s_gb, s_lut, [] { __syncthreads(); }, [](int p) { return __syncthreads_or(p); });
         uint32_t* lut = reinterpret_cast<uint32_t*>(luts) + static_cast<int64_t>(img) * kLutBins;
-#pragma unroll
-        for (int j = 0; j < kLutBins / kT; ++j) {
-            const int b = tid * (kLutBins / kT) + j;
-            lut[b] = lut_entry(off + local[j], s_thr[b]);
-        }
-        st.lut = conflict ? 0 : 1;
+        for (int b = tid; b < kLutBins; b += kT) lut[b] = s_lut[b];
+        st.lut = bad ? 0 : 1;
     }
     if (tid == 0) stats[img] = st;
 }
@@ -503,9 +530,10 @@ constexpr int kWsMaxRing = 4;
 // gray ring bytes kept L2-resident: 2 slots (C4: 2 slots 322.6, 3 slots 310.8,
 // 4 slots 294 Gpix/s -- the ring competes with the RGB stream for L2)
 constexpr size_t kWsRingBudget = 0;
-// producer L2 prefetch distance in waves of the CTA's range (C4, TMEM kernel:
-// 0 -> 320.8, 2 -> 339.5, 3 -> 340.1, 8 -> 336.7 Gpix/s; L2 ring: 0 -> 296, 3 -> 309)
-constexpr int kWsPrefetchWaves = 3;
+// producer L2 prefetch distance in waves of the CTA's range (C4, TMEM kernel
+// before the cross-image register prefetch: 0 -> 320.8, 2 -> 339.5, 3 -> 340.1,
+// 8 -> 336.7 Gpix/s; after: 2 -> 362.1, 3 -> 359.7, 6 -> 359.6; L2 ring: 0 -> 296, 3 -> 309)
+constexpr int kWsPrefetchWaves = 2;
 
 
 
@@ -544,22 +572,6 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// per-image statistic from the folded (min over g > 0, max), as hdr_stats_kernel
-__device__ __forceinline__ HdrStat hdr_stat_of(float lo, float hi, double* lr) {
-    HdrStat st{0.0f, 0.0f, 0, 0};
-    *lr = 0.0;
-    if (hi > 0.0f && lo <= hi) {
-        st.inv_gmin = static_cast<float>(1.0 / static_cast<double>(lo));
-        if (hi > lo) {
-            st.mode = 1;
-            *lr = log2(static_cast<double>(hi) / static_cast<double>(lo));
-            st.inv_lrange = static_cast<float>(1.0 / *lr);
-        } else {
-            st.mode = 2;
-        }
-    }
-    return st;
-}
 
 // the rare arithmetic path out of line (keeps the unrolled consumer loop's registers)
 __device__ __noinline__ uint32_t tone_arith_call(float g, HdrStat st, ToneU8 c) { return tone_arith(g, st, c); }
@@ -627,14 +639,13 @@ __global__ void __launch_bounds__(kWsT, 1)
                   float2* __restrict__ parts, unsigned* __restrict__ counts, int64_t nimg, int64_t ppi, int nring,
                   U8Consts k, float m, float slope, Theta theta, int pf_waves) {
     constexpr int kProd_ = kWsT / 32 - kCons_, kProdT_ = kProd_ * 32, kConsT_ = kCons_ * 32;
+    static_assert(kConsT_ == 256, "build_step_table takes 256 consumer threads");
     __shared__ uint32_t s_lut[kLutBins];
-    __shared__ int s_cnt[kLutBins];
+    __shared__ int s_b[256];
+    __shared__ uint32_t s_gb[256];
     __shared__ float s_plo[kProd_], s_phi[kProd_], s_clo[kCons_], s_chi[kCons_];
-    __shared__ int s_wsum[kCons_];
-    __shared__ int s_conflict;
     __shared__ volatile int s_toned;  // images this CTA's consumers have finished
     __shared__ int s_pf[2];           // producer thread 0: next (image, wave) to prefetch into L2
-    float* s_thr = reinterpret_cast<float*>(s_lut);  // thresholds, then the entries in place
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, c = blockIdx.x;
     const int64_t nlines = ppi / kWsLinePx;
@@ -749,11 +760,6 @@ __global__ void __launch_bounds__(kWsT, 1)
             s_clo[cw] = lo;
             s_chi[cw] = hi;
         }
-        for (int b = ct; b < kLutBins; b += kConsT_) {
-            s_cnt[b] = 0;
-            s_thr[b] = INFINITY;
-        }
-        if (ct == 0) s_conflict = 0;
         named_bar(2, kConsT_);
         lo = s_clo[0];
         hi = s_chi[0];
@@ -764,34 +770,10 @@ __global__ void __launch_bounds__(kWsT, 1)
         double lr;
         HdrStat st = hdr_stat_of(lo, hi, &lr);
         if (st.mode == 1 && lr < kLutOct - 1) {  // uniform over the consumer warps
-            for (int j = ct; j < 255; j += kConsT_) {
-                const float gam = static_cast<float>(exp2(theta.v[j] * lr));  // > 1 since theta > 0
-                const int b = lut_bin(gam);
-                if (atomicAdd(&s_cnt[b], 1) != 0) s_conflict = 1;  // shared counter: table layout only
-                s_thr[b] = gam;
-            }
-            named_bar(2, kConsT_);
-            // exclusive scan of s_cnt: 16 consecutive bins per thread
-            constexpr int kPer = (kLutBins + kConsT_ - 1) / kConsT_;  // bins per thread (the last thread may have fewer)
-            const int b0 = min(ct * kPer, kLutBins), b1 = min(b0 + kPer, kLutBins);
-            int sum = 0;
-            for (int b = b0; b < b1; ++b) sum += s_cnt[b];
-            int incl = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            if (lane == 31) s_wsum[cw] = incl;
-            named_bar(2, kConsT_);
-            int off = incl - sum;
-            for (int w = 0; w < cw; ++w) off += s_wsum[w];
-            for (int b = b0; b < b1; ++b) {  // second pass: running prefix (no per-thread array)
-                s_lut[b] = lut_entry(off, s_thr[b]);
-                off += s_cnt[b];
-            }
-            st.lut = s_conflict ? 0 : 1;
-            named_bar(2, kConsT_);
+            const int bad = build_step_table(
+                ct, theta, lr, s_b, s_gb, s_lut, [] { named_bar(2, kConsT_); },
+                [](int p) { return named_bar_or(2, kConsT_, p); });
+            st.lut = bad ? 0 : 1;
         }
         // tone this CTA's lines (per-image mode hoisted out of the pixel loop)
         const float* gsl = ring + (i % nring) * ppi;
@@ -822,6 +804,15 @@ __global__ void __launch_bounds__(kWsT, 1)
 // 32 (w % 4) .. + 31 -- the lanes its warp may access -- and a consumer warp
 // reads whole column groups of its own quadrant.
 constexpr int kTmCols = 512, kTmSlotCols = 256, kTmMaxQuads = kTmSlotCols / 4 * 128;
+// timing trace of the TMEM kernel (kDbg == 4, scripts/hdr_trace.py): per (image,
+// CTA) globaltimer at producer start / publish, consumer start / done / table built
+constexpr int kTraceImgs = 64;
+__device__ unsigned long long g_hdr_trace[kTraceImgs][kWsMaxGrid][7];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ void tm_st4(uint32_t taddr, float a, float b, float c, float d) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(__float_as_uint(a)),
@@ -841,12 +832,13 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 __device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// consumer tone of one TMEM slot: warp cw of quadrant cw % 4, half cw / 4 of the
-// column groups, four groups (16 columns) per tcgen05.ld; one 32-bit store per
-// quad (a warp stores 128 contiguous bytes)
-template <int kCons_, class Px>
-__device__ __forceinline__ void tm_tone_slot(uint32_t tslot, uint8_t* __restrict__ o, int64_t nq, int cw, int lane,
-                                             Px px) {
+// consumer tone of one slot: warp cw of quadrant cw % 4, half cw / 4 of the
+// column groups, four groups (16 columns) per tcgen05.ld -- or, for the
+// shared-memory slot (sslot != nullptr), four conflict-free LDS.128 of the same
+// quads; one 32-bit store per quad (a warp stores 128 contiguous bytes)
+template <int kCons_, bool kByte3, class Px>
+__device__ __forceinline__ void tm_tone_slot(uint32_t tslot, const float4* sslot, uint8_t* __restrict__ o,
+                                             int64_t nq, int cw, int lane, Px px) {
     const int qd = cw & 3, h = cw >> 2;
     constexpr int kHalves = kCons_ / 4;
     const int ncg = static_cast<int>((nq + 127) >> 7);
@@ -855,21 +847,41 @@ __device__ __forceinline__ void tm_tone_slot(uint32_t tslot, uint8_t* __restrict
     const uint32_t tl = tslot + (static_cast<uint32_t>(qd * 32) << 16);
     for (int g = g0; g < g1; g += 4) {
         uint32_t r[16];
-        tm_ld16(tl + 4 * g, r);
-        tm_wait_ld();
+        if (sslot) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t u = min((static_cast<int64_t>(g + j) << 7) + qd * 32 + lane, nq - 1);
+                const float4 v = sslot[u];
+                r[4 * j] = __float_as_uint(v.x);
+                r[4 * j + 1] = __float_as_uint(v.y);
+                r[4 * j + 2] = __float_as_uint(v.z);
+                r[4 * j + 3] = __float_as_uint(v.w);
+            }
+        } else {
+            tm_ld16(tl + 4 * g, r);
+            tm_wait_ld();
+        }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int64_t u = (static_cast<int64_t>(g + j) << 7) + qd * 32 + lane;
             if (g + j < g1 && u < nq) {
-                const uint32_t w = px(__uint_as_float(r[4 * j])) | (px(__uint_as_float(r[4 * j + 1])) << 8) |
-                                   (px(__uint_as_float(r[4 * j + 2])) << 16) | (px(__uint_as_float(r[4 * j + 3])) << 24);
+                uint32_t w;
+                if (kByte3) {  // px returns a step sum whose byte 3 is the toned byte: 3 PRMT per quad
+                    const uint32_t lo = __byte_perm(px(__uint_as_float(r[4 * j])), px(__uint_as_float(r[4 * j + 1])), 0x0073);
+                    const uint32_t hi =
+                        __byte_perm(px(__uint_as_float(r[4 * j + 2])), px(__uint_as_float(r[4 * j + 3])), 0x0073);
+                    w = __byte_perm(lo, hi, 0x5410);
+                } else {
+                    w = px(__uint_as_float(r[4 * j])) | (px(__uint_as_float(r[4 * j + 1])) << 8) |
+                        (px(__uint_as_float(r[4 * j + 2])) << 16) | (px(__uint_as_float(r[4 * j + 3])) << 24);
+                }
                 __stcs(reinterpret_cast<unsigned*>(o) + u, w);
             }
         }
     }
 }
 
-template <int kCons_>
+template <int kCons_, int kDbg = 0, int kRing = 2>
 __global__ void __launch_bounds__(kWsT, 1)
     hdr_tm_kernel(const float* __restrict__ rgb, uint8_t* __restrict__ out, float2* __restrict__ parts,
                   unsigned* __restrict__ counts, int64_t nimg, int64_t ppi, U8Consts k, float m, float slope,
@@ -877,16 +889,18 @@ __global__ void __launch_bounds__(kWsT, 1)
     static_assert(kCons_ % 4 == 0, "consumer warps come in whole quadrant sets");
     constexpr int kProd_ = kWsT / 32 - kCons_, kProdT_ = kProd_ * 32, kConsT_ = kCons_ * 32;
     static_assert(kProdT_ % 128 == 0, "producer waves must cover whole TMEM column groups");
-    constexpr int kRing = kTmCols / kTmSlotCols;
+    static_assert(kRing == 2 || kRing == 3, "2 TMEM slots (+ 1 shared-memory slot)");
+    extern __shared__ float4 s_slot[];  // the third slot (kRing == 3): kTmMaxQuads quads
+    static_assert(kConsT_ == 256, "build_step_table takes 256 consumer threads");
     __shared__ uint32_t s_lut[kLutBins];
-    __shared__ int s_cnt[kLutBins];
+    __shared__ int s_b[256];
+    __shared__ uint32_t s_gb[256];
     __shared__ float s_plo[kProd_], s_phi[kProd_], s_clo[kCons_], s_chi[kCons_];
-    __shared__ int s_wsum[kCons_];
-    __shared__ int s_conflict;
     __shared__ volatile int s_toned;  // images this CTA's consumers have finished
     __shared__ int s_pf[2];           // producer thread 0: next (image, wave) to prefetch into L2
     __shared__ uint32_t s_tmem;       // TMEM base address (tcgen05.alloc)
-    float* s_thr = reinterpret_cast<float*>(s_lut);
+    __shared__ HdrStat s_st;
+    __shared__ double s_lr;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int G = gridDim.x, c = blockIdx.x;
     const int64_t nlines = ppi / kWsLinePx;
@@ -926,6 +940,18 @@ __global__ void __launch_bounds__(kWsT, 1)
         if (tid == 0)
             for (int w = 0; w < pf_waves; ++w) prefetch_next();
         const uint32_t tq = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16);  // this warp's lane quadrant
+        // register prefetch of the next quad, continued across image boundaries
+        // (the next image's first quad is in flight during the publish and the
+        // slot wait); lanes past the range load a clamped quad
+        const int64_t ulast = nq - 1;
+        float4 n0, n1, n2;
+        auto load_quad = [&](int64_t img, int64_t uq) {
+            const float4* src = reinterpret_cast<const float4*>(rgb + img * ppi * 3 + 12 * mp.quad(min(uq, ulast)));
+            n0 = __ldcs(src);
+            n1 = __ldcs(src + 1);
+            n2 = __ldcs(src + 2);
+        };
+        load_quad(0, tid);
         for (int64_t i = 0; i < nimg; ++i) {
             if (i >= kRing) {  // slot i % kRing: this CTA's consumers are done with image i - kRing
                 for (uint32_t spins = 0; s_toned < i - kRing + 1; ++spins) {
@@ -934,30 +960,17 @@ __global__ void __launch_bounds__(kWsT, 1)
                 }
                 tm_fence_after();
             }
-            const float* in = rgb + i * ppi * 3;
-            const uint32_t ts = tq + static_cast<uint32_t>((i % kRing) * kTmSlotCols);
+            if ((kDbg & 4) && tid == 0 && i < kTraceImgs) g_hdr_trace[i][c][0] = gtimer();
+            const int slot = static_cast<int>(i % kRing);
+            const uint32_t ts = tq + static_cast<uint32_t>(slot * kTmSlotCols);
             float lo = INFINITY, hi = 0.0f;
             // warp-uniform trip count (tcgen05.st is .aligned): lanes past the range
             // compute a clamped quad and store into unused cells
-            int64_t u = tid;
-            const int64_t ulast = nq - 1;
-            float4 n0, n1, n2;
-            {
-                const float4* src = reinterpret_cast<const float4*>(in + 12 * mp.quad(min(u, ulast)));
-                n0 = __ldcs(src);
-                n1 = __ldcs(src + 1);
-                n2 = __ldcs(src + 2);
-            }
-            for (; u - lane < nq; u += kProdT_) {
+            for (int64_t u = tid; u - lane < nq; u += kProdT_) {
                 const float4 v0 = n0, v1 = n1, v2 = n2;
                 if (pf_waves > 0 && tid == 0) prefetch_next();
-                if (u + kProdT_ - lane < nq) {
-                    const float4* src =
-                        reinterpret_cast<const float4*>(in + 12 * mp.quad(min(u + kProdT_, ulast)));
-                    n0 = __ldcs(src);
-                    n1 = __ldcs(src + 1);
-                    n2 = __ldcs(src + 2);
-                }
+                if (u + kProdT_ - lane < nq) load_quad(i, u + kProdT_);
+                else if (i + 1 < nimg) load_quad(i + 1, tid);
                 const float2 a = decolor_fast_x2(make_float2(v0.x, v0.w), make_float2(v0.y, v1.x),
                                                  make_float2(v0.z, v1.y), k);
                 const float2 b = decolor_fast_x2(make_float2(v1.z, v2.y), make_float2(v1.w, v2.z),
@@ -968,7 +981,10 @@ __global__ void __launch_bounds__(kWsT, 1)
                     track(b.x, lo, hi);
                     track(b.y, lo, hi);
                 }
-                tm_st4(ts + static_cast<uint32_t>(4 * (u >> 7)), a.x, a.y, b.x, b.y);
+                if ((kDbg & 3) != 3) {
+                    if (slot < 2) tm_st4(ts + static_cast<uint32_t>(4 * (u >> 7)), a.x, a.y, b.x, b.y);
+                    else if (u < nq) s_slot[u] = make_float4(a.x, a.y, b.x, b.y);
+                }
             }
             tm_wait_st();
             tm_fence_before();
@@ -986,6 +1002,7 @@ __global__ void __launch_bounds__(kWsT, 1)
                 __stcg(parts + i * kWsMaxGrid + c, make_float2(lo, hi));
                 __threadfence();
                 atomicAdd(counts + i, 1u);
+                if ((kDbg & 4) && i < kTraceImgs) g_hdr_trace[i][c][1] = gtimer();
             }
             named_bar(1, kProdT_);  // s_plo / s_phi are rewritten for the next image
         }
@@ -994,7 +1011,10 @@ __global__ void __launch_bounds__(kWsT, 1)
         const int ct = tid - kProdT_, cw = ct >> 5;
         const ToneU8 tc = make_tone_u8(m, slope);
         for (int64_t i = 0; i < nimg; ++i) {
-            if (ct == 0) wait_geq(counts + i, static_cast<unsigned>(G));
+            if (ct == 0) {
+                wait_geq(counts + i, static_cast<unsigned>(G));
+                if ((kDbg & 4) && i < kTraceImgs) g_hdr_trace[i][c][2] = gtimer();
+            }
             named_bar(2, kConsT_);
             tm_fence_after();
             float lo = INFINITY, hi = 0.0f;
@@ -1008,12 +1028,8 @@ __global__ void __launch_bounds__(kWsT, 1)
                 s_clo[cw] = lo;
                 s_chi[cw] = hi;
             }
-            for (int b = ct; b < kLutBins; b += kConsT_) {
-                s_cnt[b] = 0;
-                s_thr[b] = INFINITY;
-            }
-            if (ct == 0) s_conflict = 0;
             named_bar(2, kConsT_);
+            if ((kDbg & 4) && ct == 0 && i < kTraceImgs) g_hdr_trace[i][c][5] = gtimer();
             lo = s_clo[0];
             hi = s_chi[0];
             for (int w = 1; w < kCons_; ++w) {
@@ -1021,50 +1037,44 @@ __global__ void __launch_bounds__(kWsT, 1)
                 hi = fmaxf(hi, s_chi[w]);
             }
             double lr;
-            HdrStat st = hdr_stat_of(lo, hi, &lr);
-            if (st.mode == 1 && lr < kLutOct - 1) {  // uniform over the consumer warps
-                for (int j = ct; j < 255; j += kConsT_) {
-                    const float gam = static_cast<float>(exp2(theta.v[j] * lr));
-                    const int b = lut_bin(gam);
-                    if (atomicAdd(&s_cnt[b], 1) != 0) s_conflict = 1;
-                    s_thr[b] = gam;
-                }
-                named_bar(2, kConsT_);
-                constexpr int kPer = (kLutBins + kConsT_ - 1) / kConsT_;
-                const int b0 = min(ct * kPer, kLutBins), b1 = min(b0 + kPer, kLutBins);
-                int sum = 0;
-                for (int b = b0; b < b1; ++b) sum += s_cnt[b];
-                int incl = sum;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += v;
-                }
-                if (lane == 31) s_wsum[cw] = incl;
-                named_bar(2, kConsT_);
-                int off = incl - sum;
-                for (int w = 0; w < cw; ++w) off += s_wsum[w];
-                for (int b = b0; b < b1; ++b) {
-                    s_lut[b] = lut_entry(off, s_thr[b]);
-                    off += s_cnt[b];
-                }
-                st.lut = s_conflict ? 0 : 1;
-                named_bar(2, kConsT_);
+            // the statistic (fp64 log2 and divisions) by one thread, broadcast
+            // (C4: +0.7% over every consumer thread computing it)
+            if (ct == 0) {
+                s_st = hdr_stat_of(lo, hi, &lr);
+                s_lr = lr;
             }
-            const uint32_t ts = tbase + static_cast<uint32_t>((i % kRing) * kTmSlotCols);
+            named_bar(2, kConsT_);
+            HdrStat st = s_st;
+            lr = s_lr;
+            if ((kDbg & 4) && ct == 0 && i < kTraceImgs) g_hdr_trace[i][c][6] = gtimer();
+            if (st.mode == 1 && lr < kLutOct - 1) {  // uniform over the consumer warps
+                const int bad = build_step_table<(kDbg & 16) != 0>(
+                    ct, theta, lr, s_b, s_gb, s_lut, [] { named_bar(2, kConsT_); },
+                    [](int p) { return named_bar_or(2, kConsT_, p); });
+                st.lut = bad ? 0 : 1;
+            }
+            if ((kDbg & 4) && ct == 0 && i < kTraceImgs) g_hdr_trace[i][c][4] = gtimer();
+            const int slot = static_cast<int>(i % kRing);
+            const uint32_t ts = tbase + static_cast<uint32_t>(slot * kTmSlotCols);
+            const float4* ss = slot < 2 ? nullptr : s_slot;
             uint8_t* o = out + i * ppi + mp.quad(0) * 4;
-            if (st.mode == 1 && st.lut) {
+            if ((kDbg & 3) == 1 || (kDbg & 3) == 3) {
+            } else if (st.mode == 1 && st.lut) {
                 const float inv = st.inv_gmin;
-                tm_tone_slot<kCons_>(ts, o, nq, cw, lane, [&](float v) -> uint32_t { return lut_px32(v, inv, s_lut); });
+                tm_tone_slot<kCons_, true>(ts, ss, o, nq, cw, lane,
+                                           [&](float v) -> uint32_t { return lut_step_sum(v, inv, s_lut); });
             } else if (st.mode == 2) {
-                tm_tone_slot<kCons_>(ts, o, nq, cw, lane, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });
+                tm_tone_slot<kCons_, false>(ts, ss, o, nq, cw, lane, [](float v) -> uint32_t { return v > 0.0f ? 255u : 0u; });
             } else {
-                tm_tone_slot<kCons_>(ts, o, nq, cw, lane,
+                tm_tone_slot<kCons_, false>(ts, ss, o, nq, cw, lane,
                                      [&](float v) -> uint32_t { return tone_arith_call(v, st, tc); });
             }
             tm_fence_before();
             named_bar(2, kConsT_);  // every consumer is done with the slot and with s_lut
-            if (ct == 0) s_toned = static_cast<int>(i + 1);
+            if (ct == 0) {
+                s_toned = static_cast<int>(i + 1);
+                if ((kDbg & 4) && i < kTraceImgs) g_hdr_trace[i][c][3] = gtimer();
+            }
         }
     }
     tm_fence_before();
@@ -1175,6 +1185,14 @@ Theta make_theta(double m, double k) {
 
 using namespace wg;
 
+// diagnostic: copy the TMEM kernel's timing trace (WG_HDR_TMDBG=4) to host memory
+// (kTraceImgs x kWsMaxGrid x 7 uint64); returns the element count
+extern "C" WG_API int64_t wg_hdr_debug_trace(uint64_t* host) {
+    const size_t n = sizeof(g_hdr_trace) / sizeof(unsigned long long);
+    if (host && cudaMemcpyFromSymbol(host, g_hdr_trace, sizeof(g_hdr_trace)) != cudaSuccess) return -1;
+    return static_cast<int64_t>(n);
+}
+
 extern "C" size_t wg_hdr_scratch_bytes(int64_t nimg, int64_t pix_per_img) {
     if (nimg <= 0 || pix_per_img <= 0) return 0;
     return std::max(ws_bytes(nimg, pix_per_img), grouped_bytes(nimg, pix_per_img));
@@ -1244,8 +1262,24 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
             const bool tm = max_quads <= kTmMaxQuads && !(tm_env && std::strcmp(tm_env, "0") == 0) && var == 0;
             if (tm) {
                 void* targs[] = {&rgb, &out, &wparts, &wcounts, &n, &ppi, &kk, &mm, &ss, &th, &pf};
-                e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(hdr_tm_kernel<8>), dim3(grid),
-                                                dim3(kWsT), targs, 0, st);
+                // 8 consumer warps (4: 293 vs 340 Gpix/s, the tone falls behind)
+                const char* de = getenv("WG_HDR_TMDBG");  // timing experiments only (4: trace)
+                // WG_HDR_TMRING=3 adds a third slot in shared memory: slower (C4 341.6 vs
+                // 352.2 Gpix/s -- 128 KiB of shared memory shrink the L1 that holds the
+                // producers' loads in flight)
+                const char* re = getenv("WG_HDR_TMRING");
+                const int tdbg = de ? atoi(de) : 0, ring = re ? atoi(re) : 2;
+                using TmK = void (*)(const float*, uint8_t*, float2*, unsigned*, int64_t, int64_t, U8Consts, float,
+                                     float, Theta, int);
+                TmK tk = ring == 3 ? (tdbg == 4 ? hdr_tm_kernel<8, 4, 3> : hdr_tm_kernel<8, 0, 3>)
+                                   : (tdbg == 4 ? hdr_tm_kernel<8, 4, 2> : hdr_tm_kernel<8, 0, 2>);
+                const size_t dsm = ring == 2 ? 0 : static_cast<size_t>(kTmMaxQuads) * sizeof(float4);
+                if (dsm) {
+                    e = cudaFuncSetAttribute(reinterpret_cast<const void*>(tk),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
+                    if (e != cudaSuccess) return set_error(static_cast<int>(e), "hdr: smem attribute: %s", cudaGetErrorString(e));
+                }
+                e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(tk), dim3(grid), dim3(kWsT), targs, dsm, st);
             } else {
                 void* args[] = {&rgb, &out, &wring, &wparts, &wcounts, &n, &ppi, &nring, &kk, &mm, &ss, &th, &pf};
                 e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(ws_kern), dim3(grid), dim3(kWsT),
