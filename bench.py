@@ -167,7 +167,7 @@ def op_spec(wl, op: str) -> dict:
         return {"kernel": "ldg_stream_kernel<OpDecolorF32>", "bytes_per_px": 16, "launches": 1,
                 "api": "decolor (wg_decolor_f32)", "e2e_api": "decolor_host -> wg_host_decolor_f32",
                 "io": "float32->gray float32"}
-    return {"kernel": "hdr_ws_kernel", "bytes_per_px": wl.bytes_per_px,
+    return {"kernel": "hdr_tm_kernel", "bytes_per_px": wl.bytes_per_px,
             "launches": 1, "api": "hdr_tonemap (wg_hdr_tonemap_u8)",
             "e2e_api": "hdr_tonemap_host -> wg_host_hdr_tonemap_u8", "io": "float32 radiance->uint8 (HDR adapter)"}
 

@@ -36,7 +36,7 @@ $T > $OUT/ncu_plain3.log 2>&1 && \
 echo "ncu_full_tone=$?"
 H="python bench.py --workload C4 --steps 2 --warmup 3 --no-e2e --no-cpu --no-sustained"
 $H > $OUT/ncu_plain4.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"hdr_ws_kernel" -s 3 -c 1 -o $OUT/prof_c4_hdr $H > $OUT/ncu_full_hdr.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"hdr_tm_kernel" -s 3 -c 1 -o $OUT/prof_c4_hdr $H > $OUT/ncu_full_hdr.log 2>&1
 echo "ncu_full_hdr=$?"
 # local tone map (C3 frames): per-kernel split and full captures of its two per-pixel kernels
 timeout 300 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.per_cycle_active \

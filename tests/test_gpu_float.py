@@ -272,9 +272,11 @@ def test_hdr_c4_images(torch_dev):
 
 def test_hdr_schedules_agree(torch_dev, monkeypatch):
     """Every schedule gives the same bytes: the warp-specialised persistent kernel
-    (default), the grouped three-kernel schedule (WG_HDR_SCHEDULE=grouped) and
-    its bulk-copy tone ring (WG_HDR_TILED; it once raced: LDS in flight vs TMA
-    refill). 7 images > the persistent kernel's ring slots, so slots are
+    with the gray staged in tensor memory (default), the same kernel with a
+    third slot in shared memory (WG_HDR_TMRING=3), the L2-ring variant
+    (WG_HDR_TMEM=0), the grouped three-kernel schedule (WG_HDR_SCHEDULE=grouped)
+    and its bulk-copy tone ring (WG_HDR_TILED; it once raced: LDS in flight vs
+    TMA refill). 7 images > the persistent kernels' slots, so slots are
     reused; repeated calls reuse the scratch."""
     import paper_2108_13656_b200 as wg
     from paper_2108_13656_b200 import synth
@@ -288,6 +290,13 @@ def test_hdr_schedules_agree(torch_dev, monkeypatch):
     scratch = wg.HdrScratch(7, 1024 * 2048)
     for _ in range(3):
         assert torch.equal(wg.hdr_tonemap(rgb, scratch=scratch), plain)
+    monkeypatch.setenv("WG_HDR_TMRING", "3")
+    assert torch.equal(wg.hdr_tonemap(rgb), plain)
+    monkeypatch.delenv("WG_HDR_TMRING")
+    monkeypatch.setenv("WG_HDR_TMEM", "0")
+    for _ in range(2):
+        assert torch.equal(wg.hdr_tonemap(rgb, scratch=scratch), plain)
+    monkeypatch.delenv("WG_HDR_TMEM")
     monkeypatch.setenv("WG_HDR_SCHEDULE", "grouped")
     assert torch.equal(wg.hdr_tonemap(rgb), plain)
     monkeypatch.setenv("WG_HDR_TILED", "1")
