@@ -328,6 +328,26 @@ def test_hdr_multi_image_shapes_vs_oracle(torch_dev, shape, monkeypatch):
             assert mx <= 1 and frac <= 2e-3, (sched, shape, mx, frac)
 
 
+def test_hdr_large_images_ring_fallback_vs_oracle(torch_dev, monkeypatch):
+    """Images whose per-SM range exceeds one tensor-memory slot (3072 x 2048 =
+    6.3 Mpx: > 8192 quads per CTA) take the L2-ring variant of the persistent
+    kernel; both it and the grouped schedule agree with the oracle and with each
+    other."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+    from paper_2108_13656_b200 import synth
+
+    torch, dev = torch_dev
+    rgb = torch.empty((3, 2048, 3072, 3), dtype=torch.float32, device=dev)
+    synth.fill_hdr_f32(rgb, seed=44)
+    want = oracle.hdr_u8(rgb.cpu().numpy(), threads=oracle.default_threads())
+    got = wg.hdr_tonemap(rgb)
+    mx, frac = u8_mismatch(got.cpu().numpy(), want)
+    assert mx <= 1 and frac <= U8_MAX_FRAC, (mx, frac)
+    monkeypatch.setenv("WG_HDR_SCHEDULE", "grouped")
+    assert torch.equal(wg.hdr_tonemap(rgb), got)
+
+
 def test_hdr_out_validated(torch_dev):
     import paper_2108_13656_b200 as wg
 
