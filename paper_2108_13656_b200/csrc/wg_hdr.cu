@@ -154,13 +154,15 @@ __device__ __forceinline__ int build_step_table(int t, const Theta& theta, doubl
     }
     bar();
     const int bad = t < 254 && s_b[t] >= s_b[t + 1];
-    const int b0 = t * (kLutBins / 256);
-    int cb = 0;
+    if (t < 256) {  // (groups of more than 256 threads: the rest only take the barriers)
+        const int b0 = t * (kLutBins / 256);
+        int cb = 0;
 #pragma unroll
-    for (int step = 128; step > 0; step >>= 1)
-        if (s_b[cb + step - 1] < b0) cb += step;
+        for (int step = 128; step > 0; step >>= 1)
+            if (s_b[cb + step - 1] < b0) cb += step;
 #pragma unroll
-    for (int j = 0; j < kLutBins / 256; ++j) s_lut[b0 + j] = step_word(b0 + j, cb, s_b, s_gb);
+        for (int j = 0; j < kLutBins / 256; ++j) s_lut[b0 + j] = step_word(b0 + j, cb, s_b, s_gb);
+    }
     return bar_or(bad);
 }
 __device__ __forceinline__ int named_bar_or(int id, int nthreads, int pred) {
@@ -532,8 +534,10 @@ constexpr int kWsMaxRing = 4;
 constexpr size_t kWsRingBudget = 0;
 // producer L2 prefetch distance in waves of the CTA's range (C4, TMEM kernel
 // before the cross-image register prefetch: 0 -> 320.8, 2 -> 339.5, 3 -> 340.1,
-// 8 -> 336.7 Gpix/s; after: 2 -> 362.1, 3 -> 359.7, 6 -> 359.6; L2 ring: 0 -> 296, 3 -> 309)
-constexpr int kWsPrefetchWaves = 2;
+// 8 -> 336.7 Gpix/s; after: 2 -> 362.1, 3 -> 359.7, 6 -> 359.6; with the scalar
+// producer loop: 1 -> 386.2, 2 -> 408.1, 3 -> 423.5, 4 -> 426.4, 5 -> 425.0;
+// L2 ring: 0 -> 296, 3 -> 309)
+constexpr int kWsPrefetchWaves = 4;
 
 
 
@@ -881,17 +885,18 @@ __device__ __forceinline__ void tm_tone_slot(uint32_t tslot, const float4* sslot
     }
 }
 
-template <int kCons_, int kDbg = 0, int kRing = 2>
+template <int kCons_, int kDbg = 0, int kRing = 2, bool kPackedGray = false>
 __global__ void __launch_bounds__(kWsT, 1)
     hdr_tm_kernel(const float* __restrict__ rgb, uint8_t* __restrict__ out, float2* __restrict__ parts,
                   unsigned* __restrict__ counts, int64_t nimg, int64_t ppi, U8Consts k, float m, float slope,
                   Theta theta, int pf_waves) {
+    // (12 consumer warps measured slower: 401 vs 423 Gpix/s, fewer producers)
     static_assert(kCons_ % 4 == 0, "consumer warps come in whole quadrant sets");
     constexpr int kProd_ = kWsT / 32 - kCons_, kProdT_ = kProd_ * 32, kConsT_ = kCons_ * 32;
     static_assert(kProdT_ % 128 == 0, "producer waves must cover whole TMEM column groups");
     static_assert(kRing == 2 || kRing == 3, "2 TMEM slots (+ 1 shared-memory slot)");
     extern __shared__ float4 s_slot[];  // the third slot (kRing == 3): kTmMaxQuads quads
-    static_assert(kConsT_ == 256, "build_step_table takes 256 consumer threads");
+    static_assert(kConsT_ >= 256, "build_step_table takes 256 consumer threads");
     __shared__ uint32_t s_lut[kLutBins];
     __shared__ int s_b[256];
     __shared__ uint32_t s_gb[256];
@@ -942,16 +947,23 @@ __global__ void __launch_bounds__(kWsT, 1)
         const uint32_t tq = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16);  // this warp's lane quadrant
         // register prefetch of the next quad, continued across image boundaries
         // (the next image's first quad is in flight during the publish and the
-        // slot wait); lanes past the range load a clamped quad
-        const int64_t ulast = nq - 1;
-        float4 n0, n1, n2;
-        auto load_quad = [&](int64_t img, int64_t uq) {
-            const float4* src = reinterpret_cast<const float4*>(rgb + img * ppi * 3 + 12 * mp.quad(min(uq, ulast)));
-            n0 = __ldcs(src);
-            n1 = __ldcs(src + 1);
-            n2 = __ldcs(src + 2);
+        // slot wait); two register buffers used in turn (no copy of the
+        // prefetched quad per iteration); 32-bit quad indices within the CTA's
+        // range; lanes past the range load (and track) a clamped duplicate quad
+        const uint32_t nq32 = static_cast<uint32_t>(nq), ulast = nq32 - 1u;
+        const float* base0 = rgb + 12 * mp.quad(0);
+        const int64_t img_floats = ppi * 3;
+        struct Quad {
+            float4 a, b, c;
         };
-        load_quad(0, tid);
+        auto load = [&](Quad& d, const float* base, uint32_t uq) {
+            const float4* src = reinterpret_cast<const float4*>(base) + 3u * min(uq, ulast);
+            d.a = __ldcs(src);
+            d.b = __ldcs(src + 1);
+            d.c = __ldcs(src + 2);
+        };
+        Quad qa, qb;
+        load(qa, base0, tid);
         for (int64_t i = 0; i < nimg; ++i) {
             if (i >= kRing) {  // slot i % kRing: this CTA's consumers are done with image i - kRing
                 for (uint32_t spins = 0; s_toned < i - kRing + 1; ++spins) {
@@ -963,29 +975,59 @@ __global__ void __launch_bounds__(kWsT, 1)
             if ((kDbg & 4) && tid == 0 && i < kTraceImgs) g_hdr_trace[i][c][0] = gtimer();
             const int slot = static_cast<int>(i % kRing);
             const uint32_t ts = tq + static_cast<uint32_t>(slot * kTmSlotCols);
-            float lo = INFINITY, hi = 0.0f;
-            // warp-uniform trip count (tcgen05.st is .aligned): lanes past the range
-            // compute a clamped quad and store into unused cells
-            for (int64_t u = tid; u - lane < nq; u += kProdT_) {
-                const float4 v0 = n0, v1 = n1, v2 = n2;
+            const float* base = base0 + i * img_floats;
+            // the quad loaded in the warp's last iteration: the next image's first
+            // (a harmless reload of this image's after the last image)
+            const float* alt = i + 1 < nimg ? base + img_floats + 12u * min(static_cast<uint32_t>(tid), ulast) : base;
+            // min over g > 0 as the unsigned minimum of bits(g) - 1 (0 and negative
+            // values wrap above every positive float), max as fmaxf
+            uint32_t lo1 = 0xFFFFFFFFu;
+            float hi = 0.0f;
+            const auto body = [&](const Quad& cur, Quad& nxt, uint32_t u) {
                 if (pf_waves > 0 && tid == 0) prefetch_next();
-                if (u + kProdT_ - lane < nq) load_quad(i, u + kProdT_);
-                else if (i + 1 < nimg) load_quad(i + 1, tid);
-                const float2 a = decolor_fast_x2(make_float2(v0.x, v0.w), make_float2(v0.y, v1.x),
-                                                 make_float2(v0.z, v1.y), k);
-                const float2 b = decolor_fast_x2(make_float2(v1.z, v2.y), make_float2(v1.w, v2.z),
-                                                 make_float2(v2.x, v2.w), k);
-                if (u < nq) {
-                    track(a.x, lo, hi);
-                    track(a.y, lo, hi);
-                    track(b.x, lo, hi);
-                    track(b.y, lo, hi);
+                {  // unconditional load (one selected pointer): no register merges
+                    const float* src = u + kProdT_ - lane < nq32 ? base + 12u * min(u + kProdT_, ulast) : alt;
+                    const float4* s4 = reinterpret_cast<const float4*>(src);
+                    nxt.a = __ldcs(s4);
+                    nxt.b = __ldcs(s4 + 1);
+                    nxt.c = __ldcs(s4 + 2);
                 }
+                // scalar twin of decolor_fast_x2 (same per-lane operations, same
+                // bits): the packed form needs ~40 register moves per quad to pair
+                // same-channel values of the interleaved fp32 RGB
+                float2 a, b;
+                if (kPackedGray) {
+                    a = decolor_fast_x2(make_float2(cur.a.x, cur.a.w), make_float2(cur.a.y, cur.b.x),
+                                        make_float2(cur.a.z, cur.b.y), k);
+                    b = decolor_fast_x2(make_float2(cur.b.z, cur.c.y), make_float2(cur.b.w, cur.c.z),
+                                        make_float2(cur.c.x, cur.c.w), k);
+                } else {
+                    a.x = decolor_fast_x1(cur.a.x, cur.a.y, cur.a.z, k);
+                    a.y = decolor_fast_x1(cur.a.w, cur.b.x, cur.b.y, k);
+                    b.x = decolor_fast_x1(cur.b.z, cur.b.w, cur.c.x, k);
+                    b.y = decolor_fast_x1(cur.c.y, cur.c.z, cur.c.w, k);
+                }
+                lo1 = min(min(min(lo1, __float_as_uint(a.x) - 1u), min(__float_as_uint(a.y) - 1u, __float_as_uint(b.x) - 1u)),
+                          __float_as_uint(b.y) - 1u);
+                hi = fmaxf(fmaxf(fmaxf(hi, a.x), fmaxf(a.y, b.x)), b.y);
                 if ((kDbg & 3) != 3) {
-                    if (slot < 2) tm_st4(ts + static_cast<uint32_t>(4 * (u >> 7)), a.x, a.y, b.x, b.y);
-                    else if (u < nq) s_slot[u] = make_float4(a.x, a.y, b.x, b.y);
+                    if (slot < 2) tm_st4(ts + 4u * (u >> 7), a.x, a.y, b.x, b.y);
+                    else if (u < nq32) s_slot[u] = make_float4(a.x, a.y, b.x, b.y);
                 }
+            };
+            // warp-uniform trip count (tcgen05.st is .aligned)
+            for (uint32_t u = tid;;) {
+                if (u - lane >= nq32) break;
+                body(qa, qb, u);
+                u += kProdT_;
+                if (u - lane >= nq32) {
+                    qa = qb;  // the next image's first quad (once per image)
+                    break;
+                }
+                body(qb, qa, u);
+                u += kProdT_;
             }
+            float lo = lo1 >= 0x7F800000u ? INFINITY : __uint_as_float(lo1 + 1u);  // none (or NaN / negative only)
             tm_wait_st();
             tm_fence_before();
             warp_minmax(lo, hi);
@@ -1271,8 +1313,10 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
                 const int tdbg = de ? atoi(de) : 0, ring = re ? atoi(re) : 2;
                 using TmK = void (*)(const float*, uint8_t*, float2*, unsigned*, int64_t, int64_t, U8Consts, float,
                                      float, Theta, int);
-                TmK tk = ring == 3 ? (tdbg == 4 ? hdr_tm_kernel<8, 4, 3> : hdr_tm_kernel<8, 0, 3>)
-                                   : (tdbg == 4 ? hdr_tm_kernel<8, 4, 2> : hdr_tm_kernel<8, 0, 2>);
+                const char* pe = getenv("WG_HDR_PACKED");  // A/B: packed-pair gray in the producers
+                TmK tk = ring == 3                 ? (tdbg == 4 ? hdr_tm_kernel<8, 4, 3> : hdr_tm_kernel<8, 0, 3>)
+                         : (pe && atoi(pe) == 1) ? hdr_tm_kernel<8, 0, 2, true>
+                                                 : (tdbg == 4 ? hdr_tm_kernel<8, 4, 2> : hdr_tm_kernel<8, 0, 2>);
                 const size_t dsm = ring == 2 ? 0 : static_cast<size_t>(kTmMaxQuads) * sizeof(float4);
                 if (dsm) {
                     e = cudaFuncSetAttribute(reinterpret_cast<const void*>(tk),
