@@ -234,10 +234,9 @@ __global__ void __launch_bounds__(kT) hdr_gray_kernel(const float* __restrict__ 
                 n1 = __ldcs(src + 1);
                 n2 = __ldcs(src + 2);
             }
-            const float2 a = decolor_fast_x2(make_float2(v0.x, v0.w), make_float2(v0.y, v1.x),
-                                             make_float2(v0.z, v1.y), k);
-            const float2 b = decolor_fast_x2(make_float2(v1.z, v2.y), make_float2(v1.w, v2.z),
-                                             make_float2(v2.x, v2.w), k);
+            // the scalar twin of decolor_fast_x2 (same bits; no pair moves, see hdr_tm_kernel)
+            const float2 a = make_float2(decolor_fast_x1(v0.x, v0.y, v0.z, k), decolor_fast_x1(v0.w, v1.x, v1.y, k));
+            const float2 b = make_float2(decolor_fast_x1(v1.z, v1.w, v2.x, k), decolor_fast_x1(v2.y, v2.z, v2.w, k));
             track(a.x, lo, hi);
             track(a.y, lo, hi);
             track(b.x, lo, hi);
@@ -716,10 +715,9 @@ __global__ void __launch_bounds__(kWsT, 1)
                     n1 = __ldcs(src + 1);
                     n2 = __ldcs(src + 2);
                 }
-                const float2 a = decolor_fast_x2(make_float2(v0.x, v0.w), make_float2(v0.y, v1.x),
-                                                 make_float2(v0.z, v1.y), k);
-                const float2 b = decolor_fast_x2(make_float2(v1.z, v2.y), make_float2(v1.w, v2.z),
-                                                 make_float2(v2.x, v2.w), k);
+                // the scalar twin of decolor_fast_x2 (same bits; no pair moves, see hdr_tm_kernel)
+                const float2 a = make_float2(decolor_fast_x1(v0.x, v0.y, v0.z, k), decolor_fast_x1(v0.w, v1.x, v1.y, k));
+                const float2 b = make_float2(decolor_fast_x1(v1.z, v1.w, v2.x, k), decolor_fast_x1(v2.y, v2.z, v2.w, k));
                 track(a.x, lo, hi);
                 track(a.y, lo, hi);
                 track(b.x, lo, hi);
