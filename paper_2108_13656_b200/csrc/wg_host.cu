@@ -7,8 +7,12 @@
 // staging buffers in chunks, rotating over kSlots CUDA streams so the
 // host->device copy of chunk i+1, the kernel on chunk i and the device->host
 // copy of chunk i-1 overlap (PCIe is full duplex), then return when the
-// output is complete. Staging buffers are allocated once per device and
-// grown on demand (the device-buffer manager), guarded by a per-device mutex.
+// output is complete. Staging buffers are allocated once per context and
+// grown on demand (the device-buffer manager); each device keeps a small pool
+// of such contexts (streams + staging), and a call leases one for its
+// duration, so concurrent host calls on one device (the reference drives
+// decolor_rows from a thread pool, backend.py:65-81) overlap instead of
+// serialising on a device lock.
 // Pageable caller buffers (a NumPy array, the reference's PlanarImage data)
 // are staged through per-slot pinned host buffers filled / drained by host
 // threads, so their copies overlap the device work like pinned ones.
@@ -20,6 +24,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <condition_variable>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -107,11 +112,46 @@ struct Slot {
     size_t hcap = 0;
 };
 struct DevCtx {
-    std::mutex mu;
     bool init = false;
     Slot slots[kSlots];
 };
-static DevCtx g_ctx[kMaxDevices];
+// per-device pool of contexts: a call leases one (creating up to kMaxCtx),
+// waiting only when all are in use
+constexpr int kMaxCtx = 4;
+struct DevPool {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<DevCtx*> free;
+    int created = 0;
+};
+static DevPool g_pool[kMaxDevices];
+
+class CtxLease {
+  public:
+    explicit CtxLease(int device) : pool_(g_pool[device]) {
+        std::unique_lock<std::mutex> lk(pool_.mu);
+        pool_.cv.wait(lk, [&] { return !pool_.free.empty() || pool_.created < kMaxCtx; });
+        if (!pool_.free.empty()) {
+            ctx_ = pool_.free.back();
+            pool_.free.pop_back();
+        } else {
+            ctx_ = new DevCtx();  // lives for the process (like the streams and staging it owns)
+            ++pool_.created;
+        }
+    }
+    ~CtxLease() {
+        {
+            std::lock_guard<std::mutex> lk(pool_.mu);
+            pool_.free.push_back(ctx_);
+        }
+        pool_.cv.notify_one();
+    }
+    DevCtx& ctx() { return *ctx_; }
+
+  private:
+    DevPool& pool_;
+    DevCtx* ctx_ = nullptr;
+};
 
 class DeviceGuard {
   public:
@@ -210,8 +250,8 @@ static int host_pipeline(int device, int64_t nunits, const HostIn* ins, int nin,
     for (int i = 0; i < nout; ++i)
         if ((pg_out[i] = is_pageable(outs[i].p))) hneed += align256(chunk * outs[i].bpu);
 
-    DevCtx& ctx = g_ctx[device];
-    std::lock_guard<std::mutex> lock(ctx.mu);
+    CtxLease lease(device);
+    DevCtx& ctx = lease.ctx();
     if (!ctx.init) {
         for (Slot& s : ctx.slots) {
             cudaError_t e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
@@ -326,8 +366,8 @@ static int host_pipeline(int device, int64_t nunits, const HostIn* ins, int nin,
 
 static size_t no_scratch(int64_t) { return 0; }
 
-// Runs fn(stream) on `device` with one of its pipeline streams (device
-// checks, lazy stream creation, the device lock held), then synchronises.
+// Runs fn(stream) on `device` with a stream of a leased context (device
+// checks, lazy stream creation), then synchronises.
 template <class F>
 static int on_device(int device, F fn) {
     int ndev = 0;
@@ -339,8 +379,8 @@ static int on_device(int device, F fn) {
         return set_error(WG_ENODEV, "device ordinal %d out of range (have %d)", device, ndev);
     DeviceGuard guard(device);
     if (guard.status() != cudaSuccess) return cuda_fail(guard.status(), "cudaSetDevice");
-    DevCtx& ctx = g_ctx[device];
-    std::lock_guard<std::mutex> lock(ctx.mu);
+    CtxLease lease(device);
+    DevCtx& ctx = lease.ctx();
     if (!ctx.init) {
         for (Slot& sl : ctx.slots) {
             cudaError_t e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);

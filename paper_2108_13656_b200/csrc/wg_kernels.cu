@@ -1,12 +1,17 @@
-// wg_kernels.cu -- sm_100a kernels and their stream-ordered C-ABI launchers.
+// wg_kernels.cu -- the decolor / sigmoid / quantize Ops and their stream-ordered
+// C-ABI launchers.
 //
-// Hot path: a persistent streaming kernel. Each CTA (256 threads) owns a
-// ring of kStages shared-memory tiles of 12 KiB that one elected thread fills
-// with cp.async.bulk (TMA engine, mbarrier complete_tx); every thread then
-// pulls its 48 contiguous input bytes out of shared memory with three
-// conflict-free 128-bit loads (the warp-cooperative de-interleave of packed
-// RGB), computes in registers and writes its gray bytes with one 128-bit
-// coalesced store. 12 KiB = 4096 uint8 pixels or 1024 fp32 pixels per tile.
+// Hot path: the per-pixel Ops (OpDecolorU8, OpDecolorU8Exact, OpDecolorF32,
+// OpToneF32) run on the streaming skeleton of wg_stream.cuh, all of them on
+// ldg_stream_kernel: each thread takes 48 contiguous input bytes (three
+// 128-bit coalesced loads) of a 256-thread tile with the next tile already in
+// flight in registers, de-interleaves the RGB bytes with PRMT into packed
+// f32x2 pairs (uint8), computes in registers and writes its output with one
+// 128-bit store; the grid is a multiple of the SM count. The cp.async.bulk
+// (TMA) shared-memory ring of the same skeleton (stream_kernel) measured
+// slower (uint8: issue-bound ops; fp32: 80-89% vs 105% of the copy peak) and
+// serves ops without kLdg; the fp64 row
+// kernels below (decolor_f64_kernel & co.) are the bit-identical drop-in path.
 //
 // Reference correspondence: _kernels.pyx:47-56 (decolor_rows),
 // tonemap.py:72-83 (apply_sigmoid), :172-192 (reinstate_color),

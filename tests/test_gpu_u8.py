@@ -208,6 +208,52 @@ def test_host_pipeline_matches_device(torch_dev):
     assert np.array_equal(host, devv)
 
 
+def test_host_calls_from_concurrent_threads(torch_dev):
+    """Host-array calls from several threads at once (the reference drives
+    decolor_rows from a thread pool, backend.py:65-81): each call leases its own
+    context (streams + staging) from the device's pool, so they overlap and give
+    the same bytes as sequential calls -- uint8 (pinned-style NumPy input), the
+    fp64 drop-in on pageable buffers, and the HDR host path, interleaved."""
+    import threading
+
+    import paper_2108_13656_b200 as wg
+    from paper_2108_13656_b200 import PlanarImage
+
+    rng = np.random.default_rng(21)
+    u8 = [rng.integers(0, 256, (301, 777 + 13 * i, 3), dtype=np.uint8) for i in range(6)]
+    f64 = [rng.random((129, 211 + i, 3)) for i in range(4)]
+    hdr = [(rng.random((2, 64, 96, 3)) * 100).astype(np.float32) for _ in range(2)]
+    want_u8 = [wg.decolor_host(a) for a in u8]
+    want_f64 = [wg.decolor_image(PlanarImage(a)).data for a in f64]
+    want_hdr = [wg.hdr_tonemap_host(a) for a in hdr]
+    got = {}
+    errors = []
+
+    def work(kind, i):
+        try:
+            for rep in range(3):
+                if kind == "u8":
+                    got[(kind, i, rep)] = wg.decolor_host(u8[i])
+                elif kind == "f64":
+                    got[(kind, i, rep)] = wg.decolor_image(PlanarImage(f64[i])).data
+                else:
+                    got[(kind, i, rep)] = wg.hdr_tonemap_host(hdr[i])
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    jobs = [("u8", i) for i in range(6)] + [("f64", i) for i in range(4)] + [("hdr", i) for i in range(2)]
+    ts = [threading.Thread(target=work, args=j) for j in jobs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for (kind, i, rep), v in got.items():
+        want = {"u8": want_u8, "f64": want_f64, "hdr": want_hdr}[kind][i]
+        np.testing.assert_array_equal(v, want, err_msg=f"{kind} {i} rep {rep}")
+    assert len(got) == 3 * len(jobs)
+
+
 def test_generators_pinned(torch_dev):
     """Device generators equal their integer restatement in the oracle (C3, C5)."""
     from oracle import oracle
