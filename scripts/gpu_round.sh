@@ -48,3 +48,6 @@ echo "ncu_full_lhe=$?"
 timeout 600 python scripts/ab_tone.py --op local --images 64 --iters 10 --rounds 3 --sleep 2 --configs "" > $OUT/ab_local.log 2>&1
 timeout 600 python scripts/ab_tone.py --op tone_exact --images 256 --iters 20 --rounds 3 --sleep 2 --configs "" > $OUT/ab_tone_exact.log 2>&1
 echo "ab=$?"
+timeout 300 python scripts/hdr_trace.py --images 32 --runs 3 > $OUT/hdr_trace.log 2>&1
+timeout 600 python scripts/ab_tone.py --op hdr --images 32 --iters 20 --rounds 3 --sleep 1 --configs "PF=4;TM=0;SCHED=grouped" > $OUT/ab_hdr.log 2>&1
+echo "hdr_extra=$?"
