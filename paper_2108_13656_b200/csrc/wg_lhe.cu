@@ -650,17 +650,13 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
             grp.gray255(L.kt, tv);  // t = v nb directly (the scale folded into the constants)
             uint32_t words[kGrp];
             uint32_t run_addr = dummy, run = 0;
-            // the bin test as a group maximum of |frac(t) - 1/2| (one FMNMX per
-            // pixel); a group with a pixel within the margin of a bin edge sends
-            // all its pixels to the fix (which only moves counts whose fp64 bin
-            // differs, so the sure ones are no-ops)
-            float dmax = 0.0f;
             const auto px = [&](int p, uint32_t base) {
                 const float tu = tv[p];
                 const float t = fminf(fmaxf(tu, 0.5f), L.t_hi);
                 const float tf = __fadd_rd(t, 8388608.0f);
-                dmax = fmaxf(dmax, fabsf(__fsub_rn(__fsub_rn(t, __fsub_rn(tf, 8388608.0f)), 0.5f)));
+                const bool sure = fabsf(__fsub_rn(__fsub_rn(t, __fsub_rn(tf, 8388608.0f)), 0.5f)) < L.half_m;
                 words[p] = plane_u16(L, tu);  // unsure bins are patched by the fix
+                slow |= static_cast<uint32_t>(!sure) << p;
                 const uint32_t addr = base + (__float_as_uint(tf) << 2);  // unsure: moved by the fix
                 const bool flush = addr != run_addr;
                 red_shared_at(flush ? run_addr : lane_cell, run);
@@ -682,7 +678,6 @@ __global__ void __launch_bounds__(kBlock, 4) lhe_hist16_kernel(U8Lhe L, LheGeom 
                 }
             }
             red_shared_at(run_addr, run);
-            if (!(dmax < L.half_m)) slow = 0xFFFFu;
             if (vec) {
 #pragma unroll
                 for (int q = 0; q < kGrp / 8; ++q)
@@ -806,10 +801,10 @@ __device__ __forceinline__ uint64_t l2_policy_evict_last_lhe() {
     return p;
 }
 
-// byte of r' (in [256, 512): mantissa bits 22..15 = floor(r + 1/2)), from
-// e = bits(r') + m; the pixel is within m of a rounding boundary iff
-// (e & 0x7FFF) < 2 m (tested as a group minimum in apply16_groups)
+// byte of r' (in [256, 512): mantissa bits 22..15 = floor(r + 1/2)) and the
+// flag "within m of a rounding boundary", from e = bits(r') + m
 __device__ __forceinline__ uint32_t q_byte(uint32_t e) { return (e >> 15) & 255u; }
+__device__ __forceinline__ bool q_unsure(uint32_t e, uint32_t m) { return (e & 0x7FFFu) < 2u * m; }
 
 // kF: the plane's fraction bits when fixed at compile time (8: bins 129..256), else -1
 template <bool kGray, bool kIdent, int kF>
@@ -902,9 +897,8 @@ __device__ __forceinline__ void apply16_groups(const U8Lhe& L, const Apply16& A,
         uint32_t ot[4] = {0u, 0u, 0u, 0u}, og[4] = {0u, 0u, 0u, 0u};
         float4 f;
         uint4 o;
-        // toned word e (and gray word eg) of pixel p: byte = q_byte, distance to the
-        // rounding boundary (plus the margin) = the low 15 bits
-        const auto eval = [&](int p, uint32_t& e, uint32_t& eg) {
+#pragma unroll
+        for (int p = 0; p < kGrp; ++p) {
             if ((p & 3) == 0) {  // the quad's blend fractions and table offsets, loaded where used
                 f = reinterpret_cast<const float4*>(sxf)[(p >> 2) * G + gx];
                 o = reinterpret_cast<const uint4*>(sxo)[(p >> 2) * G + gx];
@@ -924,6 +918,8 @@ __device__ __forceinline__ void apply16_groups(const U8Lhe& L, const Apply16& A,
             }
             const float uf = __fsub_rn(__uint_as_float(fb), 8388608.0f);
             const float4 cq = *reinterpret_cast<const float4*>(quadb + boff);
+            uint32_t e;
+            bool uns;
             if constexpr (kIdent) {  // raw curves, NaN = identity tile (the pixel's own value)
                 const float v = __fmaf_rn(uf, A.uscale, A.uhalf);
                 const float c00 = cq.x != cq.x ? v : cq.x, c01 = cq.y != cq.y ? v : cq.y;
@@ -932,32 +928,21 @@ __device__ __forceinline__ void apply16_groups(const U8Lhe& L, const Apply16& A,
                 const float bottom = __fmaf_rn(wx, __fsub_rn(c11, c10), c10);
                 const float eq = __fmaf_rn(wy, __fsub_rn(bottom, top), top);
                 e = __float_as_uint(__fadd_rn(__fmaf_rn(sf, __fsub_rn(eq, v), v), 256.5f)) + A.mq_ident;
+                uns = q_unsure(e, A.mq_ident);
             } else {
                 const float T = __fmaf_rn(wx, cq.y, cq.x), B = __fmaf_rn(wx, cq.w, cq.z);
                 const float E = __fmaf_rn(wy, __fsub_rn(B, T), T);
                 e = __float_as_uint(__fmaf_rn(A.oms_us, uf, E)) + A.mq;
+                uns = q_unsure(e, A.mq);
             }
-            if constexpr (kGray) eg = __float_as_uint(__fadd_rn(__fmaf_rn(uf, A.uscale, A.uhalf), 256.5f)) + A.mg;
-        };
-        const uint32_t mt2 = 2u * (kIdent ? A.mq_ident : A.mq), mg2 = 2u * A.mg;
-        // the unsure test as a group minimum of the low 15 bits (one LOP3 + one
-        // VIMNMX per pixel)
-        uint32_t dmin = 0xFFFFFFFFu, dming = 0xFFFFFFFFu;
-#pragma unroll
-        for (int p = 0; p < kGrp; ++p) {
-            uint32_t e, eg = 0u;
-            eval(p, e, eg);
             ot[p >> 2] |= q_byte(e) << (8 * (p & 3));
-            dmin = min(dmin, e & 0x7FFFu);
             if constexpr (kGray) {
+                const uint32_t eg = __float_as_uint(__fadd_rn(__fmaf_rn(uf, A.uscale, A.uhalf), 256.5f)) + A.mg;
+                uns = uns || q_unsure(eg, A.mg);
                 og[p >> 2] |= q_byte(eg) << (8 * (p & 3));
-                dming = min(dming, eg & 0x7FFFu);
             }
+            slow |= static_cast<uint32_t>(uns) << p;
         }
-        // a group with a pixel inside a margin sends all of its pixels to the
-        // fp64 queue (~3% of groups at the defaults; rebuilding the mask in place
-        // kept the words live and spilled)
-        if (dmin < mt2 || (kGray && dming < mg2)) slow = 0xFFFFu;  // (row tails trim it below)
         if (vec) {
             st_global_cs_v4(toned + p0, make_uint4(ot[0], ot[1], ot[2], ot[3]));
             if constexpr (kGray) st_global_cs_v4(gray + p0, make_uint4(og[0], og[1], og[2], og[3]));
