@@ -36,7 +36,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--configs", default="ROUTE=linear")
-    ap.add_argument("--op", default="tone", choices=("tone", "decolor", "tone_exact", "local", "hdr"))
+    ap.add_argument("--op", default="tone", choices=("tone", "decolor", "tone_exact", "local", "hdr", "rgb"))
     ap.add_argument("--sleep", type=float, default=0.0)
     ap.add_argument("--lib", default=None, help="load this build of the library (cross-build A/B)")
     args = ap.parse_args()
@@ -58,6 +58,7 @@ def main():
     op = {"tone": lambda: wg.decolor_tone(rgb, out=out), "decolor": lambda: wg.decolor(rgb, out=out),
           "tone_exact": lambda: wg.decolor_tone(rgb, out=out, exact=True),
           "hdr": lambda: wg.hdr_tonemap(rgb, out=out),
+          "rgb": lambda: wg.decolor_tone(rgb, return_rgb=True, out=out)[0],
           "local": lambda: wg.decolor_tone_local(img4, grid=grid, scratch=scratch,
                                                  out=out.view(args.images, wl.height, wl.width))}[args.op]
     tone_ref = op().clone()
@@ -102,7 +103,7 @@ def main():
     for name, v in res.items():
         m = statistics.median(v)
         print(json.dumps({"kernel": name, "gpix_s": round(m, 1), "vs_decolor": round(m / base, 3),
-                          "frac": round(m * (13 if args.op == "hdr" else 4) / 6545.3, 3), "all": [round(x, 1) for x in v]}))
+                          "frac": round(m * {"hdr": 13, "rgb": 7}.get(args.op, 4) / 6454.6, 3), "all": [round(x, 1) for x in v]}))
 
 
 if __name__ == "__main__":
