@@ -545,7 +545,8 @@ def main():
     # ---- optional final gather of the gray shards (strong scaling, N > 1): timed apart from the metric
     gather = None
     if scaling == "strong" and world > 1:
-        gather = run_gather(torch, sharder, out, n_total, world)
+        step_into = (lambda o: wg.decolor(rgb, out=o)) if args.op == "decolor" and wl.output == "gray_u8" else None
+        gather = run_gather(torch, sharder, out, n_total, world, step_into, first, stream)
     del out, rgb
     torch.cuda.empty_cache()
 
@@ -638,8 +639,11 @@ def run_plan(args, wl, world, rank, scaling, spec):
                                      "pixels_per_rank": [(b - a) * wl.pix_per_image for a, b in shards]}}))
 
 
-def run_gather(torch, sharder, out, n_total, world):
-    """sharder.gather_to_root of every rank's gray shard to rank 0, timed on its own."""
+def run_gather(torch, sharder, out, n_total, world, step_into=None, first=0, stream=None):
+    """sharder.gather_to_root of every rank's gray shard to rank 0, timed on its own;
+    with ``step_into`` (the rank's decolor launch with an ``out=`` tensor) also the
+    gather fused into the launch: the kernel stores the shard straight into the
+    root's buffer mapped over CUDA IPC / NVLink (sharder.PeerBuffer)."""
     torch.cuda.synchronize()
     torch.distributed.barrier()
     t0 = time.perf_counter()
@@ -650,9 +654,39 @@ def run_gather(torch, sharder, out, n_total, world):
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     nbytes = n_total * out[0].numel() * out.element_size()
     del full
-    return {"gather_ms": round(float(t.item()) * 1e3, 3), "bytes": int(nbytes),
-            "note": "sharder.gather_to_root (NCCL gather to rank 0), outside the device-timed metric; "
-                    "max over ranks of the wall time"}
+    res = {"gather_ms": round(float(t.item()) * 1e3, 3), "bytes": int(nbytes),
+           "note": "sharder.gather_to_root (NCCL gather to rank 0), outside the device-timed metric; "
+                   "max over ranks of the wall time"}
+    if step_into is not None and out.dtype == torch.uint8:
+        try:
+            peer = sharder.PeerBuffer(n_total, tuple(out.shape[1:]), out.device.index)
+        except Exception as e:  # (no IPC between these processes)
+            res["fused"] = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+            return res
+        view = peer.view(first, out.shape[0])
+        step_into(view)  # warm (peer mapping, TLB)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        step_into(view)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        wall = time.perf_counter() - t0
+        t = torch.tensor([e0.elapsed_time(e1), wall * 1e3], dtype=torch.float64, device=out.device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ok = None
+        if torch.distributed.get_rank() == 0:
+            ok = bool(torch.equal(peer.view(first, out.shape[0]), out))  # the root's own shard, same bytes
+        peer.close()
+        res["fused"] = {"step_ms": round(float(t[0].item()), 3), "wall_ms": round(float(t[1].item()), 3),
+                        "root_shard_equal": ok,
+                        "note": "decolor launch whose out= is the root's buffer (CUDA IPC, NVLink stores): "
+                                "the gather fused into the kernel; device time max over ranks, then wall "
+                                "time including the barrier"}
+    return res
 
 
 def run_size_sweep(wg, torch, dev, stream, rank, iters: int = 5):

@@ -68,6 +68,19 @@ WG_API const char* wg_last_error(void);                   /* thread-local; "" wh
 WG_API int wg_device_count(void);
 WG_API int wg_sm_count(int device);
 
+/* ---- peer buffers: the optional final gather fused into the launch (SURVEY.md 8 e) ----
+ * The root rank allocates the whole batch's output with wg_ipc_alloc and
+ * sends the 64-byte CUDA IPC handle to the other ranks (torch.distributed);
+ * each maps it with wg_ipc_open (peer access over NVLink) and passes
+ * root_ptr + its shard offset as the `out` of its decolor call, so the shard
+ * is stored straight into the root's memory by the kernel. Replaces
+ * decolor-then-gather (sharder.gather_to_root); the reference has no
+ * collective at all (single process). */
+WG_API int wg_ipc_alloc(size_t bytes, int device, void** dptr, uint8_t* handle64);
+WG_API int wg_ipc_open(const uint8_t* handle64, int device, void** dptr);
+WG_API int wg_ipc_close(void* dptr);
+WG_API int wg_ipc_free(void* dptr, int device);
+
 /* ---- device-pointer, stream-ordered hot path ------------------------------ */
 
 /* uint8 RGB -> uint8 gray, i.e. quantize_u8(decolor_image(dequantize_u8(rgb)))

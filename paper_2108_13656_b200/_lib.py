@@ -69,6 +69,10 @@ SIGNATURES = {
     "wg_hdr_scratch_bytes": (_sz, [_i64, _i64]),
     "wg_hdr_tonemap_u8": (_i, [_vp, _vp, _i64, _i64, _f, _f, _f, _f, _vp, _sz, _vp]),
     "wg_hdr_debug_trace": (_i64, [_vp]),
+    "wg_ipc_alloc": (_i, [_sz, _i, _vp, _vp]),
+    "wg_ipc_open": (_i, [_vp, _i, _vp]),
+    "wg_ipc_close": (_i, [_vp]),
+    "wg_ipc_free": (_i, [_vp, _i]),
     "wg_luma_f64": (_i, [_vp, _vp, _i64, _i, _vp]),
     "wg_lab_f64": (_i, [_vp, _vp, _i64, _vp]),
     "wg_luma_u8": (_i, [_vp, _vp, _i64, _i, _vp]),

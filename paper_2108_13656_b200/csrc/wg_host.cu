@@ -415,6 +415,54 @@ extern "C" int wg_device_count(void) {
 
 extern "C" int wg_sm_count(int device) { return sm_count(device); }
 
+// ====================================================================== peer buffers (SURVEY.md 8 e)
+// The optional final gather as part of the decolor launch: the root allocates
+// the whole batch's output here and shares a CUDA IPC handle (64 bytes, sent
+// over torch.distributed); every other rank maps it (peer access over NVLink
+// enabled by the open) and its decolor kernel stores its shard straight into
+// the root's HBM -- no staging copy and no separate collective.
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+
+extern "C" int wg_ipc_alloc(size_t bytes, int device, void** dptr, uint8_t* handle) {
+    if (!dptr || !handle || bytes == 0) return set_error(WG_EINVAL, "ipc_alloc: null pointer or zero size");
+    DeviceGuard guard(device);
+    if (guard.status() != cudaSuccess) return cuda_fail(guard.status(), "cudaSetDevice");
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);  // its own allocation: the handle's base is the pointer
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(ipc)");
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    std::memcpy(handle, &h, sizeof h);
+    *dptr = p;
+    return WG_OK;
+}
+
+extern "C" int wg_ipc_open(const uint8_t* handle, int device, void** dptr) {
+    if (!dptr || !handle) return set_error(WG_EINVAL, "ipc_open: null pointer");
+    DeviceGuard guard(device);
+    if (guard.status() != cudaSuccess) return cuda_fail(guard.status(), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    cudaError_t e = cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    return WG_OK;
+}
+
+extern "C" int wg_ipc_close(void* dptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(dptr);
+    return e == cudaSuccess ? WG_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
+extern "C" int wg_ipc_free(void* dptr, int device) {
+    DeviceGuard guard(device);
+    cudaError_t e = cudaFree(dptr);
+    return e == cudaSuccess ? WG_OK : cuda_fail(e, "cudaFree(ipc)");
+}
+
 // ====================================================================== host-side container check
 // PlanarImage's validation (core.py:69-80: finite, then inside [0, 1]) over a
 // host float64 array, split over host threads: 0 ok, 1 a non-finite sample,

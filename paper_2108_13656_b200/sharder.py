@@ -13,6 +13,12 @@ test_core.py:201-206). Two drivers:
   separately from the device metric);
 * one process driving several GPUs: :func:`run_on_devices` fans the shards
   of a host batch out to ``wg_host_*`` calls, one host thread per device.
+
+The gather can also be part of the launch itself: :class:`PeerBuffer` is the
+whole batch's output allocated on the root and mapped into every rank over
+CUDA IPC (NVLink peer access); a rank passes ``peer.view(first, count)`` as the
+``out=`` of its decolor call and the kernel stores its shard straight into
+the root's memory -- no staging copy, no separate collective.
 """
 
 from __future__ import annotations
@@ -88,3 +94,89 @@ def run_on_devices(fn: Callable[[np.ndarray, int], np.ndarray], batch: np.ndarra
         futs = [pool.submit(fn, batch[a:b], d) for (a, b), d in zip(spans, devices) if b > a]
         parts = [f.result() for f in futs]
     return np.concatenate(parts, axis=0) if parts else fn(batch[:0], devices[0])
+
+
+class _CudaArray:
+    """A raw device pointer as a ``__cuda_array_interface__`` object (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class PeerBuffer:
+    """The full batch's output on ``root``, mapped into every rank (SURVEY.md 8 e).
+
+    The root allocates ``n_items`` items of ``item_shape`` (``wg_ipc_alloc``,
+    its own cudaMalloc) and broadcasts the 64-byte CUDA IPC handle; the other
+    ranks map it (``wg_ipc_open``, peer access over NVLink). ``view(first,
+    count)`` is a tensor over items [first, first + count) of the root's buffer
+    on every rank: given as ``out=`` to ``decolor`` / ``decolor_tone``, the
+    kernel's stores land in the root's HBM. Call :meth:`close` on every rank
+    (collective) when done; the root's full batch is :meth:`full` until then.
+    """
+
+    def __init__(self, n_items: int, item_shape, device: int, dtype: str = "uint8", group=None, root: int = 0):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if dtype not in ("uint8", "float32"):
+            raise ValueError(f"unsupported dtype {dtype}")
+        self._torch = torch
+        self.device = int(device)
+        self.item_shape = tuple(int(x) for x in item_shape)
+        self.dtype = dtype
+        self.itemsize = 1 if dtype == "uint8" else 4
+        self.item_elems = int(np.prod(self.item_shape)) if self.item_shape else 1
+        self.n_items = int(n_items)
+        self.group, self.root = group, root
+        self.rank = dist.get_rank(group)
+        nbytes = max(1, self.n_items * self.item_elems * self.itemsize)
+        handle = (ctypes.c_uint8 * 64)()
+        ptr = ctypes.c_void_p()
+        if self.rank == root:
+            _lib.call("wg_ipc_alloc", nbytes, self.device, ctypes.byref(ptr), handle)
+        box = [bytes(handle)]
+        dist.broadcast_object_list(box, src=root, group=group)
+        if self.rank != root:
+            ctypes.memmove(handle, box[0], 64)
+            _lib.call("wg_ipc_open", handle, self.device, ctypes.byref(ptr))
+        self.ptr = int(ptr.value)
+        self._open = True
+
+    def view(self, first: int, count: int):
+        """Items [first, first + count) of the root's buffer, as a tensor on this rank's device."""
+        if not (0 <= first and first + count <= self.n_items):
+            raise ValueError(f"items [{first}, {first + count}) outside [0, {self.n_items})")
+        typestr = "|u1" if self.dtype == "uint8" else "<f4"
+        off = first * self.item_elems * self.itemsize
+        with self._torch.cuda.device(self.device):
+            return self._torch.as_tensor(_CudaArray(self.ptr + off, (count, *self.item_shape), typestr),
+                                         device=f"cuda:{self.device}")
+
+    def full(self):
+        """The whole batch (root only)."""
+        if self.rank != self.root:
+            raise ValueError("full() is the root's view; other ranks use view()")
+        return self.view(0, self.n_items)
+
+    def close(self):
+        """Collective: every rank's stores are complete, then unmap / free."""
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if not self._open:
+            return
+        self._torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        if self.rank != self.root:
+            _lib.call("wg_ipc_close", self.ptr)
+        dist.barrier(group=self.group)  # every mapping closed before the root frees
+        if self.rank == self.root:
+            _lib.call("wg_ipc_free", self.ptr, self.device)
+        self._open = False
