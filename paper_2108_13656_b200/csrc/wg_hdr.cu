@@ -633,10 +633,7 @@ __device__ __forceinline__ void ws_tone_range(const float* __restrict__ gsl, uin
     }
 }
 
-// kDbg (timing experiments only, WG_HDR_DBG; output invalid): 1 = consumers do
-// not tone, 2 = producers do not load (synthetic values), 3 = producers do not
-// store the gray and consumers do not tone
-template <int kCons_, int kDbg = 0>
+template <int kCons_>
 __global__ void __launch_bounds__(kWsT, 1)
     hdr_ws_kernel(const float* __restrict__ rgb, uint8_t* __restrict__ out, float* __restrict__ ring,
                   float2* __restrict__ parts, unsigned* __restrict__ counts, int64_t nimg, int64_t ppi, int nring,
@@ -681,6 +678,23 @@ __global__ void __launch_bounds__(kWsT, 1)
         };
         if (tid == 0)
             for (int w = 0; w < pf_waves; ++w) prefetch_next();
+        // (as hdr_tm_kernel: register prefetch continued across images, two
+        // register buffers in turn, one selected-pointer load per quad, an
+        // integer minimum over g > 0; lanes past the range load and track a
+        // clamped duplicate quad and store nothing)
+        const uint32_t nq32 = static_cast<uint32_t>(nq), ulast = nq32 - 1u;
+        const float* base0 = rgb + 12 * mp.quad(0);
+        const int64_t img_floats = ppi * 3;
+        struct Quad {
+            float4 a, b, c;
+        };
+        Quad qa, qb;
+        {
+            const float4* src = reinterpret_cast<const float4*>(base0) + 3u * min(static_cast<uint32_t>(tid), ulast);
+            qa.a = __ldcs(src);
+            qa.b = __ldcs(src + 1);
+            qa.c = __ldcs(src + 2);
+        }
         for (int64_t i = 0; i < nimg; ++i) {
             if (i >= nring) {  // slot i % nring: this CTA's consumers are done with image i - nring
                 for (uint32_t spins = 0; s_toned < i - nring + 1; ++spins) {
@@ -688,42 +702,47 @@ __global__ void __launch_bounds__(kWsT, 1)
                     if (spins > (1u << 26)) __trap();
                 }
             }
-            const float* in = rgb + i * ppi * 3;
-            float* g = ring + (i % nring) * ppi;
-            float lo = INFINITY, hi = 0.0f;
-            int64_t u = tid;
-            float4 n0, n1, n2;
-            if (kDbg == 2) {
-                n0 = make_float4(float(u) + 1.0f, 2.0f, 3.0f, 4.0f);
-                n1 = make_float4(5.0f, 6.0f, 7.0f, 8.0f);
-                n2 = make_float4(9.0f, 10.0f, 11.0f, float(i));
-            } else if (u < nq) {
-                const float4* src = reinterpret_cast<const float4*>(in + 12 * mp.quad(u));
-                n0 = __ldcs(src);
-                n1 = __ldcs(src + 1);
-                n2 = __ldcs(src + 2);
-            }
-            for (; u < nq; u += kProdT_) {
-                const int64_t q = mp.quad(u);
-                const float4 v0 = n0, v1 = n1, v2 = n2;
+            float* g = ring + (i % nring) * ppi + 4 * mp.quad(0);
+            const float* base = base0 + i * img_floats;
+            const float* alt = i + 1 < nimg ? base + img_floats + 12u * min(static_cast<uint32_t>(tid), ulast) : base;
+            uint32_t lo1 = 0xFFFFFFFFu;
+            float hi = 0.0f;
+            const auto body = [&](const Quad& cur, Quad& nxt, uint32_t u) {
                 if (pf_waves > 0 && tid == 0) prefetch_next();
-                if (kDbg == 2) {
-                    n0.x += 1.0f;
-                } else if (u + kProdT_ < nq) {
-                    const float4* src = reinterpret_cast<const float4*>(in + 12 * mp.quad(u + kProdT_));
-                    n0 = __ldcs(src);
-                    n1 = __ldcs(src + 1);
-                    n2 = __ldcs(src + 2);
+                {
+                    const float* src = u + kProdT_ < nq32 ? base + 12u * (u + kProdT_) : alt;
+                    const float4* s4 = reinterpret_cast<const float4*>(src);
+                    nxt.a = __ldcs(s4);
+                    nxt.b = __ldcs(s4 + 1);
+                    nxt.c = __ldcs(s4 + 2);
                 }
-                // the scalar twin of decolor_fast_x2 (same bits; no pair moves, see hdr_tm_kernel)
-                const float2 a = make_float2(decolor_fast_x1(v0.x, v0.y, v0.z, k), decolor_fast_x1(v0.w, v1.x, v1.y, k));
-                const float2 b = make_float2(decolor_fast_x1(v1.z, v1.w, v2.x, k), decolor_fast_x1(v2.y, v2.z, v2.w, k));
-                track(a.x, lo, hi);
-                track(a.y, lo, hi);
-                track(b.x, lo, hi);
-                track(b.y, lo, hi);
-                if (kDbg != 3) st_v4_hint(g + 4 * q, make_float4(a.x, a.y, b.x, b.y), pol_gray);
+                const float2 a = make_float2(decolor_fast_x1(cur.a.x, cur.a.y, cur.a.z, k),
+                                             decolor_fast_x1(cur.a.w, cur.b.x, cur.b.y, k));
+                const float2 b = make_float2(decolor_fast_x1(cur.b.z, cur.b.w, cur.c.x, k),
+                                             decolor_fast_x1(cur.c.y, cur.c.z, cur.c.w, k));
+                lo1 = min(min(min(lo1, __float_as_uint(a.x) - 1u), min(__float_as_uint(a.y) - 1u, __float_as_uint(b.x) - 1u)),
+                          __float_as_uint(b.y) - 1u);
+                hi = fmaxf(fmaxf(fmaxf(hi, a.x), fmaxf(a.y, b.x)), b.y);
+                st_v4_hint(g + 4 * u, make_float4(a.x, a.y, b.x, b.y), pol_gray);
+            };
+            for (uint32_t u = tid;;) {
+                if (u >= nq32) break;
+                body(qa, qb, u);
+                u += kProdT_;
+                if (u >= nq32) {
+                    qa = qb;  // the next image's first quad (once per image)
+                    break;
+                }
+                body(qb, qa, u);
+                u += kProdT_;
             }
+            if (static_cast<uint32_t>(tid) >= nq32 && i + 1 < nimg) {  // (a range smaller than one wave)
+                const float4* src = reinterpret_cast<const float4*>(alt);
+                qa.a = __ldcs(src);
+                qa.b = __ldcs(src + 1);
+                qa.c = __ldcs(src + 2);
+            }
+            float lo = lo1 >= 0x7F800000u ? INFINITY : __uint_as_float(lo1 + 1u);
             warp_minmax(lo, hi);
             if (lane == 0) {
                 s_plo[warp] = lo;
@@ -780,8 +799,7 @@ __global__ void __launch_bounds__(kWsT, 1)
         // tone this CTA's lines (per-image mode hoisted out of the pixel loop)
         const float* gsl = ring + (i % nring) * ppi;
         uint8_t* o = out + i * ppi;
-        if (kDbg == 1 || kDbg == 3) {
-        } else if (st.mode == 1 && st.lut) {
+        if (st.mode == 1 && st.lut) {
             const float inv = st.inv_gmin;
             ws_tone_range<2, kConsT_>(gsl, o, mp, ct, [&](float v) -> uint32_t { return lut_px32(v, inv, s_lut); });
         } else if (st.mode == 2) {
@@ -1265,10 +1283,9 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
     const bool ws_ok = (pix_per_img % kWsLinePx) == 0 && (reinterpret_cast<uintptr_t>(rgb) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(out) & 15) == 0 && device >= 0 && device < kMaxDevices;
     // 8 consumer warps of 32 (C4: 4 -> 274, 12 -> 261, 16 -> 270 vs 308 Gpix/s)
-    static std::atomic<int> ws_occ[4][kMaxDevices];  // idempotent lazy cache
-    const char* dbg = getenv("WG_HDR_DBG");  // timing experiments only (output invalid)
-    const int var = dbg ? std::min(std::max(atoi(dbg), 0), 3) : 0;
-    const auto ws_kern = var == 1 ? hdr_ws_kernel<8, 1> : var == 2 ? hdr_ws_kernel<8, 2> : var == 3 ? hdr_ws_kernel<8, 3> : hdr_ws_kernel<8, 0>;
+    static std::atomic<int> ws_occ[1][kMaxDevices];  // idempotent lazy cache
+    const int var = 0;
+    const auto ws_kern = hdr_ws_kernel<8>;
     if (ws_ok && ws_enabled()) {
         if (!ws_occ[var][device]) {
             int coop = 0, occ = 0;
@@ -1299,7 +1316,7 @@ extern "C" int wg_hdr_tonemap_u8(const float* rgb, uint8_t* out, int64_t nimg, i
             // TMEM staging when a CTA's per-image range fits one TMEM slot
             const int64_t max_quads = (lines + grid - 1) / grid * (kWsLinePx / 4);
             const char* tm_env = getenv("WG_HDR_TMEM");
-            const bool tm = max_quads <= kTmMaxQuads && !(tm_env && std::strcmp(tm_env, "0") == 0) && var == 0;
+            const bool tm = max_quads <= kTmMaxQuads && !(tm_env && std::strcmp(tm_env, "0") == 0);
             if (tm) {
                 void* targs[] = {&rgb, &out, &wparts, &wcounts, &n, &ppi, &kk, &mm, &ss, &th, &pf};
                 // 8 consumer warps (4: 293 vs 340 Gpix/s, the tone falls behind)

@@ -26,7 +26,7 @@ import paper_2108_13656_b200 as wg  # noqa: E402
 from paper_2108_13656_b200 import synth  # noqa: E402
 
 KEYS = {"GRID": "WG_LDG_GRID_PER_SM", "ROUTE": "WG_TONE_ROUTE", "XK": "WG_TONE_EXACT_KERNEL",
-        "LP": "WG_LHE_PLANE", "PF": "WG_HDR_PF", "SCHED": "WG_HDR_SCHEDULE", "RING": "WG_HDR_RING_MB", "DBG": "WG_HDR_DBG", "TM": "WG_HDR_TMEM", "CONS": "WG_HDR_CONS", "TMDBG": "WG_HDR_TMDBG", "RING3": "WG_HDR_TMRING", "PACKED": "WG_HDR_PACKED"}
+        "LP": "WG_LHE_PLANE", "PF": "WG_HDR_PF", "SCHED": "WG_HDR_SCHEDULE", "RING": "WG_HDR_RING_MB", "TM": "WG_HDR_TMEM", "TMDBG": "WG_HDR_TMDBG", "RING3": "WG_HDR_TMRING", "PACKED": "WG_HDR_PACKED"}
 
 
 def main():
