@@ -10,12 +10,14 @@
 //   out = quantize_u8(apply_sigmoid(t))      (tonemap.py:72-83, codec.py:22-25)
 //
 // Default schedule (images a multiple of 32 px): ONE warp-specialised
-// persistent kernel (hdr_ws_kernel, below): producer warps write each CTA's
-// range of the fp32 gray into an L2-resident ring and publish exact per-CTA
+// persistent kernel, one 1024-thread CTA per SM: producer warps compute the
+// fp32 gray of the CTA's range of every image and publish exact per-CTA
 // (min over g > 0, max) partials; consumer warps of the same CTA fold the
 // image's partials once all CTAs have published, build the threshold table
-// and tone the CTA's own range from L2 -- 13-14 B/px of HBM traffic instead
-// of 21 (C4: 308 vs 288 Gpix/s).
+// and tone the CTA's own range. hdr_tm_kernel keeps the gray in the SM's
+// tensor memory (two image slots; C4: 429 Gpix/s, 0.99 x the 13 B/px of
+// algorithmic traffic); hdr_ws_kernel, for images whose per-SM share exceeds
+// a slot, keeps it in an L2-resident ring (C4: 320).
 //
 // Grouped schedule (WG_HDR_SCHEDULE=grouped, and other image sizes): three
 // kernels per group of images:
