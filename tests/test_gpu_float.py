@@ -348,6 +348,30 @@ def test_hdr_large_images_ring_fallback_vs_oracle(torch_dev, monkeypatch):
     assert torch.equal(wg.hdr_tonemap(rgb), got)
 
 
+@pytest.mark.parametrize("lines_extra", [0, 1])
+def test_hdr_tmem_slot_boundary_vs_oracle(torch_dev, lines_extra, monkeypatch):
+    """Images whose per-SM share is exactly one full tensor-memory slot (148 x
+    1024 lines of 32 px: 8192 quads per CTA, every TMEM column of the slot in
+    use) and one line more (one CTA over the slot: the L2-ring kernel), three
+    images so the two slots are reused; both against the oracle and the
+    grouped schedule."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+    from paper_2108_13656_b200 import synth
+
+    torch, dev = torch_dev
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    ppi = (sms * 1024 + lines_extra) * 32
+    rgb = torch.empty((3, ppi // 64, 64, 3), dtype=torch.float32, device=dev)
+    synth.fill_hdr_f32(rgb, seed=51 + lines_extra)
+    got = wg.hdr_tonemap(rgb)
+    want = oracle.hdr_u8(rgb.cpu().numpy(), threads=oracle.default_threads())
+    mx, frac = u8_mismatch(got.cpu().numpy(), want)
+    assert mx <= 1 and frac <= U8_MAX_FRAC, (lines_extra, mx, frac)
+    monkeypatch.setenv("WG_HDR_SCHEDULE", "grouped")
+    assert torch.equal(wg.hdr_tonemap(rgb), got)
+
+
 def test_hdr_out_validated(torch_dev):
     import paper_2108_13656_b200 as wg
 
