@@ -45,6 +45,32 @@ def test_f64_cube_bit_identical_to_reference():
     assert hashlib.sha256(out.tobytes()).hexdigest() == ref["compiled"]["gray_f64_sha256"]
 
 
+def test_f64_dropin_edge_samples():
+    """The fp64 drop-in on dequantized uint8 data, on the same data with one
+    sample moved off the k / 255 grid at the very end, and with a -0.0 pixel:
+    the oracle's bits every time (also the plugin entry on a row range)."""
+    import paper_2108_13656_b200 as wg
+    from oracle import oracle
+
+    rng = np.random.default_rng(17)
+    x = wg.dequantize_u8(rng.integers(0, 256, (601, 701, 3), dtype=np.uint8))
+    want = oracle.decolor_f64(x)
+    assert np.array_equal(wg.decolor_image(wg.PlanarImage(x)).data, want)
+    y = x.copy()
+    y[-1, -1, 2] = np.nextafter(y[-1, -1, 2], 0.0) if y[-1, -1, 2] > 0 else 1e-300
+    assert np.array_equal(wg.decolor_image(wg.PlanarImage(y)).data, oracle.decolor_f64(y))
+    z = x.copy()
+    z[3, 4] = -0.0
+    gz = wg.decolor_image(wg.PlanarImage(z)).data
+    assert np.array_equal(gz.view(np.uint64), oracle.decolor_f64(z).view(np.uint64))
+    # the plugin entry on a row range of dequantized data
+    from paper_2108_13656_b200 import _kernels_cuda
+
+    out = np.zeros((601, 701))
+    _kernels_cuda.decolor_rows(x, out, 0.55, 0.8, 100, 500)
+    assert np.array_equal(out[100:500], want[100:500]) and not out[:100].any() and not out[500:].any()
+
+
 def test_f64_golden_images():
     import paper_2108_13656_b200 as wg
 
