@@ -398,6 +398,33 @@ def test_hdr_tmem_slot_boundary_vs_oracle(torch_dev, lines_extra, monkeypatch):
     assert torch.equal(wg.hdr_tonemap(rgb), got)
 
 
+def test_hdr_nonfinite_samples_contained(torch_dev):
+    """NaN / inf radiance in one image of a batch: the call completes (every
+    table lookup is clamped inside the table), and the other images' bytes equal
+    their single-image results on every schedule."""
+    import paper_2108_13656_b200 as wg
+    from paper_2108_13656_b200 import synth
+
+    torch, dev = torch_dev
+    rgb = torch.empty((3, 256, 384, 3), dtype=torch.float32, device=dev)
+    synth.fill_hdr_f32(rgb, seed=77)
+    alone = [wg.hdr_tonemap(rgb[i: i + 1].clone()) for i in (0, 2)]
+    rgb[1, 10, 10] = float("nan")
+    rgb[1, 20, 20] = float("inf")
+    rgb[1, 30, 30, 1] = -float("inf")
+    for sched in ("default", "ring", "grouped"):
+        env = {"ring": ("WG_HDR_TMEM", "0"), "grouped": ("WG_HDR_SCHEDULE", "grouped")}.get(sched)
+        if env:
+            os.environ[env[0]] = env[1]
+        try:
+            got = wg.hdr_tonemap(rgb)
+            torch.cuda.synchronize()
+        finally:
+            if env:
+                del os.environ[env[0]]
+        assert torch.equal(got[0:1], alone[0]) and torch.equal(got[2:3], alone[1]), sched
+
+
 def test_hdr_out_validated(torch_dev):
     import paper_2108_13656_b200 as wg
 
