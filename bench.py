@@ -658,6 +658,7 @@ def run_gather(torch, sharder, out, n_total, world, step_into=None, first=0, str
            "note": "sharder.gather_to_root (NCCL gather to rank 0), outside the device-timed metric; "
                    "max over ranks of the wall time"}
     if step_into is not None and out.dtype == torch.uint8:
+        torch.cuda.empty_cache()  # the gather's buffers back to the device for the peer buffer
         try:
             peer = sharder.PeerBuffer(n_total, tuple(out.shape[1:]), out.device.index)
         except Exception as e:  # (no IPC between these processes)
