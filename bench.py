@@ -545,7 +545,13 @@ def main():
     # ---- optional final gather of the gray shards (strong scaling, N > 1): timed apart from the metric
     gather = None
     if scaling == "strong" and world > 1:
-        step_into = (lambda o: wg.decolor(rgb, out=o)) if args.op == "decolor" and wl.output == "gray_u8" else None
+        step_into = None
+        if args.op == "decolor" and wl.output == "gray_u8":
+            from paper_2108_13656_b200 import _lib as wg_lib
+
+            def step_into(ptr, _n=rgb.numel() // 3):  # the C ABI with the root's address as out
+                wg_lib.call("wg_decolor_u8", rgb.data_ptr(), ptr, _n, wg.DEFAULT_PARAMS.beta_r,
+                            wg.DEFAULT_PARAMS.beta_k, stream.cuda_stream)
         gather = run_gather(torch, sharder, out, n_total, world, step_into, first, stream)
     del out, rgb
     torch.cuda.empty_cache()
@@ -664,23 +670,28 @@ def run_gather(torch, sharder, out, n_total, world, step_into=None, first=0, str
         except Exception as e:  # (no IPC between these processes)
             res["fused"] = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
             return res
-        view = peer.view(first, out.shape[0])
-        step_into(view)  # warm (peer mapping, TLB)
-        torch.cuda.synchronize()
-        torch.distributed.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0 = time.perf_counter()
-        e0.record(stream)
-        step_into(view)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        torch.distributed.barrier()
-        wall = time.perf_counter() - t0
-        t = torch.tensor([e0.elapsed_time(e1), wall * 1e3], dtype=torch.float64, device=out.device)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ok = None
-        if torch.distributed.get_rank() == 0:
-            ok = bool(torch.equal(peer.view(first, out.shape[0]), out))  # the root's own shard, same bytes
+        try:
+            ptr = peer.ptr_at(first)
+            step_into(ptr)  # warm (peer mapping, TLB)
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(stream)
+            step_into(ptr)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            wall = time.perf_counter() - t0
+            t = torch.tensor([e0.elapsed_time(e1), wall * 1e3], dtype=torch.float64, device=out.device)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ok = None
+            if torch.distributed.get_rank() == 0:
+                ok = bool(torch.equal(peer.full()[first: first + out.shape[0]], out))  # the root's own shard
+        except Exception as e:
+            peer.close()
+            res["fused"] = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+            return res
         peer.close()
         res["fused"] = {"step_ms": round(float(t[0].item()), 3), "wall_ms": round(float(t[1].item()), 3),
                         "root_shard_equal": ok,

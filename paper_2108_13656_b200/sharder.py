@@ -148,15 +148,28 @@ class PeerBuffer:
         self.ptr = int(ptr.value)
         self._open = True
 
+    def ptr_at(self, first: int) -> int:
+        """Device address of item ``first`` of the root's buffer in this rank's mapping
+        (for the C ABI's ``out`` pointer: the launch's device is the caller's)."""
+        if not 0 <= first <= self.n_items:
+            raise ValueError(f"item {first} outside [0, {self.n_items}]")
+        return self.ptr + first * self.item_elems * self.itemsize
+
     def view(self, first: int, count: int):
-        """Items [first, first + count) of the root's buffer, as a tensor on this rank's device."""
+        """Items [first, first + count) of the root's buffer, as a tensor on this rank's device.
+
+        (torch infers the tensor's device from the pointer; when a peer mapping
+        reports the root's device instead, use :meth:`ptr_at` with the C ABI.)
+        """
         if not (0 <= first and first + count <= self.n_items):
             raise ValueError(f"items [{first}, {first + count}) outside [0, {self.n_items})")
         typestr = "|u1" if self.dtype == "uint8" else "<f4"
-        off = first * self.item_elems * self.itemsize
         with self._torch.cuda.device(self.device):
-            return self._torch.as_tensor(_CudaArray(self.ptr + off, (count, *self.item_shape), typestr),
-                                         device=f"cuda:{self.device}")
+            t = self._torch.as_tensor(_CudaArray(self.ptr_at(first), (count, *self.item_shape), typestr),
+                                      device=f"cuda:{self.device}")
+        if t.device.index != self.device:
+            raise RuntimeError(f"peer view landed on {t.device}, not cuda:{self.device}: use ptr_at()")
+        return t
 
     def full(self):
         """The whole batch (root only)."""

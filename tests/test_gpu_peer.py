@@ -38,8 +38,11 @@ def _worker(rank, world, port, n_total, h, w, result_dir):
     synth.fill_uniform_u8(rgb, seed=3, first_image=first)
     gray = sharder.PeerBuffer(n_total, (h, w), 0)
     toned = sharder.PeerBuffer(n_total, (h, w), 0)
-    wg.decolor(rgb, out=gray.view(first, last - first))
-    wg.decolor_tone(rgb, out=toned.view(first, last - first))
+    wg.decolor(rgb, out=gray.view(first, last - first))  # a tensor view (same device here)
+    from paper_2108_13656_b200 import _lib  # and the raw address through the C ABI (any device)
+
+    _lib.call("wg_decolor_tone_u8", rgb.data_ptr(), toned.ptr_at(first), None, rgb.numel() // 3, 0.55, 0.8, 0.5, 8.0,
+              torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     dist.barrier()
     if rank == 0:
