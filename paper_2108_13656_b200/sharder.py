@@ -142,9 +142,21 @@ class PeerBuffer:
             _lib.call("wg_ipc_alloc", nbytes, self.device, ctypes.byref(ptr), handle)
         box = [bytes(handle)]
         dist.broadcast_object_list(box, src=root, group=group)
+        err = None
         if self.rank != root:
             ctypes.memmove(handle, box[0], 64)
-            _lib.call("wg_ipc_open", handle, self.device, ctypes.byref(ptr))
+            try:
+                _lib.call("wg_ipc_open", handle, self.device, ctypes.byref(ptr))
+            except Exception as e:  # every rank learns of it below (no rank left waiting)
+                err = f"rank {self.rank}: {e}"
+        errs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(errs, err, group=group)
+        if any(errs):
+            if self.rank == root:
+                _lib.call("wg_ipc_free", ptr.value, self.device)
+            elif err is None:
+                _lib.call("wg_ipc_close", ptr.value)
+            raise RuntimeError("peer buffer mapping failed: " + "; ".join(e for e in errs if e))
         self.ptr = int(ptr.value)
         self._open = True
 
