@@ -62,3 +62,46 @@ def test_decolor_into_root_buffer(tmp_path):
     # 5 images over 2 ranks (3 + 2, unequal shards), 4K-wide rows
     mp.spawn(_worker, args=(2, _free_port(), 5, 270, 3840, str(tmp_path)), nprocs=2, join=True)
     assert (tmp_path / "result.txt").read_text() == "ok"
+
+
+def _bench_gather_worker(rank, world, port, result_dir):
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import paper_2108_13656_b200 as wg
+    from paper_2108_13656_b200 import _lib, sharder, synth
+
+    dev = torch.device("cuda", 0)
+    n_total, h, w = 3, 180, 320
+    first, last = sharder.shard_range(n_total, world, rank)
+    rgb = torch.empty((last - first, h, w, 3), dtype=torch.uint8, device=dev)
+    synth.fill_uniform_u8(rgb, seed=9, first_image=first)
+    out = wg.decolor(rgb)
+    stream = torch.cuda.current_stream(dev)
+
+    def step_into(ptr, _n=rgb.numel() // 3):
+        _lib.call("wg_decolor_u8", rgb.data_ptr(), ptr, _n, 0.55, 0.8, stream.cuda_stream)
+
+    res = bench.run_gather(torch, sharder, out, n_total, world, step_into, first, stream)
+    if rank == 0:
+        with open(os.path.join(result_dir, "gather.txt"), "w") as f:
+            f.write(repr(res))
+    dist.destroy_process_group()
+
+
+def test_bench_gather_paths_two_ranks(tmp_path):
+    """bench.run_gather (strong scaling, N > 1): the sharder's gather and the
+    fused peer-buffer launch, with two ranks on one device over gloo -- the
+    fused launch reproduces the root's own shard."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_bench_gather_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    res = eval((tmp_path / "gather.txt").read_text())
+    assert res["gather_ms"] >= 0 and res["fused"]["root_shard_equal"] is True, res
