@@ -903,6 +903,9 @@ __device__ __forceinline__ void tm_tone_slot(uint32_t tslot, const float4* sslot
     }
 }
 
+// kDbg & 4: per-image globaltimer trace (scripts/hdr_trace.py); kRing 3: a third
+// slot in shared memory (A/B only: slower); kPackedGray: the producers' packed
+// f32x2 gray (A/B only: slower, ~40 register moves per quad)
 template <int kCons_, int kDbg = 0, int kRing = 2, bool kPackedGray = false>
 __global__ void __launch_bounds__(kWsT, 1)
     hdr_tm_kernel(const float* __restrict__ rgb, uint8_t* __restrict__ out, float2* __restrict__ parts,
@@ -1028,10 +1031,8 @@ __global__ void __launch_bounds__(kWsT, 1)
                 lo1 = min(min(min(lo1, __float_as_uint(a.x) - 1u), min(__float_as_uint(a.y) - 1u, __float_as_uint(b.x) - 1u)),
                           __float_as_uint(b.y) - 1u);
                 hi = fmaxf(fmaxf(fmaxf(hi, a.x), fmaxf(a.y, b.x)), b.y);
-                if ((kDbg & 3) != 3) {
-                    if (slot < 2) tm_st4(ts + 4u * (u >> 7), a.x, a.y, b.x, b.y);
-                    else if (u < nq32) s_slot[u] = make_float4(a.x, a.y, b.x, b.y);
-                }
+                if (slot < 2) tm_st4(ts + 4u * (u >> 7), a.x, a.y, b.x, b.y);
+                else if (u < nq32) s_slot[u] = make_float4(a.x, a.y, b.x, b.y);
             };
             // warp-uniform trip count (tcgen05.st is .aligned)
             for (uint32_t u = tid;;) {
@@ -1118,8 +1119,7 @@ __global__ void __launch_bounds__(kWsT, 1)
             const uint32_t ts = tbase + static_cast<uint32_t>(slot * kTmSlotCols);
             const float4* ss = slot < 2 ? nullptr : s_slot;
             uint8_t* o = out + i * ppi + mp.quad(0) * 4;
-            if ((kDbg & 3) == 1 || (kDbg & 3) == 3) {
-            } else if (st.mode == 1 && st.lut) {
+            if (st.mode == 1 && st.lut) {
                 const float inv = st.inv_gmin;
                 tm_tone_slot<kCons_, true>(ts, ss, o, nq, cw, lane,
                                            [&](float v) -> uint32_t { return lut_step_sum(v, inv, s_lut); });
