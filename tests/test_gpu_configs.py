@@ -9,6 +9,7 @@ max-abs <= 1e-6. Input sha256s and seeds are printed (pytest -s) for the log.
 """
 
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -61,6 +62,30 @@ def test_c4_all_images():
         bad += int(round(frac * want.size))
         total += want.size
     assert bad <= U8_MAX_FRAC * total
+
+
+def test_c4_full_batch_scale_invariance():
+    """A size-independent property at the full C4 size (32 x 2048^2): the HDR
+    adapter depends on radiance only through g / gmin, and the fp32 gray is
+    exactly homogeneous under power-of-two scales (every rounding scales with
+    the operands; the roots see powers of four), so x * 4 and x / 8 must give
+    the very same bytes -- on the tensor-memory kernel and the grouped schedule."""
+    import torch
+
+    import paper_2108_13656_b200 as wg
+    from paper_2108_13656_b200 import synth
+
+    wl = synth.WORKLOADS["C4"]
+    rgb = torch.empty((wl.n_images, wl.height, wl.width, 3), dtype=torch.float32, device="cuda")
+    synth.fill_hdr_f32(rgb, seed=0, first_image=0)
+    base = wg.hdr_tonemap(rgb)
+    assert torch.equal(wg.hdr_tonemap(rgb * 4.0), base)
+    assert torch.equal(wg.hdr_tonemap(rgb * 0.125), base)
+    os.environ["WG_HDR_SCHEDULE"] = "grouped"
+    try:
+        assert torch.equal(wg.hdr_tonemap(rgb * 4.0), base)
+    finally:
+        del os.environ["WG_HDR_SCHEDULE"]
 
 
 def test_c5_shard_edges():
